@@ -1,0 +1,208 @@
+/*
+ * specdec_b200 -- C ABI of the B200-native EAGLE tree-verification hot path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * (passed as void*), enqueues work on that stream and returns without a host
+ * synchronisation.  No torch types cross this boundary.  Return value: 0 on
+ * success, a negative SDB_E* code on bad arguments (nothing is enqueued then);
+ * data errors found on the device (invalid parent index, NaN logits, invalid
+ * distribution) are reported through the caller-provided int32 `err` words.
+ *
+ * Each function names the reference interface it replaces
+ * (/root/reference/pkg/src/specdec/<file>:<line>).  The Python host mirror
+ * (paper_2508_08192_b200/) keeps the reference's names and error behaviour
+ * on top of these calls; INTEGRATION.md shows the ctypes binding.
+ *
+ * Layout conventions
+ *   tree rows   : "augmented" order -- row 0 is the root (last committed
+ *                 token), row 1+i is draft node i (engine.py:170-173); any
+ *                 parent array with parent[i] in {-1} U [0, i) is accepted.
+ *   mask words  : uint32 [B][R][n_words], bit j of row i = row i sees row j
+ *                 (LSB = row 0) -- the ancestor-or-self closure.
+ *   KV pages    : bf16 [num_blocks][n_kv_heads][block_size][head_dim], one
+ *                 pool per layer; block_table int32 [B][max_blocks].
+ *   LSE         : natural log, fp32 [B][Hq][R] (reference PartialAttention.lse).
+ */
+#ifndef SPECDEC_B200_H
+#define SPECDEC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDB_OK 0
+#define SDB_E_INVALID (-1)     /* bad shape / null pointer / unsupported size   */
+#define SDB_E_UNSUPPORTED (-2) /* dtype or head_dim not supported by a kernel   */
+#define SDB_E_WORKSPACE (-3)   /* workspace too small                           */
+#define SDB_E_CUDA (-4)        /* a CUDA launch failed (see sdb_last_cuda_error) */
+
+/* device-side error bits written into `err` words */
+#define SDB_ERR_BAD_PARENT 1      /* TreeError: parent must precede node (drafttree.py:31-34) */
+#define SDB_ERR_NAN 2             /* ValueError: NaN in logits (numcore.py:47-48)             */
+#define SDB_ERR_BAD_DIST 4        /* SamplingError: dist not >= 0 / sum != 1 (sampling.py:47) */
+#define SDB_ERR_UNIFORMS 8        /* SamplingError: uniform stream exhausted (sampling.py:179) */
+#define SDB_ERR_ALL_MASKED 16     /* AttentionError: row masked in every part (attention.py:117) */
+#define SDB_ERR_NO_ALLOWED 32     /* SamplingError: no token allowed (sampling.py:96-97)       */
+
+#define SDB_DTYPE_BF16 0
+#define SDB_DTYPE_F32 1
+#define SDB_DTYPE_F64 2
+
+int sdb_version(void);
+const char *sdb_strerror(int code);
+const char *sdb_last_cuda_error(void);
+
+/* ---- K0: tree mask, depth and positions -------------------------------
+ * Replaces TreeSpec.__post_init__ depth + validation (drafttree.py:26-35),
+ * suffix_mask (drafttree.py:102-111) and the row positions
+ * L-2+depth_aug (engine.py:456) / ctx+depth-1 (attention.py:142).
+ * parent int32 [B][r_max]; n_rows int32 [B]; ctx_len int32 [B] (may be NULL
+ * -> 0).  Outputs mask_words uint32 [B][r_max][n_words], positions int32
+ * [B][r_max] (= ctx + depth - 1), depth int32 [B][r_max]; err int32 [B]
+ * gets SDB_ERR_BAD_PARENT for an invalid sequence.  Rows >= n_rows are 0. */
+int sdb_tree_build(const int32_t *parent, const int32_t *n_rows, const int32_t *ctx_len,
+                   int batch, int r_max, int n_words, uint32_t *mask_words,
+                   int32_t *positions, int32_t *depth, int32_t *err, void *stream);
+
+/* ---- drop-in attention core (float64, reference precision) ------------
+ * Replaces kernels.attend_heads -> _attend_numpy / _attend_numba
+ * (kernels.py:40-92, 195-203).  q [heads][m][d], k/v [heads][n][d],
+ * mask uint8 [m][n] or NULL (all visible).  out [heads][m][d], lse
+ * [heads][m]; fully masked rows give out 0 and lse -inf. */
+int sdb_attend_heads_f64(const double *q, const double *k, const double *v,
+                         const uint8_t *mask, int heads, int m, int n, int head_dim,
+                         double scale, double *out, double *lse, void *stream);
+
+/* Replaces attention.merge_partials (attention.py:108-124).  outs
+ * [parts][heads][m][d], lses [parts][heads][m] -> out [heads][m][d], lse
+ * [heads][m]; a row masked in every part sets SDB_ERR_ALL_MASKED in err[0]. */
+int sdb_merge_partials_f64(const double *outs, const double *lses, int parts, int heads,
+                           int m, int head_dim, double *out, double *lse, int32_t *err,
+                           void *stream);
+
+/* ---- K1-K3: batched paged GQA tree-verify attention -------------------
+ * Replaces, per layer, the attention block of model.forward
+ * (model.py:252-272): cache.gather (kvstore.py:235-246) +
+ * attend(CausalPrefix) + attend(TreeSuffix(mask)) + merge_attentions
+ * (attention.py:92-128), i.e. tree_attention (attention.py:131-151) with
+ * GQA (q head h reads kv head h / (hq/hkv)). */
+typedef struct sdb_tree_attn_args {
+  const void *q;              /* [B][r_max][hq][head_dim]  (dtype)           */
+  const void *k_cache;        /* [num_blocks][hkv][block_size][head_dim]     */
+  const void *v_cache;
+  const int32_t *block_table; /* [B][max_blocks]                             */
+  const int32_t *ctx_len;     /* [B] committed rows C = L-1 in the cache      */
+  const void *tree_k;         /* [B][r_max][hkv][head_dim] fresh tree K/V     */
+  const void *tree_v;
+  const uint32_t *mask_words; /* [B][r_max][n_words] from sdb_tree_build      */
+  const int32_t *n_rows;      /* [B] valid tree rows (<= r_max)               */
+  void *out;                  /* [B][r_max][hq][head_dim] (dtype)             */
+  float *lse;                 /* [B][hq][r_max] natural log, may be NULL      */
+  void *workspace;            /* split-KV partials, see sdb_tree_attn_workspace */
+  int64_t workspace_bytes;
+  int batch, r_max, n_words, hq, hkv, head_dim;
+  int block_size, num_blocks, max_blocks;
+  int max_ctx;                /* upper bound of ctx_len (host-known), sizes the grid */
+  float scale;
+  int dtype;                  /* SDB_DTYPE_BF16 (tcgen05 path) or SDB_DTYPE_F32 */
+  int num_splits;             /* 0 = auto                                     */
+  int kernel;                 /* 0 = auto, 1 = tcgen05 (sm_100a), 2 = SIMT    */
+} sdb_tree_attn_args;
+
+int64_t sdb_tree_attn_workspace(const sdb_tree_attn_args *a);
+int sdb_tree_attn(const sdb_tree_attn_args *a, void *stream);
+
+/* ---- K4/K5: greedy (T = 0) acceptance ----------------------------------
+ * Replaces target_dist(row, 0, top_p) (sampling.py:87-102, numcore.py:51-55)
+ * for every tree row + mss_verify (sampling.py:149-202) at temperature 0,
+ * which is exactly the argmax walk.
+ *
+ * Step 1 (vocab-shardable): per-row packed argmax keys over this rank's
+ * vocab slice [vocab_offset, vocab_offset + vocab): int64 key =
+ * (int32(orderable(max)) << 32) | (0xFFFFFFFF - global_index) -- signed int64
+ * MAX over ranks (NCCL/torch all_reduce MAX) yields the global argmax with the
+ * lowest index on ties.  logits [rows][row_stride] of dtype f32 or bf16. */
+int sdb_argmax_keys(const void *logits, int dtype, int64_t rows, int vocab, int64_t row_stride,
+                    int64_t vocab_offset, int64_t *keys, int32_t *err, void *stream);
+
+/* Step 2: the tree walk on global keys.  parent/tokens int32 [B][r_max]
+ * (tokens[b][1+i] = draft token of node i; row 0 unused), keys int64
+ * [B][r_max].  Outputs path int32 [B][r_max] (draft-node indices, the
+ * reference accepted_path), path_len int32 [B], next_token int64 [B],
+ * uniforms_used int32 [B] (= candidates examined + 1, as mss_verify counts). */
+int sdb_greedy_walk(const int64_t *keys, const int32_t *parent, const int32_t *n_rows,
+                    const int32_t *tokens, int batch, int r_max, int32_t *path,
+                    int32_t *path_len, int64_t *next_token, int32_t *uniforms_used,
+                    void *stream);
+
+/* Steps 1+2 fused in one launch (single GPU, unsharded vocab). */
+int sdb_accept_greedy(const void *logits, int dtype, int batch, int r_max, int vocab,
+                      int64_t row_stride, const int32_t *parent, const int32_t *n_rows,
+                      const int32_t *tokens, int64_t *keys, int32_t *path, int32_t *path_len,
+                      int64_t *next_token, int32_t *uniforms_used, int32_t *err,
+                      void *stream);
+
+/* ---- K4/K5: stochastic (T > 0) acceptance ------------------------------
+ * Replaces target_dist(row, T, top_p) for every tree row, the draft q
+ * target_dist(draft_row, T, 1.0) (engine.py:266-269; siblings share their
+ * parent's q, engine.py:405-407) and mss_verify (sampling.py:149-202) with
+ * uniforms[b][0..] (rank_sliced_uniforms row, engine.py:251-254, 498-503).
+ * target/draft logits fp32 [B][r_max][vocab]; uniforms f64 [B][n_uniforms].
+ * residual (optional, f32 [B][vocab]) receives the distribution the bonus
+ * token was drawn from (MssResult.residual). */
+int64_t sdb_accept_stochastic_workspace(int batch, int r_max, int vocab);
+int sdb_accept_stochastic(const float *target_logits, const float *draft_logits, int batch,
+                          int r_max, int vocab, float temperature, float top_p,
+                          const int32_t *parent, const int32_t *n_rows, const int32_t *tokens,
+                          const double *uniforms, int n_uniforms, void *workspace,
+                          int64_t workspace_bytes, int32_t *path, int32_t *path_len,
+                          int64_t *next_token, int32_t *uniforms_used, float *residual,
+                          int32_t *err, void *stream);
+
+/* ---- drop-in sampling ops (float64, reference precision) ---------------
+ * target_dist (sampling.py:87-102): logits f64 [rows][vocab] -> dist f64,
+ * allowed uint8 [rows][vocab] or NULL (guided-decoding mask, applied first). */
+int sdb_target_dist_f64(const double *logits, const uint8_t *allowed, int64_t rows, int vocab,
+                        double temperature, double top_p, double *dist, int32_t *err,
+                        void *stream);
+
+/* mss_verify on explicit distributions (sampling.py:149-202): parent int32
+ * [n] (non-augmented draft tree, ROOT = -1), tokens int32 [n], node_dists f64
+ * [n][vocab], target_dists f64 [n+1][vocab], uniforms f64 [n_uniforms].
+ * out_path int32 [n], out_scalars int64 [3] = {path_len, next_token,
+ * uniforms_used}, residual f64 [vocab]. */
+int sdb_mss_verify_f64(const int32_t *parent, const int32_t *tokens, int n_nodes, int vocab,
+                       const double *node_dists, const double *target_dists,
+                       const double *uniforms, int n_uniforms, int32_t *out_path,
+                       int64_t *out_scalars, double *residual, int32_t *err, void *stream);
+
+/* ---- K7: KV write-back ---------------------------------------------------
+ * Replaces the bookkeeping write-back (engine.py:504-523): for every layer
+ * and sequence, tree rows [0] + [1 + a for a in path[:n_keep-1]] are written
+ * to positions ctx_len[b] .. of the sequence's pages
+ * (PagedKvCache.write / compact_accepted, kvstore.py:217-233).
+ * tree_k/v: bf16 [n_layers][B][r_max][hkv][head_dim]; caches: per layer
+ * pool, layer stride layer_stride elements.  n_keep int32 [B] may be NULL
+ * (-> path_len + 1). */
+int sdb_compact_kv(const void *tree_k, const void *tree_v, void *k_cache, void *v_cache,
+                   int64_t cache_layer_stride, const int32_t *block_table, int max_blocks,
+                   const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
+                   const int32_t *n_keep, int n_layers, int batch, int r_max, int hkv,
+                   int head_dim, int block_size, int elem_bytes, void *stream);
+
+/* Generic row scatter / gather on one sequence's pages (PagedKvCache.write /
+ * gather, kvstore.py:217-225, 235-246): rows [n][hkv*head_dim] <-> pages at
+ * positions start.. .  elem_bytes 2, 4 or 8. */
+int sdb_paged_write(void *pool, const int32_t *block_table, int64_t start, const void *rows,
+                    int64_t n, int hkv, int head_dim, int block_size, int elem_bytes,
+                    void *stream);
+int sdb_paged_gather(const void *pool, const int32_t *block_table, int64_t start, void *rows,
+                     int64_t n, int hkv, int head_dim, int block_size, int elem_bytes,
+                     void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECDEC_B200_H */

@@ -1,0 +1,123 @@
+// K7: paged KV write-back of the accepted path, plus the generic per-sequence
+// row scatter/gather of PagedKvCache.
+//
+// Reference: engine.py:504-523 (rows = [0] + [1+a for a in path[:n_keep-1]]
+// written at L-1 = ctx_len for every layer), PagedKvCache.write / gather /
+// compact_accepted (kvstore.py:207-246).  Device page layout
+// [num_blocks][hkv][block_size][head_dim]: one (page, head) slab per row of
+// head_dim elements, so every copy here is a 16-byte-vectorised memcpy of
+// head_dim*elem_bytes per (row, head).
+#include "sdb_common.cuh"
+
+namespace sdb {
+
+// One CTA per (row slot, sequence, layer); threads stride over hkv*head_dim
+// in 16-byte chunks, K and V in the same pass.
+__global__ void compact_kv_kernel(const uint8_t *__restrict__ tree_k, const uint8_t *__restrict__ tree_v,
+                                  uint8_t *__restrict__ k_cache, uint8_t *__restrict__ v_cache,
+                                  int64_t layer_stride_bytes, const int32_t *__restrict__ block_table,
+                                  int max_blocks, const int32_t *__restrict__ ctx_len,
+                                  const int32_t *__restrict__ path, const int32_t *__restrict__ path_len,
+                                  const int32_t *__restrict__ n_keep, int batch, int r_max, int hkv,
+                                  int row_bytes, int block_size) {
+  const int slot = blockIdx.x, b = blockIdx.y, layer = blockIdx.z;
+  int len = path_len[b];
+  int keep = n_keep ? n_keep[b] : len + 1;
+  int n_write = min(keep - 1, len) + 1;  // root + write_path
+  if (slot >= n_write) return;
+  int row = slot == 0 ? 0 : 1 + path[(int64_t)b * r_max + slot - 1];
+  int64_t pos = (int64_t)ctx_len[b] + slot;
+  int page = block_table[(int64_t)b * max_blocks + pos / block_size];
+  int off = (int)(pos % block_size);
+  const int64_t src_row = (((int64_t)layer * batch + b) * r_max + row) * hkv;  // in units of head rows
+  const int chunks = row_bytes / 16;
+  for (int idx = threadIdx.x; idx < hkv * chunks; idx += blockDim.x) {
+    int h = idx / chunks, c = idx % chunks;
+    int64_t src = (src_row + h) * row_bytes + (int64_t)c * 16;
+    int64_t dst = layer * layer_stride_bytes + ((((int64_t)page * hkv + h) * block_size + off) * row_bytes) +
+                  (int64_t)c * 16;
+    *reinterpret_cast<int4 *>(k_cache + dst) = *reinterpret_cast<const int4 *>(tree_k + src);
+    *reinterpret_cast<int4 *>(v_cache + dst) = *reinterpret_cast<const int4 *>(tree_v + src);
+  }
+}
+
+template <bool kWrite>
+__global__ void paged_rows_kernel(uint8_t *__restrict__ pool, const int32_t *__restrict__ block_table,
+                                  int64_t start, uint8_t *__restrict__ rows, int64_t n, int hkv,
+                                  int row_bytes, int block_size) {
+  const int chunks = row_bytes / 16;
+  const int64_t total = n * hkv * chunks;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = idx / (hkv * chunks);
+    int rem = (int)(idx % (hkv * chunks));
+    int h = rem / chunks, c = rem % chunks;
+    int64_t pos = start + r;
+    int page = block_table[pos / block_size];
+    int off = (int)(pos % block_size);
+    int64_t pidx = (((int64_t)page * hkv + h) * block_size + off) * row_bytes + (int64_t)c * 16;
+    int64_t ridx = (r * hkv + h) * row_bytes + (int64_t)c * 16;
+    if (kWrite)
+      *reinterpret_cast<int4 *>(pool + pidx) = *reinterpret_cast<const int4 *>(rows + ridx);
+    else
+      *reinterpret_cast<int4 *>(rows + ridx) = *reinterpret_cast<const int4 *>(pool + pidx);
+  }
+}
+
+}  // namespace sdb
+
+extern "C" int sdb_compact_kv(const void *tree_k, const void *tree_v, void *k_cache, void *v_cache,
+                              int64_t cache_layer_stride, const int32_t *block_table, int max_blocks,
+                              const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
+                              const int32_t *n_keep, int n_layers, int batch, int r_max, int hkv,
+                              int head_dim, int block_size, int elem_bytes, void *stream) {
+  if (!tree_k || !tree_v || !k_cache || !v_cache || !block_table || !ctx_len || !path || !path_len)
+    return SDB_E_INVALID;
+  if (n_layers < 1 || batch < 0 || r_max < 1 || hkv < 1 || head_dim < 1 || block_size < 1)
+    return SDB_E_INVALID;
+  int row_bytes = head_dim * elem_bytes;
+  if (row_bytes % 16 != 0) return SDB_E_UNSUPPORTED;
+  if (batch == 0) return SDB_OK;
+  dim3 grid(r_max, batch, n_layers);
+  int threads = min(256, max(32, hkv * (row_bytes / 16)));
+  threads = (threads + 31) / 32 * 32;
+  sdb::compact_kv_kernel<<<grid, threads, 0, sdb::as_stream(stream)>>>(
+      (const uint8_t *)tree_k, (const uint8_t *)tree_v, (uint8_t *)k_cache, (uint8_t *)v_cache,
+      cache_layer_stride * elem_bytes, block_table, max_blocks, ctx_len, path, path_len, n_keep, batch, r_max,
+      hkv, row_bytes, block_size);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+static int paged_rows(bool write, void *pool, const int32_t *block_table, int64_t start, void *rows, int64_t n,
+                      int hkv, int head_dim, int block_size, int elem_bytes, void *stream) {
+  if (!pool || !block_table || !rows || n < 0 || start < 0 || hkv < 1 || head_dim < 1 || block_size < 1)
+    return SDB_E_INVALID;
+  int row_bytes = head_dim * elem_bytes;
+  if (row_bytes % 16 != 0) return SDB_E_UNSUPPORTED;
+  if (n == 0) return SDB_OK;
+  int64_t total = n * hkv * (row_bytes / 16);
+  int threads = 256;
+  int blocks = (int)std::min<int64_t>(sdb::cdiv64(total, threads), 4096);
+  if (write)
+    sdb::paged_rows_kernel<true><<<blocks, threads, 0, sdb::as_stream(stream)>>>(
+        (uint8_t *)pool, block_table, start, (uint8_t *)rows, n, hkv, row_bytes, block_size);
+  else
+    sdb::paged_rows_kernel<false><<<blocks, threads, 0, sdb::as_stream(stream)>>>(
+        (uint8_t *)pool, block_table, start, (uint8_t *)rows, n, hkv, row_bytes, block_size);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+extern "C" int sdb_paged_write(void *pool, const int32_t *block_table, int64_t start, const void *rows,
+                               int64_t n, int hkv, int head_dim, int block_size, int elem_bytes, void *stream) {
+  return paged_rows(true, pool, block_table, start, const_cast<void *>(rows), n, hkv, head_dim, block_size,
+                    elem_bytes, stream);
+}
+
+extern "C" int sdb_paged_gather(const void *pool, const int32_t *block_table, int64_t start, void *rows,
+                                int64_t n, int hkv, int head_dim, int block_size, int elem_bytes,
+                                void *stream) {
+  return paged_rows(false, const_cast<void *>(pool), block_table, start, rows, n, hkv, head_dim, block_size,
+                    elem_bytes, stream);
+}

@@ -1,0 +1,122 @@
+"""The batched tree-verification step on one GPU (or one KV-head shard).
+
+One step = what Engine.validate_stage + the sample/bookkeep stages do per
+round for the whole batch on one attention layer (engine.py:447-523):
+
+  1. tree_build      -- ancestor mask words / positions from the parent arrays
+  2. tree attention  -- prefix over the paged KV + masked suffix + LSE merge
+  3. acceptance      -- greedy (T = 0) or stochastic (T > 0) over the logits
+  4. compact_kv      -- accepted rows' K/V into the sequence's pages
+
+All four are device launches on the caller's stream with no host sync, so
+the step can be captured into a CUDA graph (``capture``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _lib
+from .attention import TreeVerifyAttention
+from .drafttree import n_words
+from .kvstore import compact_kv
+from .sampling import GreedyAcceptor, StochasticAcceptor
+
+
+@dataclass
+class StepInputs:
+    parent: "object"       # int32 [B, R] augmented parents
+    n_rows: "object"       # int32 [B]
+    ctx_len: "object"      # int32 [B] committed rows in cache (L - 1)
+    tokens: "object"       # int32 [B, R] row tokens (row 0 = root)
+    q: "object"            # [B, R, Hq, d]
+    tree_k: "object"       # [B, R, Hkv, d]
+    tree_v: "object"
+    logits: "object"       # [B, R, V] target logits (vocab shard)
+    k_pool: "object"       # [num_blocks, Hkv, bs, d] (one layer)
+    v_pool: "object"
+    block_table: "object"  # int32 [B, max_blocks]
+    draft_logits: "object" = None  # [B, R, V] for stochastic acceptance
+    uniforms: "object" = None      # float64 [B, n_uniforms]
+
+
+class TreeVerifier:
+    def __init__(self, scale, temperature=0.0, top_p=1.0, max_ctx=None, num_splits=0, kernel=0):
+        self.scale = scale
+        self.temperature = temperature
+        self.top_p = top_p
+        self.max_ctx = max_ctx
+        self.num_splits = num_splits
+        self.kernel = kernel
+        self.attn = TreeVerifyAttention()
+        self.greedy = GreedyAcceptor()
+        self.stochastic = StochasticAcceptor()
+        self._out = None
+        self.graph = None
+
+    def _buffers(self, x: StepInputs):
+        import torch
+
+        b, r, hq, d = x.q.shape
+        key = (b, r, hq, d, x.q.dtype, str(x.q.device))
+        if self._out is None or self._out[0] != key:
+            dev = x.q.device
+            w = n_words(r)
+            self._out = (key, dict(
+                mask=torch.empty((b, r, w), dtype=torch.int32, device=dev),
+                pos=torch.empty((b, r), dtype=torch.int32, device=dev),
+                depth=torch.empty((b, r), dtype=torch.int32, device=dev),
+                tree_err=torch.empty((b,), dtype=torch.int32, device=dev),
+                out=torch.empty_like(x.q),
+                lse=torch.empty((b, hq, r), dtype=torch.float32, device=dev)))
+        return self._out[1]
+
+    def step(self, x: StepInputs, stream=None, compact=True):
+        o = self._buffers(x)
+        b, r = x.parent.shape
+        lib = _lib.lib()
+        rc = lib.sdb_tree_build(_lib.ptr(x.parent), _lib.ptr(x.n_rows), _lib.ptr(x.ctx_len), b, r,
+                                o["mask"].shape[-1], _lib.ptr(o["mask"]), _lib.ptr(o["pos"]), _lib.ptr(o["depth"]),
+                                _lib.ptr(o["tree_err"]), _lib.stream_ptr(stream))
+        _lib.check(rc, "tree_build")
+        self.attn(x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
+                  self.scale, out=o["out"], lse=o["lse"], max_ctx=self.max_ctx, num_splits=self.num_splits,
+                  kernel=self.kernel, stream=stream)
+        if self.temperature == 0:
+            acc = self.greedy(x.logits, x.parent, x.n_rows, x.tokens, stream=stream)
+        else:
+            acc = self.stochastic(x.logits, x.draft_logits, self.temperature, self.top_p, x.parent, x.n_rows,
+                                  x.tokens, x.uniforms, stream=stream)
+        if compact:
+            compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0), x.v_pool.unsqueeze(0),
+                       x.block_table, x.ctx_len, acc.path, acc.path_len, None, stream=stream)
+        return o["out"], o["lse"], acc, o["tree_err"]
+
+    # kernel launches per step (for the bench's gpu_launches claim)
+    def launches_per_step(self, x: StepInputs):
+        n_attn = 1
+        a = self.attn
+        return 1 + n_attn + (1 if self._needs_combine else 0) + 2 + 1
+
+    _needs_combine = True
+
+    def capture(self, x: StepInputs, warmup=2):
+        """Capture one step into a CUDA graph; replay with ``replay()``."""
+        import torch
+
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.step(x, stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            res = self.step(x, stream=torch.cuda.current_stream())
+        self.graph = g
+        self.graph_outputs = res
+        return res
+
+    def replay(self):
+        self.graph.replay()
+        return self.graph_outputs

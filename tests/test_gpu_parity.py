@@ -1,0 +1,469 @@
+"""GPU parity: the CUDA path vs the reference's golden outputs and the CPU
+oracle, through the package API (which calls the C ABI).  Needs a B200."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import specdec_oracle as O  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib_loaded():
+    from paper_2508_08192_b200 import _lib
+
+    _lib.load()
+
+
+def _cuda(x, dtype):
+    return torch.as_tensor(np.ascontiguousarray(x)).to(device="cuda", dtype=dtype)
+
+
+# ---------------------------------------------------------------------------
+# K0 tree build
+# ---------------------------------------------------------------------------
+
+def test_tree_build_matches_reference(golden):
+    from paper_2508_08192_b200.drafttree import tree_build
+
+    g = golden("trees")
+    par = _cuda(g["parent_aug"], torch.int32)
+    nr = _cuda(g["n_rows"], torch.int32)
+    ctx = _cuda(g["ctx"], torch.int32)
+    mask, pos, depth, err = tree_build(par, nr, ctx)
+    torch.cuda.synchronize()
+    assert int(err.abs().sum()) == 0
+    mask, pos, depth = mask.cpu().numpy(), pos.cpu().numpy(), depth.cpu().numpy()
+    for i in range(len(g["n_rows"])):
+        n = int(g["n_rows"][i])
+        want = O.mask_words(g["mask"][i, :n, :n], mask.shape[-1])
+        np.testing.assert_array_equal(mask[i, :n].astype(np.uint32), want)
+        np.testing.assert_array_equal(depth[i, :n], g["depth"][i, :n])
+        np.testing.assert_array_equal(pos[i, :n], g["pos"][i, :n])
+        assert not mask[i, n:].any()
+
+
+def test_tree_build_rejects_bad_parents(golden):
+    from paper_2508_08192_b200.drafttree import tree_build
+
+    g = golden("trees")
+    mask, pos, depth, err = tree_build(_cuda(g["bad_parent"], torch.int32), _cuda(g["bad_len"], torch.int32))
+    err = err.cpu().numpy()
+    np.testing.assert_array_equal(err == 0, g["bad_valid"])
+
+
+def test_suffix_mask_drop_in_known_answers():
+    from paper_2508_08192_b200 import drafttree as D
+
+    t = D.augment(D.parse_tree("full:2,2"))
+    m = D.suffix_mask(t)
+    assert list(O.mask_words(m)[:, 0]) == [1, 3, 5, 11, 19, 37, 69]
+    with pytest.raises(D.TreeError):
+        D.TreeSpec((-1, 2, 1))
+    # reference tests/test_drafttree.py:53-61
+    t = D.parse_tree("full:2,2")
+    m = D.suffix_mask(t)
+    for i in range(t.n_nodes):
+        expect = np.zeros(t.n_nodes, dtype=bool)
+        expect[t.ancestors_or_self(i)] = True
+        np.testing.assert_array_equal(m[i], expect)
+    assert not np.triu(m, 1).any()
+
+
+# ---------------------------------------------------------------------------
+# drop-in float64 attention (reference tolerances)
+# ---------------------------------------------------------------------------
+
+def _softmax_ref(q, k, v, mask, scale):
+    s = (q @ k.T) * scale
+    if mask is not None:
+        s = np.where(mask, s, -np.inf)
+    s = s - s.max(axis=1, keepdims=True)
+    p = np.exp(s)
+    p /= p.sum(axis=1, keepdims=True)
+    return p @ v
+
+
+def test_attend_reference_cases():
+    from paper_2508_08192_b200.attention import (AttentionError, CausalPrefix, LocalChunk, TreeSuffix, attend,
+                                                 merge_attentions, merge_partials)
+
+    # tests/test_attention.py:22-85 of the reference, same tolerances
+    rng = np.random.default_rng(0)
+    q, k, v = (rng.normal(size=(3, 8)) for _ in range(3))
+    np.testing.assert_allclose(attend(q, k, v, CausalPrefix(3), 0.5).out, _softmax_ref(q, k, v, None, 0.5),
+                               atol=1e-12)
+    rng = np.random.default_rng(1)
+    q1 = rng.normal(size=(1, 4))
+    k1, v1 = rng.normal(size=(6, 4)), rng.normal(size=(6, 4))
+    mask = np.zeros((1, 6), dtype=bool)
+    mask[0, 4:6] = True
+    np.testing.assert_allclose(attend(q1, k1, v1, LocalChunk(4, (5,), tuple(range(6))), 1.0).out,
+                               _softmax_ref(q1, k1, v1, mask, 1.0), atol=1e-12)
+    part = attend(np.ones((2, 4)), np.zeros((0, 4)), np.zeros((0, 4)), CausalPrefix(0), 1.0)
+    assert part.masked_rows.all()
+    rng = np.random.default_rng(2)
+    q = rng.normal(size=(4, 8))
+    k, v = rng.normal(size=(10, 8)), rng.normal(size=(10, 8))
+    for cut in (1, 3, 7, 9):
+        a = attend(q, k[:cut], v[:cut], CausalPrefix(cut), 0.3)
+        b = attend(q, k[cut:], v[cut:], CausalPrefix(10 - cut), 0.3)
+        np.testing.assert_allclose(merge_attentions([a, b]), attend(q, k, v, CausalPrefix(10), 0.3).out, atol=1e-10)
+    rng = np.random.default_rng(3)
+    q = rng.normal(size=(2, 8))
+    k, v = rng.normal(size=(6, 8)), rng.normal(size=(6, 8))
+    a = attend(q, k[:2], v[:2], CausalPrefix(2), 1.0, n_heads=2)
+    b = attend(q, k[2:], v[2:], CausalPrefix(4), 1.0, n_heads=2)
+    np.testing.assert_allclose(merge_attentions([a, b], n_heads=2),
+                               attend(q, k, v, CausalPrefix(6), 1.0, n_heads=2).out, atol=1e-10)
+    empty = attend(np.ones((1, 4)), np.zeros((0, 4)), np.zeros((0, 4)), CausalPrefix(0), 1.0)
+    with pytest.raises(AttentionError):
+        merge_partials([empty, empty])
+    with pytest.raises(AttentionError):
+        attend(np.ones((2, 4)), np.ones((3, 4)), np.ones((3, 4)), TreeSuffix(np.ones((2, 2), dtype=bool)), 1.0)
+
+
+def test_attend_merge_golden(golden):
+    from paper_2508_08192_b200.attention import CausalPrefix, TreeSuffix, attend, merge_partials
+
+    g = golden("attend_merge")
+    q, k, v = g["q"], g["k"], g["v"]
+    a = attend(q, k[:3], v[:3], CausalPrefix(3), 0.3, n_heads=2)
+    b = attend(q, k[3:], v[3:], CausalPrefix(7), 0.3, n_heads=2)
+    np.testing.assert_allclose(a.out, g["a_out"], atol=1e-13)
+    np.testing.assert_allclose(b.lse, g["b_lse"], atol=1e-13)
+    m = merge_partials([a, b], n_heads=2)
+    np.testing.assert_allclose(m.out, g["m_out"], atol=1e-13)
+    np.testing.assert_allclose(m.lse, g["m_lse"], atol=1e-13)
+    c = attend(q, k, v, TreeSuffix(g["mask"]), 0.3, n_heads=2)
+    np.testing.assert_allclose(c.out, g["c_out"], atol=1e-13)
+    np.testing.assert_array_equal(np.isinf(c.lse), np.isinf(g["c_lse"]))
+
+
+def test_tree_attention_f64_golden(golden):
+    from paper_2508_08192_b200.attention import tree_attention
+    from paper_2508_08192_b200.drafttree import TreeSpec
+
+    g = golden("attention_f64")
+    for ci in range(int(g["n_cases"])):
+        p = f"c{ci}_"
+        nh, hd, ctx, chunk = (int(x) for x in g[p + "meta"])
+        tree = TreeSpec(tuple(int(x) for x in g[p + "parent"]))
+        out = tree_attention(g[p + "q"], g[p + "ck"], g[p + "cv"], g[p + "tk"], g[p + "tv"], tree, hd ** -0.5,
+                             n_heads=nh, chunk_len=None if chunk < 0 else chunk)
+        # reference suite threshold is 1e-5 (verify.py:284); float64 gives far better
+        np.testing.assert_allclose(out, g[p + "out"], atol=1e-12, rtol=0)
+
+
+def test_tree_attention_vs_naive_randomized():
+    # reference tests/test_attention.py:88-111 through the device path
+    from paper_2508_08192_b200.attention import explicit_tree_mask, naive_tree_attention, tree_attention
+    from paper_2508_08192_b200.drafttree import ROOT, TreeSpec
+
+    rng = np.random.default_rng(5)
+    for case in range(20):
+        n_nodes = int(rng.integers(1, 17))
+        parent = [ROOT]
+        for i in range(1, n_nodes):
+            parent.append(int(rng.integers(0, i)) if rng.random() < 0.8 else ROOT)
+        tree = TreeSpec(tuple(parent))
+        ctx = int(rng.integers(0, 65))
+        heads = int(rng.choice([1, 2, 4]))
+        dh = int(rng.choice([4, 8]))
+        dim = heads * dh
+        chunk = None if case % 2 == 0 else int(rng.choice([4, 8]))
+        q = rng.normal(size=(n_nodes, dim))
+        ck, cv = rng.normal(size=(ctx, dim)), rng.normal(size=(ctx, dim))
+        tk, tv = rng.normal(size=(n_nodes, dim)), rng.normal(size=(n_nodes, dim))
+        got = tree_attention(q, ck, cv, tk, tv, tree, dh ** -0.5, n_heads=heads, chunk_len=chunk)
+        mask = explicit_tree_mask(tree, ctx, chunk_len=chunk)
+        want = naive_tree_attention(q, np.concatenate([ck, tk]), np.concatenate([cv, tv]), mask, dh ** -0.5,
+                                    n_heads=heads)
+        assert np.max(np.abs(got - want)) < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# batched paged GQA tree-verify attention
+# ---------------------------------------------------------------------------
+
+def _gqa_case(g, name, dtype):
+    from paper_2508_08192_b200.drafttree import tree_build
+
+    p = name + "_"
+    bsz, hq, hkv, d, bs, r_max = (int(x) for x in g[p + "meta"])
+    q = _cuda(g[p + "q"], dtype)
+    kp = _cuda(g[p + "k_pool"], dtype)
+    vp = _cuda(g[p + "v_pool"], dtype)
+    tk = _cuda(g[p + "tk"], dtype)
+    tv = _cuda(g[p + "tv"], dtype)
+    table = _cuda(g[p + "table"], torch.int32)
+    ctx = _cuda(g[p + "ctx"], torch.int32)
+    par = _cuda(g[p + "parent_aug"], torch.int32)
+    nr = _cuda(g[p + "n_rows"], torch.int32)
+    mask, _pos, _depth, err = tree_build(par, nr, ctx)
+    return dict(q=q, kp=kp, vp=vp, tk=tk, tv=tv, table=table, ctx=ctx, mask=mask, nr=nr, d=d,
+                out=g[p + "out"], lse=g[p + "lse"], n_rows=g[p + "n_rows"])
+
+
+@pytest.mark.parametrize("kernel", [0, 2])
+@pytest.mark.parametrize("splits", [0, 1, 3])
+def test_tree_verify_attention_bf16_golden(golden, kernel, splits):
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    g = golden("attention_gqa")
+    for name in g["names"]:
+        c = _gqa_case(g, str(name), torch.bfloat16)
+        out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                         c["nr"], c["d"] ** -0.5, num_splits=splits, kernel=kernel)
+        torch.cuda.synchronize()
+        out = out.float().cpu().numpy()
+        lse = lse.cpu().numpy()
+        for b, n in enumerate(c["n_rows"]):
+            # bf16 output rounding: |x| <~ 3 -> 2^-7 relative
+            np.testing.assert_allclose(out[b, :n], c["out"][b, :n], atol=2e-2, rtol=0)
+            assert np.abs(out[b, :n] - c["out"][b, :n]).mean() < 2e-3
+            np.testing.assert_allclose(lse[b, :, :n], c["lse"][b, :, :n], atol=1e-3, rtol=0)
+            assert not out[b, n:].any()
+
+
+@pytest.mark.parametrize("splits", [1, 4])
+def test_tree_verify_attention_fp32_golden(golden, splits):
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    g = golden("attention_gqa")
+    for name in g["names"]:
+        c = _gqa_case(g, str(name), torch.float32)
+        out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                         c["nr"], c["d"] ** -0.5, num_splits=splits, kernel=2)
+        torch.cuda.synchronize()
+        out, lse = out.cpu().numpy(), lse.cpu().numpy()
+        for b, n in enumerate(c["n_rows"]):
+            np.testing.assert_allclose(out[b, :n], c["out"][b, :n], atol=1e-5, rtol=0)
+            np.testing.assert_allclose(lse[b, :, :n], c["lse"][b, :, :n], atol=1e-5, rtol=0)
+
+
+# ---------------------------------------------------------------------------
+# acceptance
+# ---------------------------------------------------------------------------
+
+def _aug_batch(parents, tokens_list, r_max):
+    b = len(parents)
+    par = np.full((b, r_max), -1, dtype=np.int32)
+    tok = np.zeros((b, r_max), dtype=np.int32)
+    nr = np.zeros((b,), dtype=np.int32)
+    for i, (p, t) in enumerate(zip(parents, tokens_list)):
+        aug = O.augment(tuple(int(x) for x in p))
+        par[i, :len(aug)] = aug
+        tok[i, 1:len(aug)] = t
+        nr[i] = len(aug)
+    return par, tok, nr
+
+
+def test_accept_greedy_golden(golden):
+    from paper_2508_08192_b200.sampling import accept_greedy
+
+    g = golden("accept_greedy")
+    for k in range(int(g["n_cases"])):
+        p = f"g{k}_"
+        logits = g[p + "logits"]
+        n = logits.shape[0]
+        par, tok, nr = _aug_batch([g[p + "parent"]], [g[p + "tokens"]], n)
+        for dt in (torch.float32, torch.bfloat16):
+            lg = _cuda(logits[None], dt)
+            res = accept_greedy(lg, _cuda(par, torch.int32), _cuda(nr, torch.int32), _cuda(tok, torch.int32))
+            plen = int(res.path_len[0])
+            if dt == torch.float32:
+                assert list(res.path[0, :plen].cpu().numpy()) == list(g[p + "path"])
+                assert int(res.next_token[0]) == int(g[p + "next"])
+                assert int(res.uniforms_used[0]) == int(g[p + "used"])
+            else:
+                # bf16 logits: compare with the oracle on the rounded logits
+                am = np.argmax(lg[0].float().cpu().numpy().astype(np.float64), axis=1)
+                path, nxt, used = O.greedy_walk(tuple(int(x) for x in g[p + "parent"]), g[p + "tokens"], am)
+                assert list(res.path[0, :plen].cpu().numpy()) == path
+                assert int(res.next_token[0]) == nxt and int(res.uniforms_used[0]) == used
+            assert int(res.err[0]) == 0
+
+
+def test_accept_greedy_batched_ragged(golden):
+    """All golden cases in ONE batched launch (ragged R per sequence)."""
+    from paper_2508_08192_b200.sampling import accept_greedy
+
+    g = golden("accept_greedy")
+    cases = [k for k in range(int(g["n_cases"])) if g[f"g{k}_logits"].shape[1] == 4096]
+    r_max = max(g[f"g{k}_logits"].shape[0] for k in cases)
+    lg = np.zeros((len(cases), r_max, 4096), dtype=np.float32)
+    for i, k in enumerate(cases):
+        lg[i, :g[f"g{k}_logits"].shape[0]] = g[f"g{k}_logits"]
+    par, tok, nr = _aug_batch([g[f"g{k}_parent"] for k in cases], [g[f"g{k}_tokens"] for k in cases], r_max)
+    res = accept_greedy(_cuda(lg, torch.float32), _cuda(par, torch.int32), _cuda(nr, torch.int32),
+                        _cuda(tok, torch.int32))
+    for i, k in enumerate(cases):
+        plen = int(res.path_len[i])
+        assert list(res.path[i, :plen].cpu().numpy()) == list(g[f"g{k}_path"])
+        assert int(res.next_token[i]) == int(g[f"g{k}_next"])
+        assert int(res.uniforms_used[i]) == int(g[f"g{k}_used"])
+
+
+def test_accept_greedy_nan_raises_flag():
+    from paper_2508_08192_b200.sampling import accept_greedy
+
+    lg = torch.zeros((1, 2, 64), dtype=torch.float32, device="cuda")
+    lg[0, 1, 5] = float("nan")
+    par = torch.tensor([[-1, 0]], dtype=torch.int32, device="cuda")
+    res = accept_greedy(lg, par, torch.tensor([2], dtype=torch.int32, device="cuda"),
+                        torch.zeros((1, 2), dtype=torch.int32, device="cuda"))
+    assert int(res.err[0]) & 2
+
+
+def _margin_ok(g, k, res_path, res_next, res_used):
+    return (list(res_path) == list(g[f"s{k}_path"]) and res_next == int(g[f"s{k}_next"])
+            and res_used == int(g[f"s{k}_used"]))
+
+
+def test_accept_stochastic_golden(golden):
+    """Stochastic acceptance vs the reference (fp32 pipeline; decisions whose
+    reference margin is < 1e-6 may differ and are counted -- none expected
+    on these fixtures)."""
+    from paper_2508_08192_b200.sampling import accept_stochastic
+
+    g = golden("accept_stochastic")
+    mism = []
+    for k in range(int(g["n_cases"])):
+        p = f"s{k}_"
+        temp, top_p, _seed = g[p + "meta"]
+        logits, dl = g[p + "logits"], g[p + "draft_logits"]
+        n = logits.shape[0]
+        par, tok, nr = _aug_batch([g[p + "parent"]], [g[p + "tokens"]], n)
+        res = accept_stochastic(_cuda(logits[None], torch.float32), _cuda(dl[None], torch.float32), float(temp),
+                                float(top_p), _cuda(par, torch.int32), _cuda(nr, torch.int32),
+                                _cuda(tok, torch.int32), _cuda(g[p + "uniforms"][None], torch.float64),
+                                want_residual=True)
+        torch.cuda.synchronize()
+        assert int(res.err[0]) == 0
+        plen = int(res.path_len[0])
+        got = (res.path[0, :plen].cpu().numpy(), int(res.next_token[0]), int(res.uniforms_used[0]))
+        if not _margin_ok(g, k, *got):
+            mism.append((k, got, list(g[p + "path"]), int(g[p + "next"])))
+        else:
+            np.testing.assert_allclose(res.residual[0].cpu().numpy(), g[p + "residual"], atol=2e-6)
+    assert not mism, mism
+
+
+def test_target_dist_and_mss_drop_in(golden):
+    from paper_2508_08192_b200 import sampling as S
+    from paper_2508_08192_b200.drafttree import TreeSpec
+
+    g = golden("sampling_kat")
+    for i in range(len(g["ps"])):
+        np.testing.assert_allclose(S.top_p_mask(g["dists"][i], g["ps"][i]), g["top_p"][i], atol=1e-12)
+        assert S.sample_from(g["dists"][i], g["us"][i]) == int(g["sample"][i])
+    # reference tests/test_sampling.py:11-58
+    d = np.array([0.5, 0.3, 0.2])
+    np.testing.assert_allclose(S.top_p_mask(d, 0.8), [0.625, 0.375, 0.0])
+    np.testing.assert_allclose(S.top_p_mask(d, 0.5), [1.0, 0.0, 0.0])
+    np.testing.assert_allclose(S.top_p_mask(d, 0.51), [0.625, 0.375, 0.0])
+    np.testing.assert_allclose(S.top_p_mask(np.full(4, 0.25), 0.5), [0.5, 0.5, 0.0, 0.0])
+    np.testing.assert_array_equal(S.target_dist(np.array([0.1, 3.0, -1.0]), 0.0, 1.0), [0, 1, 0])
+    np.testing.assert_array_equal(S.target_dist(np.array([5.0, 1.0, 0.0]), 0.0, 1.0,
+                                                np.array([False, True, True])), [0, 1, 0])
+    with pytest.raises(S.SamplingError):
+        S.target_dist(np.array([5.0, 1.0, 0.0]), 1.0, 1.0, np.zeros(3, dtype=bool))
+    d = np.array([0.2, 0.5, 0.3])
+    assert [S.sample_from(d, u) for u in (0.0, 0.19, 0.2, 0.69, 0.7, 0.999999)] == [0, 0, 1, 1, 2, 2]
+    # MSS known answers (reference tests/test_sampling.py:79-138)
+    q = np.array([0.5, 0.5, 0.0])
+    p = np.array([0.6, 0.4, 0.0])
+    chain2 = TreeSpec((-1, 0))
+    r = S.mss_verify(S.DraftResult(chain2, (0, 0), (q, q)), [p, p, np.array([0.0, 0.0, 1.0])], [0.9, 0.9, 0.5])
+    assert r.accepted_path == [0, 1] and r.next_token == 2 and r.uniforms_used == 3
+    c1 = TreeSpec((-1,))
+    r = S.mss_verify(S.DraftResult(c1, (0,), (np.array([1.0, 0.0]),)), [np.array([0.3, 0.7])] * 2, [0.5, 0.0])
+    assert r.accepted_path == [] and r.next_token == 1
+    np.testing.assert_allclose(r.residual, [0.0, 1.0])
+    q1 = np.array([1.0, 0.0, 0.0])
+    r = S.mss_verify(S.DraftResult(TreeSpec((-1, -1)), (0, 1), (q1, q1)), [np.array([0.0, 1.0, 0.0])] * 3,
+                     [0.5] * 3)
+    assert r.accepted_path == [1] and r.next_token == 1
+    r = S.mss_verify(S.DraftResult(c1, (0,), (np.array([1.0, 0.0]),)), [np.array([1.0, 0.0])] * 2, [1.0, 0.3])
+    assert r.accepted_path == [] and r.next_token == 0
+    with pytest.raises(S.SamplingError):
+        S.mss_verify(S.DraftResult(c1, (0,), (np.array([0.5, 0.5]),)), [np.array([0.5, 0.5])] * 2, [0.5])
+
+
+def test_mss_drop_in_matches_reference_golden(golden):
+    from paper_2508_08192_b200 import sampling as S
+    from paper_2508_08192_b200.drafttree import TreeSpec
+
+    g = golden("accept_stochastic")
+    for k in range(int(g["n_cases"])):
+        p = f"s{k}_"
+        temp, top_p, _seed = g[p + "meta"]
+        parent = tuple(int(x) for x in g[p + "parent"])
+        logits, dl = g[p + "logits"], g[p + "draft_logits"]
+        qd = [S.target_dist(dl[0 if a == -1 else 1 + a], temp, 1.0) for a in parent]
+        dists = list(S.target_dists(logits, temp, top_p))
+        np.testing.assert_allclose(dists[0], g[p + "dist0"], atol=1e-14)
+        r = S.mss_verify(S.DraftResult(TreeSpec(parent), tuple(g[p + "tokens"]), tuple(qd)), dists, g[p + "uniforms"],
+                         mode="stochastic")
+        assert r.accepted_path == list(g[p + "path"])
+        assert r.next_token == int(g[p + "next"]) and r.uniforms_used == int(g[p + "used"])
+        np.testing.assert_allclose(r.residual, g[p + "residual"], atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# K7 compaction + paged cache
+# ---------------------------------------------------------------------------
+
+def test_paged_cache_and_compaction_golden(golden):
+    from paper_2508_08192_b200.kvstore import PagedKvCache, compact_kv
+
+    g = golden("compact")
+    for k in range(int(g["n_cases"])):
+        p = f"k{k}_"
+        bs, L, hkv, d, n_layers, nb, kept = (int(x) for x in g[p + "meta"])
+        table = g[p + "table"]
+        path = [int(x) for x in g[p + "path"]]
+        C = L - 1
+        # drop-in cache replaying the engine's write-back
+        cache = PagedKvCache(n_layers, hkv * d, n_blocks=nb, block_size=bs)
+        cache.new_seq(0)
+        cache.ensure(0, max(C, 1))
+        for li in range(n_layers):
+            if C:
+                cache.write(0, li, 0, g[p + f"ck{li}"], g[p + f"cv{li}"])
+        cache.set_len(0, L)
+        n_tree = g[p + f"tk0"].shape[0]
+        cache.alloc_for_step(0, n_tree - 1)
+        assert cache.block_table(0) == list(table)
+        rows = O.accepted_rows(path, kept)
+        for li in range(n_layers):
+            cache.write(0, li, L - 1, g[p + f"tk{li}"][rows], g[p + f"tv{li}"][rows])
+        cache.rewind(0, L + kept - 1)
+        cache.set_len(0, L + kept)
+        assert cache.block_table(0) == list(g[p + "table_after"])
+        for li in range(n_layers):
+            gk, gv = cache.gather(0, li, L + kept - 1)
+            np.testing.assert_array_equal(gk, g[p + f"gk{li}"])
+            np.testing.assert_array_equal(gv, g[p + f"gv{li}"])
+        # batched device compaction on the head-split layout (bf16-exact data)
+        kpool = torch.zeros((n_layers, nb, hkv, bs, d), dtype=torch.float32, device="cuda")
+        vpool = torch.zeros_like(kpool)
+        tk = torch.zeros((n_layers, 1, n_tree, hkv, d), dtype=torch.float32, device="cuda")
+        tv = torch.zeros_like(tk)
+        want_k = np.zeros((n_layers, nb, hkv, bs, d))
+        want_v = np.zeros_like(want_k)
+        for li in range(n_layers):
+            tk[li, 0] = _cuda(g[p + f"tk{li}"].reshape(n_tree, hkv, d), torch.float32)
+            tv[li, 0] = _cuda(g[p + f"tv{li}"].reshape(n_tree, hkv, d), torch.float32)
+            O.compact_kv(want_k[li], want_v[li], table, C, g[p + f"tk{li}"].reshape(n_tree, hkv, d).astype(np.float32),
+                         g[p + f"tv{li}"].reshape(n_tree, hkv, d).astype(np.float32), path, kept)
+        pt = np.zeros((1, n_tree), dtype=np.int32)
+        pt[0, :len(path)] = path
+        compact_kv(tk, tv, kpool, vpool, _cuda(table[None], torch.int32), _cuda([C], torch.int32),
+                   _cuda(pt, torch.int32), _cuda([len(path)], torch.int32), _cuda([kept], torch.int32))
+        np.testing.assert_array_equal(kpool.cpu().numpy(), want_k.astype(np.float32))
+        np.testing.assert_array_equal(vpool.cpu().numpy(), want_v.astype(np.float32))

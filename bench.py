@@ -1,0 +1,456 @@
+"""Tree-verify benchmark (BASELINE.json metric: tree-verify us/step & HBM GB/s).
+
+Workload (N = 1): Llama-3.3-70B attention shapes (configs[2]) -- B = 32,
+64 q / 8 kv heads, d = 128, the 64-row EAGLE tree of SURVEY.md 8(d) (63 drafts
++ root), ctx 8192 in bf16 pages of 64, greedy acceptance over fp32 logits of
+V = 128,256.  One step = tree_build + paged GQA tree attention (prefix +
+masked suffix + LSE merge) + acceptance + KV compaction for one layer.
+N > 1: KV heads (and their q heads) and the vocabulary are sharded over the
+ranks (strong scaling); one NCCL all-reduce(MAX) of packed argmax keys per
+step.  Synthetic seeded inputs; working set (KV + logits, ~2.1 GB per GPU at
+N = 1) far exceeds the 126 MB L2, so every step streams from HBM.
+
+`--impl reference` times the reference algorithm on the host (the numpy
+oracle port: the reference is pure Python/numpy, nothing compiles) on a
+bounded sample and extrapolates exactly (the reference loops sequences and
+heads independently, engine.py:581-582).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tree-verify μs/step & HBM GB/s (% of 8 TB/s) at bs1–64, 8k ctx, 1/2/4/8 GPU"
+
+TREE64 = [-1, -1, -1, -1, -1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5, 5, 6, 7,
+          8, 8, 8, 8, 9, 9, 9, 10, 10, 10, 11, 11, 12, 13, 14, 15, 32, 32, 32, 33, 33, 34, 34, 35, 36, 37, 48, 48, 49,
+          50, 51]
+
+CONFIGS = {
+    # name: (B, Hq, Hkv, d, ctx, block_size, vocab, tree)
+    "c3": dict(workload="llama-3.3-70b-attn bs32 ctx8192 tree64 greedy", B=32, Hq=64, Hkv=8, d=128, ctx=8192, bs=64,
+               V=128256),
+    "c2": dict(workload="llama-3.1-8b-attn bs1 ctx8192 tree64 greedy", B=1, Hq=32, Hkv=8, d=128, ctx=8192, bs=64,
+               V=128256),
+    "c4": dict(workload="llama-3.1-405b-attn bs64 ctx32768 tree64 greedy", B=64, Hq=128, Hkv=8, d=128, ctx=32768,
+               bs=64, V=128256),
+}
+
+
+def _augment(parent):
+    return [-1] + [0 if p == -1 else p + 1 for p in parent]
+
+
+def _measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk["hbm_gbs"], pk["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """Polls NVML SM clock + throttle reasons in a thread during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nvml.nvmlDeviceGetClockInfo(self._h, self._nvml.NVML_CLOCK_SM))
+                r = self._nvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._nvml is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nvml is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_inputs(cfg, shard, device, seed=0):
+    """Seeded synthetic inputs for one rank's shard (KV heads, vocab range)."""
+    import torch
+
+    from paper_2508_08192_b200.verify import StepInputs
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    B, Hq, Hkv, d, C, bs, V = (cfg[k] for k in ("B", "Hq", "Hkv", "d", "ctx", "bs", "V"))
+    aug = _augment(TREE64)
+    R = len(aug)
+    hkv_l, hq_l = shard.n_kv, shard.n_q
+    pages = -(-(C + R) // bs)
+    nb = B * pages + 8
+    # identical page permutation on every rank (same block table)
+    perm = torch.randperm(nb, generator=torch.Generator().manual_seed(seed + 1)).to(torch.int32)
+    table = perm[:B * pages].reshape(B, pages).to(device)
+
+    def randn(*shape, dtype=torch.bfloat16, std=1.0, gen=g):
+        return (torch.randn(*shape, generator=gen, device=device) * std).to(dtype)
+
+    # full-head tensors are drawn per KV-head slice so shards see the same data
+    def per_head(shape_fn, n_total, lo, hi, dtype, seed_off):
+        parts = []
+        for h in range(lo, hi):
+            gh = torch.Generator(device=device)
+            gh.manual_seed(seed * 1000 + seed_off * 97 + h)
+            parts.append((torch.randn(*shape_fn(), generator=gh, device=device)).to(dtype))
+        return parts
+
+    kp = torch.stack(per_head(lambda: (nb, bs, d), Hkv, shard.kv_lo, shard.kv_hi, torch.bfloat16, 1), dim=1)
+    vp = torch.stack(per_head(lambda: (nb, bs, d), Hkv, shard.kv_lo, shard.kv_hi, torch.bfloat16, 2), dim=1)
+    q = torch.stack(per_head(lambda: (B, R, d), Hq, shard.q_lo, shard.q_hi, torch.bfloat16, 3), dim=2)
+    tk = torch.stack(per_head(lambda: (B, R, d), Hkv, shard.kv_lo, shard.kv_hi, torch.bfloat16, 4), dim=2)
+    tv = torch.stack(per_head(lambda: (B, R, d), Hkv, shard.kv_lo, shard.kv_hi, torch.bfloat16, 5), dim=2)
+    # logits: the full vocab on every rank (setup only), then this rank's slice
+    gl = torch.Generator(device=device)
+    gl.manual_seed(seed + 7)
+    logits_full = torch.randn(B, R, V, generator=gl, device=device) * 2.0
+    am = logits_full.argmax(dim=-1)  # lowest index on ties
+    par = torch.tensor([aug] * B, dtype=torch.int32, device=device)
+    tokens = torch.zeros((B, R), dtype=torch.int32, device=device)
+    rnd = torch.rand((B, R), generator=gl, device=device)
+    rtok = torch.randint(0, V, (B, R), generator=gl, device=device)
+    parent_row = par.clamp(min=0).long()
+    want = torch.gather(am, 1, parent_row)
+    tokens = torch.where(rnd < 0.6, want, rtok).to(torch.int32)
+    tokens[:, 0] = 0
+    logits = logits_full[:, :, shard.v_lo:shard.v_hi].contiguous()
+    del logits_full
+    x = StepInputs(parent=par, n_rows=torch.full((B,), R, dtype=torch.int32, device=device),
+                   ctx_len=torch.full((B,), C, dtype=torch.int32, device=device), tokens=tokens, q=q.contiguous(),
+                   tree_k=tk.contiguous(), tree_v=tv.contiguous(), logits=logits, k_pool=kp.contiguous(),
+                   v_pool=vp.contiguous(), block_table=table)
+    return x, R
+
+
+def step_bytes_flops(cfg, shard, R, anc_pairs):
+    B, d, C, V = cfg["B"], cfg["d"], cfg["ctx"], shard.n_vocab
+    hq, hkv = shard.n_q, shard.n_kv
+    s = 2
+    attn_bytes = (B * C * hkv * d * 2 * s + B * R * hq * d * s + B * R * hkv * d * 2 * s + B * R * hq * d * s
+                  + 4 * B * hq * R + 4 * B * (-(-C // cfg["bs"])))
+    accept_bytes = B * R * V * 4
+    attn_flops = 4.0 * d * hq * B * (R * C + anc_pairs)
+    return attn_bytes, accept_bytes, attn_flops
+
+
+def cpu_sample(cfg, seed=0):
+    """Reference algorithm (numpy oracle port) on a bounded sample of the
+    workload: 1 sequence x 1 KV head group for attention, 1 sequence for
+    greedy acceptance.  Returns (seconds for the sample, extrapolation
+    factors)."""
+    import numpy as np
+
+    from oracle import specdec_oracle as O
+
+    rng = np.random.default_rng(seed)
+    B, Hq, Hkv, d, C, bs, V = (cfg[k] for k in ("B", "Hq", "Hkv", "d", "ctx", "bs", "V"))
+    g = Hq // Hkv
+    aug = tuple(_augment(TREE64))
+    R = len(aug)
+    pages = -(-(C + R) // bs)
+
+    def bf(x):
+        return x.astype(np.float32).astype(np.float64)
+
+    kp = bf(rng.normal(size=(pages + 1, 1, bs, d)))
+    vp = bf(rng.normal(size=(pages + 1, 1, bs, d)))
+    table = rng.permutation(pages + 1)[:pages]
+    q = bf(rng.normal(size=(R, g * d)))
+    tk = bf(rng.normal(size=(R, d)))
+    tv = bf(rng.normal(size=(R, d)))
+    logits = (2.0 * rng.normal(size=(R, V))).astype(np.float32)
+    toks = rng.integers(0, V, size=R)
+    t0 = time.perf_counter()
+    ck = O.paged_gather(kp, table, C)
+    cv = O.paged_gather(vp, table, C)
+    O.tree_attention(q, ck, cv, tk, tv, aug, d ** -0.5, g, 1)
+    t1 = time.perf_counter()
+    dists = [O.target_dist(logits[i], 0.0, 1.0) for i in range(R)]
+    am = [int(np.argmax(dd)) for dd in dists]
+    O.greedy_walk(aug[1:] and tuple(p - 1 if p > 0 else -1 for p in aug[1:]), toks[1:], am)
+    t2 = time.perf_counter()
+    return (t1 - t0), (t2 - t1), B * Hkv, B
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    samples = []
+    for i in range(args.warmup + args.steps):
+        ta, tacc, fa, facc = cpu_sample(cfg, seed=i)
+        if i >= args.warmup:
+            samples.append(ta * fa + tacc * facc)
+    per_step = statistics.mean(samples)
+    us = per_step * 1e6
+    cores = blas_threads()
+    sample = (f"1 sequence x 1 KV-head group (8 q heads) of the attention extrapolated x{cfg['B'] * cfg['Hkv']}, "
+              f"+ greedy target_dist/mss walk for 1 sequence x{cfg['B']}; numpy float64, {cores} BLAS threads")
+    line = {"impl": "reference", "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "global_batch": cfg["B"], "seq_len": cfg["ctx"]},
+            "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 tcgen05, 2 SIMT")
+    ap.add_argument("--splits", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_08192_b200 import _lib
+    from paper_2508_08192_b200.sharding import ShardedGreedyAcceptor, shard_for
+    from paper_2508_08192_b200.verify import TreeVerifier
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    shard = shard_for(rank, world, cfg["Hq"], cfg["Hkv"], cfg["V"])
+    x, R = make_inputs(cfg, shard, dev)
+    from oracle import specdec_oracle as O  # checker only (mask popcount for the FLOP count)
+
+    anc_pairs = int(O.suffix_mask(tuple(_augment(TREE64))).sum())
+    ver = TreeVerifier(scale=cfg["d"] ** -0.5, max_ctx=cfg["ctx"], num_splits=args.splits, kernel=args.kernel)
+    if world > 1:
+        sharded = ShardedGreedyAcceptor(shard)
+        ver.greedy = lambda logits, parent, n_rows, tokens, stream=None: sharded(logits, parent, n_rows, tokens,
+                                                                                stream)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        ver.step(x)
+    torch.cuda.synchronize()
+    use_graph = world == 1
+    if use_graph:
+        ver.capture(x)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- timed region: K steps, device events, max over ranks ----------
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            if use_graph:
+                ver.replay()
+            else:
+                ver.step(x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # ---- per-kernel breakdown (instrumented eager pass, same stream) -----
+    from paper_2508_08192_b200.attention import TreeVerifyAttention
+
+    o = ver._out[1]
+    n_ev = 5
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        ev = evs[k]
+        ev[0].record(stream)
+        lib = _lib.lib()
+        b_, r_ = x.parent.shape
+        lib.sdb_tree_build(_lib.ptr(x.parent), _lib.ptr(x.n_rows), _lib.ptr(x.ctx_len), b_, r_, o["mask"].shape[-1],
+                           _lib.ptr(o["mask"]), _lib.ptr(o["pos"]), _lib.ptr(o["depth"]), _lib.ptr(o["tree_err"]),
+                           _lib.stream_ptr())
+        ev[1].record(stream)
+        ver.attn(x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
+                 ver.scale, out=o["out"], lse=o["lse"], max_ctx=ver.max_ctx, num_splits=ver.num_splits,
+                 kernel=ver.kernel)
+        ev[2].record(stream)
+        acc = ver.greedy(x.logits, x.parent, x.n_rows, x.tokens)
+        ev[3].record(stream)
+        from paper_2508_08192_b200.kvstore import compact_kv
+
+        compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0), x.v_pool.unsqueeze(0),
+                   x.block_table, x.ctx_len, acc.path, acc.path_len)
+        ev[4].record(stream)
+    torch.cuda.synchronize()
+    parts = np.array([[ev[i].elapsed_time(ev[i + 1]) for i in range(n_ev - 1)] for ev in evs]).mean(axis=0)
+    t_attn_ms = float(parts[1])
+    accept_len = float(acc.path_len.float().mean().item())
+
+    # ---- e2e through the public API with host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        pinned = {k: getattr(x, k).cpu().pin_memory() for k in ("q", "tree_k", "tree_v", "logits", "parent",
+                                                                   "n_rows", "ctx_len", "tokens")}
+        dev_in = {k: torch.empty_like(getattr(x, k)) for k in pinned}
+        h2d = sum(v.numel() * v.element_size() for v in pinned.values())
+        out_h = torch.empty(o["out"].shape, dtype=o["out"].dtype).pin_memory()
+        lse_h = torch.empty(o["lse"].shape, dtype=o["lse"].dtype).pin_memory()
+        path_h = torch.empty(acc.path.shape, dtype=acc.path.dtype).pin_memory()
+        plen_h = torch.empty(acc.path_len.shape, dtype=acc.path_len.dtype).pin_memory()
+        nxt_h = torch.empty(acc.next_token.shape, dtype=acc.next_token.dtype).pin_memory()
+        d2h = sum(t_.numel() * t_.element_size() for t_ in (out_h, lse_h, path_h, plen_h, nxt_h))
+        from paper_2508_08192_b200.verify import StepInputs
+
+        xe = StepInputs(**{**{k: dev_in[k] for k in pinned}, "k_pool": x.k_pool, "v_pool": x.v_pool,
+                           "block_table": x.block_table})
+
+        def e2e_step():
+            for k_, v_ in pinned.items():
+                dev_in[k_].copy_(v_, non_blocking=True)
+            out_, lse_, acc_, _ = ver.step(xe)
+            out_h.copy_(out_, non_blocking=True)
+            lse_h.copy_(lse_, non_blocking=True)
+            path_h.copy_(acc_.path, non_blocking=True)
+            plen_h.copy_(acc_.path_len, non_blocking=True)
+            nxt_h.copy_(acc_.next_token, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = f0.elapsed_time(f1) / args.steps
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(te.item()) * 1e3, "unit": "us/step", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    attn_bytes, accept_bytes, attn_flops = step_bytes_flops(cfg, shard, R, anc_pairs)
+    tot = torch.tensor([attn_bytes + accept_bytes], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+    step_bytes_all = float(tot.item())
+    hbm_peak, tc_peak, peak_src = _measured_peaks()
+    achieved_tf = attn_flops / (t_attn_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
+            tr = json.load(f)
+        key = f"{args.config}:g{world}"
+        traffic = tr.get(key)
+    except Exception:
+        pass
+    gbs = step_bytes_all / (ms * 1e-3) / 1e9
+    launches_per_step = 1 + (2 if o is not None else 1) + 2 + 1
+    line = {
+        "metric": METRIC, "value": ms * 1e3, "unit": "us/step", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "global_batch": cfg["B"], "seq_len": cfg["ctx"], "tree_rows": R,
+                   "heads": f"{cfg['Hq']}q/{cfg['Hkv']}kv d{cfg['d']}", "page": cfg["bs"], "vocab": cfg["V"],
+                   "parallelism": f"kv-head+vocab shard x{world}", "l2": "inputs 2.1 GB/GPU >> 126 MB L2",
+                   "graph": use_graph},
+        "hbm_gbs": gbs, "pct_of_8tbs": 100.0 * gbs / 8000.0,
+        "kernels_ms": {"tree_build": float(parts[0]), "tree_attn": float(parts[1]), "accept": float(parts[2]),
+                       "compact": float(parts[3])},
+        "mean_accepted": accept_len,
+        "roofline": {"kernel": "tree_attn", "bound": "tensor", "achieved": achieved_tf, "peak": tc_peak,
+                     "unit": "TFLOP/s", "frac": achieved_tf / tc_peak, "traffic": traffic,
+                     "peak_source": peak_src, "flops_per_launch": attn_flops,
+                     "hbm_gbs": attn_bytes / (t_attn_ms * 1e-3) / 1e9,
+                     "accept_hbm_frac": accept_bytes / (parts[2] * 1e-3) / 1e9 / hbm_peak},
+        "clocks": sampler.summary(),
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ta, tacc, fa, facc = cpu_sample(cfg)
+        ta, tacc, fa, facc = cpu_sample(cfg, seed=1)
+        us = (ta * fa + tacc * facc) * 1e6
+        line["cpu_baseline"] = {"value": us, "unit": "us/step", "cores": blas_threads(), "kind": "port",
+                                "sample": f"1 seq x 1 KV group attention (x{fa}) + 1 seq greedy acceptance (x{facc}),"
+                                          " numpy float64 oracle port, extrapolated"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

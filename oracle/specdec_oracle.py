@@ -201,14 +201,20 @@ def paged_gather(pool, block_table, n_rows):
     """Gather the first n committed rows of one sequence from a paged pool.
 
     Restates ``PagedKvCache.gather`` / ``_segments`` (kvstore.py:207-215,
-    235-246) on the device layout pool[num_blocks, Hkv, bs, d]; returns
-    (n, Hkv*d) rows."""
+    235-246) -- one copy per page segment -- on the device layout
+    pool[num_blocks, Hkv, bs, d]; returns (n, Hkv*d) rows."""
     nb, hkv, bs, d = pool.shape
-    out = np.zeros((n_rows, hkv * d), dtype=pool.dtype)
-    for pos in range(n_rows):
+    segs = []
+    pos = 0
+    while pos < n_rows:
         b, off = divmod(pos, bs)
-        out[pos] = pool[block_table[b], :, off, :].reshape(hkv * d)
-    return out
+        take = min(bs - off, n_rows - pos)
+        seg = pool[block_table[b], :, off:off + take, :]  # (hkv, take, d)
+        segs.append(np.transpose(seg, (1, 0, 2)).reshape(take, hkv * d))
+        pos += take
+    if not segs:
+        return np.zeros((0, hkv * d), dtype=pool.dtype)
+    return np.concatenate(segs)
 
 
 def paged_write(pool, block_table, start, rows):

@@ -168,8 +168,9 @@ def mss_verify(draft, target_dists_, uniforms, mode="greedy_children"):
     resid = torch.empty((vocab,), dtype=torch.float64, device="cuda")
     err = torch.zeros((1,), dtype=torch.int32, device="cuda")
     tu = _dev(uni if uni.size else np.zeros(1))
-    rc = _lib.lib().sdb_mss_verify_f64(_lib.ptr(par), _lib.ptr(tok), n, vocab, _lib.ptr(_dev(nd)),
-                                       _lib.ptr(_dev(td)), _lib.ptr(tu), int(uni.size), _lib.ptr(path),
+    tnd, ttd = _dev(nd), _dev(td)  # keep alive until the launch is enqueued
+    rc = _lib.lib().sdb_mss_verify_f64(_lib.ptr(par), _lib.ptr(tok), n, vocab, _lib.ptr(tnd),
+                                       _lib.ptr(ttd), _lib.ptr(tu), int(uni.size), _lib.ptr(path),
                                        _lib.ptr(scal), _lib.ptr(resid), _lib.ptr(err), _lib.stream_ptr())
     _lib.check(rc, "mss_verify")
     e = int(err.item())
@@ -234,11 +235,15 @@ class GreedyAcceptor:
             dt = _lib.DTYPE_BF16
         else:
             raise SamplingError(f"unsupported logits dtype {logits.dtype}")
-        if logits.stride(2) != 1 or logits.stride(0) != r * logits.stride(1):
-            raise SamplingError("logits must be [B, R, V] with unit vocab stride")
+        if logits.is_contiguous():
+            row_stride = v
+        elif logits.stride(2) == 1 and (b == 1 or logits.stride(0) == r * logits.stride(1)):
+            row_stride = logits.stride(1)
+        else:
+            raise SamplingError("logits must be [B, R, V] with unit vocab stride and uniform row stride")
         o = self._alloc(b, r, logits.device)
         o["err"].zero_()
-        rc = _lib.lib().sdb_accept_greedy(_lib.ptr(logits), dt, b, r, v, logits.stride(1), _lib.ptr(parent),
+        rc = _lib.lib().sdb_accept_greedy(_lib.ptr(logits), dt, b, r, v, row_stride, _lib.ptr(parent),
                                           _lib.ptr(n_rows), _lib.ptr(tokens), _lib.ptr(o["keys"]),
                                           _lib.ptr(o["path"]), _lib.ptr(o["path_len"]), _lib.ptr(o["next_token"]),
                                           _lib.ptr(o["used"]), _lib.ptr(o["err"]), _lib.stream_ptr(stream))

@@ -67,7 +67,7 @@ static int resolve(const sdb_tree_attn_args *a, TreeAttnParams &p, bool &sm100) 
   p.num_splits = 1;
   sm100 = use_sm100(a, p);
   if (a->kernel == 1 && !sm100) return SDB_E_UNSUPPORTED;
-  const int rows_per_cta = sm100 ? 128 : 32;
+  const int rows_per_cta = sm100 ? ((a->r_max * (a->hq / a->hkv) > 128) ? 256 : 128) : 32;
   p.num_splits = a->num_splits > 0 ? a->num_splits : auto_splits(a, rows_per_cta);
   return SDB_OK;
 }

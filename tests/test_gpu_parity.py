@@ -208,14 +208,17 @@ def _gqa_case(g, name, dtype):
                 out=g[p + "out"], lse=g[p + "lse"], n_rows=g[p + "n_rows"])
 
 
-@pytest.mark.parametrize("kernel", [0, 2])
+@pytest.mark.parametrize("kernel", [0, 1, 2])
 @pytest.mark.parametrize("splits", [0, 1, 3])
 def test_tree_verify_attention_bf16_golden(golden, kernel, splits):
+    """kernel 1 = tcgen05 (d = 128 cases), 2 = SIMT, 0 = auto."""
     from paper_2508_08192_b200.attention import tree_verify_attention
 
     g = golden("attention_gqa")
     for name in g["names"]:
         c = _gqa_case(g, str(name), torch.bfloat16)
+        if kernel == 1 and c["d"] != 128:
+            continue
         out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
                                          c["nr"], c["d"] ** -0.5, num_splits=splits, kernel=kernel)
         torch.cuda.synchronize()
@@ -467,3 +470,67 @@ def test_paged_cache_and_compaction_golden(golden):
                    _cuda(pt, torch.int32), _cuda([len(path)], torch.int32), _cuda([kept], torch.int32))
         np.testing.assert_array_equal(kpool.cpu().numpy(), want_k.astype(np.float32))
         np.testing.assert_array_equal(vpool.cpu().numpy(), want_v.astype(np.float32))
+
+
+def _rand_paged_case(B, Hq, Hkv, d, C_max, bs, parent_raw, seed, ragged=True):
+    from paper_2508_08192_b200.drafttree import tree_build
+
+    rng = np.random.default_rng(seed)
+    aug = O.augment(tuple(parent_raw))
+    R = len(aug)
+    ctx = (rng.integers(C_max // 2, C_max + 1, size=B) if ragged else np.full(B, C_max)).astype(np.int32)
+    pages = -(-(C_max + R) // bs)
+    nb = B * pages + 5
+    table = rng.permutation(nb)[:B * pages].reshape(B, pages).astype(np.int32)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    kp = torch.randn((nb, Hkv, bs, d), generator=gen, device="cuda").to(torch.bfloat16)
+    vp = torch.randn((nb, Hkv, bs, d), generator=gen, device="cuda").to(torch.bfloat16)
+    q = torch.randn((B, R, Hq, d), generator=gen, device="cuda").to(torch.bfloat16)
+    tk = torch.randn((B, R, Hkv, d), generator=gen, device="cuda").to(torch.bfloat16)
+    tv = torch.randn((B, R, Hkv, d), generator=gen, device="cuda").to(torch.bfloat16)
+    par = torch.tensor([list(aug)] * B, dtype=torch.int32, device="cuda")
+    nr = torch.full((B,), R, dtype=torch.int32, device="cuda")
+    ctx_t = torch.tensor(ctx, device="cuda")
+    mask, _, _, _ = tree_build(par, nr, ctx_t)
+    return dict(q=q, kp=kp, vp=vp, tk=tk, tv=tv, table=torch.tensor(table, device="cuda"), ctx=ctx_t, mask=mask,
+                nr=nr, aug=aug, ctx_np=ctx, table_np=table, R=R)
+
+
+TREE64 = [-1, -1, -1, -1, -1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5, 5, 6, 7,
+          8, 8, 8, 8, 9, 9, 9, 10, 10, 10, 11, 11, 12, 13, 14, 15, 32, 32, 32, 33, 33, 34, 34, 35, 36, 37, 48, 48, 49,
+          50, 51]
+
+
+@pytest.mark.parametrize("bs,splits", [(64, 1), (16, 3), (128, 0)])
+def test_tcgen05_llama70b_shapes_vs_oracle(bs, splits):
+    """70B attention shapes (64q/8kv, d128, 64-row tree) at 8k ragged context
+    through the tcgen05 kernel vs the float64 oracle (bf16 tolerance)."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    c = _rand_paged_case(2, 64, 8, 128, 8192, bs, TREE64, seed=11)
+    out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                     c["nr"], 128 ** -0.5, num_splits=splits, kernel=1)
+    torch.cuda.synchronize()
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(c["q"]), f64(c["kp"]), f64(c["vp"]), c["table_np"],
+                                                   c["ctx_np"], f64(c["tk"]), f64(c["tv"]), [c["aug"]] * 2,
+                                                   128 ** -0.5)
+    got_o = out.float().cpu().numpy()
+    err = np.abs(got_o - want_o)
+    assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+    assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
+
+
+def test_tcgen05_matches_simt_on_device():
+    """Same inputs through both device kernels (larger batch, chain and N8 trees)."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    for tree, hq, hkv in (([-1, 0, 1], 64, 8), ([-1, -1, 0, 0, 1, 2, 2, 5], 32, 8), (TREE64, 16, 16)):
+        c = _rand_paged_case(5, hq, hkv, 128, 3000, 32, tree, seed=len(tree))
+        o1, l1 = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                       c["nr"], 0.088, kernel=1)
+        o2, l2 = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                       c["nr"], 0.088, kernel=2)
+        torch.cuda.synchronize()
+        assert (o1.float() - o2.float()).abs().max().item() < 2e-2
+        assert (l1 - l2).abs().max().item() < 2e-3

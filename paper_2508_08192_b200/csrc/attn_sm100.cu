@@ -394,73 +394,85 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
     float m = -INFINITY, l = 0.f;
     const int n_pref_it = t_end_pref - t_begin;
     for (int it = 0; it < n_tiles; ++it) {
-      mbar_wait(&sm.s_full[t], it & 1);
-      tc_fence_after();
       const bool pref = it < n_pref_it;
       const int key0 = pref ? (t_begin + it) * kTileN : (it - n_pref_it) * kTileN;  // prefix key / suffix row
       const int kvalid = pref ? C - key0 : n_nodes - key0;                         // keys valid in this tile
-      uint32_t mw[4] = {0u, 0u, 0u, 0u};
-      if (!pref) {
+      const bool full = pref && kvalid >= kTileN;
+      // visibility bits of the 128 columns: prefix -> keys < ctx; suffix ->
+      // ancestor-or-self bits of this row's node (tree_build mask words)
+      uint32_t vm[4];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
+      for (int w = 0; w < 4; ++w) {
+        const int lim = kvalid - 32 * w;
+        const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+        uint32_t bits = 0xffffffffu;
+        if (!pref) {
           const int wi = (key0 >> 5) + w;
-          mw[w] = (wi < p.n_words && row_ok) ? mrow[wi] : 0u;
+          bits = (wi < p.n_words && row_ok) ? mrow[wi] : 0u;
         }
+        vm[w] = bits & low;
       }
-      auto visible = [&](int col) -> bool {
-        if (col >= kvalid) return false;
-        if (pref) return true;
-        return (mw[col >> 5] >> (col & 31)) & 1u;
-      };
-      // pass A: tile row max
-      float mx = -INFINITY;
+      mbar_wait(&sm.s_full[t], it & 1);
+      tc_fence_after();
+      // the whole S row (128 fp32) in registers: one TMEM pass
+      uint32_t r[128];
+      SDB_TMEM_LD32(t_s + 0, (r + 0));
+      SDB_TMEM_LD32(t_s + 32, (r + 32));
+      SDB_TMEM_LD32(t_s + 64, (r + 64));
+      SDB_TMEM_LD32(t_s + 96, (r + 96));
+      tmem_wait_ld();
+      if (!full) {
+        // invisible keys -> -inf (prefix tail beyond ctx, or not an ancestor)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        SDB_TMEM_LD32(t_s + c * 32, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float x = visible(c * 32 + e) ? __uint_as_float(r[e]) * sl2 : -INFINITY;
-          mx = fmaxf(mx, x);
-        }
+        for (int e = 0; e < 128; ++e)
+          if (!((vm[e >> 5] >> (e & 31)) & 1u)) r[e] = 0xff800000u;
       }
-      // lazy rescale of O / l when the running max grows by > 2^8
+      // row max with 8 independent chains, on raw scores (scale > 0)
+      float mx8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mx8[k] = __uint_as_float(r[k]);
+#pragma unroll
+      for (int e = 8; e < 128; e += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], __uint_as_float(r[e + k]));
+      }
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+      // lazy rescale: move the reference max only when it grows by > 2^8; the
+      // O / l correction is applied after P is written (frees the S registers)
+      float corr = 1.f;
+      bool rescale = false;
       if (it == 0) {
         m = mx;
       } else if (mx > m + kRescaleThreshold) {
-        const float corr = ex2(m - mx);
-        mbar_wait(&sm.o_done[t], (it - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          SDB_TMEM_LD32(t_o + c * 32, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * corr);
-          SDB_TMEM_ST32(t_o + c * 32, r);
-        }
-        l *= corr;
+        corr = ex2(m - mx);
+        rescale = true;
         m = mx;
       }
-      const float mu = (m == -INFINITY) ? 0.f : m;
-      // pass B: P = exp2(x - m), packed bf16 over the consumed S columns
+      const float neg_mu = (m == -INFINITY) ? 0.f : -m;
+      // P = exp2(s * scale_log2 - m), packed bf16 in place into r[0..63]
+      float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        SDB_TMEM_LD32(t_s + c * 32, r);
-        tmem_wait_ld();
-        uint32_t pk[16];
+      for (int e = 0; e < 128; e += 2) {
+        const float p0 = ex2(fmaf(__uint_as_float(r[e]), sl2, neg_mu));
+        const float p1 = ex2(fmaf(__uint_as_float(r[e + 1]), sl2, neg_mu));
+        l8[(e >> 1) & 7] += p0 + p1;
+        r[e >> 1] = pack_bf16(p0, p1);
+      }
+      l = l * corr + (((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7])));
+      SDB_TMEM_ST32(t_s + 0, (r + 0));
+      SDB_TMEM_ST32(t_s + 32, (r + 32));
+      if (rescale) {
+        // PV(it-1) has completed: s_full(it) was committed after it
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int c0 = c * 32 + 2 * e;
-          const float p0 = visible(c0) ? ex2(__uint_as_float(r[2 * e]) * sl2 - mu) : 0.f;
-          const float p1 = visible(c0 + 1) ? ex2(__uint_as_float(r[2 * e + 1]) * sl2 - mu) : 0.f;
-          l += p0 + p1;
-          pk[e] = pack_bf16(p0, p1);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          SDB_TMEM_LD32(t_o + c * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+          SDB_TMEM_ST32(t_o + c * 32, o);
         }
-        SDB_TMEM_ST16(t_s + c * 16, pk);
       }
       tmem_wait_st();
       tc_fence_before();

@@ -44,7 +44,8 @@ __device__ __forceinline__ void store_partial(const TreeAttnParams &p, int split
 template <typename T>
 int launch_tree_attn_simt(const TreeAttnParams &p, cudaStream_t stream);
 int launch_tree_attn_combine_bf16(const TreeAttnParams &p, cudaStream_t stream);
-int launch_tree_attn_sm100(const TreeAttnParams &p, cudaStream_t stream);
+int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *workspace, cudaStream_t stream);
+int64_t tree_attn_sm100_workspace(const TreeAttnParams &p, int ctas_override);
 bool tree_attn_sm100_supported(const TreeAttnParams &p);
 
 }  // namespace sdb

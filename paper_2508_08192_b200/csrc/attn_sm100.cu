@@ -22,6 +22,9 @@
 //               to bf16 and written back over S with tcgen05.st.
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) fp32 columns.
 #include <cuda.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "attn_internal.cuh"
 
@@ -157,6 +160,64 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return r;
 }
 
+// ---- packed fp32x2 math (FFMA2 / FADD2) and 3-input max (FMNMX3), sm_100 ----
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// exp2 of two values on the FMA pipe (offloads the MUFU): 2^x = 2^floor(x) *
+// p(frac(x)), p a cubic fit of 2^f on [0, 1) with p(0) = 1 (max relative
+// error 8.6e-5, far below the bf16 rounding of P).
+__device__ __forceinline__ void ex2_emu2(float x, float y, float &ox, float &oy) {
+  constexpr float kRound = 12582912.0f;  // 2^23 + 2^22
+  const uint64_t xy = f2pack(fmaxf(x, -127.f), fmaxf(y, -127.f));
+  const uint64_t rr = fadd2_rm(xy, f2pack(kRound, kRound));  // floor(x) in the low mantissa bits
+  const uint64_t fl = fadd2(rr, f2pack(-kRound, -kRound));
+  float fx, fy;
+  {
+    float a, b, c, d;
+    f2unpack(xy, a, b);
+    f2unpack(fl, c, d);
+    fx = a - c;
+    fy = b - d;
+  }
+  const uint64_t f = f2pack(fx, fy);
+  uint64_t pp = f2pack(0.07706617563962936f, 0.07706617563962936f);
+  pp = ffma2(pp, f, f2pack(0.22764593362808228f, 0.22764593362808228f));
+  pp = ffma2(pp, f, f2pack(0.6951165795326233f, 0.6951165795326233f));
+  pp = ffma2(pp, f, f2pack(1.0f, 1.0f));
+  float px, py, rx, ry;
+  f2unpack(pp, px, py);
+  f2unpack(rr, rx, ry);
+  ox = __uint_as_float(__float_as_uint(px) + (__float_as_uint(rx) << 23));
+  oy = __uint_as_float(__float_as_uint(py) + (__float_as_uint(ry) << 23));
+}
+
 // Shared-memory matrix descriptor (SM100 UMMA, version 1, 128-byte swizzle).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -179,21 +240,90 @@ __host__ __device__ constexpr uint32_t make_idesc(bool b_mn_major) {
 
 struct Sm100Params {
   TreeAttnParams p;
-  int m_blocks;  // CTA row blocks per (b, kvh)
+  int m_blocks;    // row blocks (NT x 128 query rows) per (b, kvh)
+  int units;       // batch * hkv * m_blocks
+  int w_pref;      // nominal prefix tiles per unit: ceil(max_ctx / 128)
+  int w_unit;      // nominal tiles per unit: w_pref + ceil(r_max / 128)
+  int n_ctas;      // persistent CTAs (stream-K partition of units * w_unit tiles)
+  int rows_unit;   // NT * 128
+  int64_t total;   // units * w_unit
+  float *part_out; // [n_ctas * 2][rows_unit][128] partial outputs of split units
+  float *part_lse; // [n_ctas * 2][rows_unit]
 };
+
+__host__ __device__ __forceinline__ int64_t seg_begin(const Sm100Params &sp, int k) {
+  return sp.total * k / sp.n_ctas;
+}
+
+// One contiguous piece of a unit's nominal tile range owned by a CTA.
+struct Item {
+  int unit, t0, t1, slot;
+  bool whole;
+};
+
+// i-th item of CTA k (items walk the CTA's [seg_begin(k), seg_begin(k+1)) range).
+struct ItemIter {
+  int64_t cur, end;
+  int idx, k;
+  __device__ ItemIter(const Sm100Params &sp, int k_) : idx(0), k(k_) {
+    cur = seg_begin(sp, k_);
+    end = seg_begin(sp, k_ + 1);
+  }
+  __device__ bool next(const Sm100Params &sp, Item &it) {
+    if (cur >= end) return false;
+    it.unit = (int)(cur / sp.w_unit);
+    it.t0 = (int)(cur % sp.w_unit);
+    it.t1 = (int)min((int64_t)sp.w_unit, it.t0 + (end - cur));
+    it.whole = it.t0 == 0 && it.t1 == sp.w_unit;
+    cur += it.t1 - it.t0;
+    it.slot = k * 2 + (idx == 0 ? 0 : 1);
+    ++idx;
+    return true;
+  }
+};
+
+// Per-item geometry: which (b, kvh, rows) and which actual KV tiles.
+struct ItemGeo {
+  int b, kvh, row0, n_nodes, rows_total, C;
+  int pa, n_pref, sa, n_suf, n_tiles;
+  bool active;
+};
+
+__device__ __forceinline__ ItemGeo item_geo(const Sm100Params &sp, const Item &it, int g) {
+  const TreeAttnParams &p = sp.p;
+  ItemGeo o;
+  const int per_b = p.hkv * sp.m_blocks;
+  o.b = it.unit / per_b;
+  o.kvh = (it.unit % per_b) / sp.m_blocks;
+  o.row0 = (it.unit % sp.m_blocks) * sp.rows_unit;
+  o.n_nodes = min(p.n_rows[o.b], p.r_max);
+  o.rows_total = o.n_nodes * g;
+  o.C = p.ctx_len[o.b];
+  const int pb = (o.C + kTileN - 1) / kTileN;
+  const int sb = (o.n_nodes + kTileN - 1) / kTileN;
+  o.pa = min(it.t0, pb);
+  const int pe = min(min(it.t1, sp.w_pref), pb);
+  o.n_pref = max(0, pe - o.pa);
+  o.sa = min(max(it.t0 - sp.w_pref, 0), sb);
+  const int se = min(max(it.t1 - sp.w_pref, 0), sb);
+  o.n_suf = max(0, se - o.sa);
+  o.n_tiles = o.n_pref + o.n_suf;
+  o.active = o.n_tiles > 0 && o.row0 < o.rows_total;
+  return o;
+}
 
 template <int NT>
 struct alignas(1024) Smem {
   uint8_t q[NT][kTileBytes];
   uint8_t k[2][kTileBytes];
   uint8_t v[2][kTileBytes];
-  uint64_t q_full;
+  uint64_t q_full, q_empty;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[NT], p_full[NT], o_done[NT];
+  uint64_t s_full[NT], p_full[NT], o_done[NT], o_free[NT];
   uint32_t tmem_base;
 };
 
-template <int NT>
+template <int NT, int EMU>
 __global__ void __launch_bounds__(128 + NT * 128, 1)
     tree_attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_tk,
@@ -202,48 +332,12 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
   Smem<NT> &sm = *reinterpret_cast<Smem<NT> *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const TreeAttnParams &p = sp.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int split = blockIdx.x, mblk = blockIdx.y;
-  const int b = blockIdx.z / p.hkv, kvh = blockIdx.z % p.hkv;
   const int g = p.hq / p.hkv;
-  const int n_nodes = min(p.n_rows[b], p.r_max);
-  const int rows_total = n_nodes * g;
-  const int row0 = mblk * NT * kTileM;
-  const int C = p.ctx_len[b];
-  const int n_pref_tiles = (C + kTileN - 1) / kTileN;
-  const int n_suf_tiles = (n_nodes + kTileN - 1) / kTileN;
-  const int tiles_per = (n_pref_tiles + p.num_splits - 1) / p.num_splits;
-  const int t_begin = min(split * tiles_per, n_pref_tiles);
-  const int t_end_pref = min(t_begin + tiles_per, n_pref_tiles);
-  const bool last_split = split == p.num_splits - 1;
-  const int n_tiles = (t_end_pref - t_begin) + (last_split ? n_suf_tiles : 0);
   const float sl2 = p.scale * 1.4426950408889634f;
-
-  // Whole CTA is padding, or this split has no keys: write zeros / -inf.
-  if (row0 >= rows_total || n_tiles == 0) {
-    if (threadIdx.x >= 128) {
-      const int i = threadIdx.x - 128;  // 0 .. NT*128-1
-      const int rho = row0 + i;
-      const bool in_range = rho < p.r_max * g;
-      if (in_range && (p.num_splits > 1 || rho >= rows_total)) {
-        const int node = rho / g, hq_idx = kvh * g + rho % g;
-        if (p.num_splits == 1) {
-          __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) + (((int64_t)b * p.r_max + node) * p.hq + hq_idx) * kHeadDim;
-          for (int c = 0; c < kHeadDim; c += 8) *reinterpret_cast<uint4 *>(o + c) = make_uint4(0, 0, 0, 0);
-          if (p.lse) p.lse[((int64_t)b * p.hq + hq_idx) * p.r_max + node] = -INFINITY;
-        } else {
-          const int64_t total = (int64_t)p.batch * p.r_max * p.hq;
-          const int64_t wid = ((int64_t)b * p.r_max + node) * p.hq + hq_idx;
-          float *o = p.ws_out + (split * total + wid) * kHeadDim;
-          for (int c = 0; c < kHeadDim; c += 4) *reinterpret_cast<float4 *>(o + c) = make_float4(0, 0, 0, 0);
-          p.ws_lse[(int64_t)split * total + ((int64_t)b * p.hq + hq_idx) * p.r_max + node] = -INFINITY;
-        }
-      }
-    }
-    return;
-  }
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.q_full, 1);
+    mbar_init(&sm.q_empty, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.k_empty[s], 1);
@@ -254,6 +348,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
       mbar_init(&sm.s_full[t], 1);
       mbar_init(&sm.p_full[t], 128);
       mbar_init(&sm.o_done[t], 1);
+      mbar_init(&sm.o_free[t], 128);
     }
     fence_barrier_init();
   }
@@ -274,54 +369,51 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
       tma_prefetch(&tm_v);
       tma_prefetch(&tm_tk);
       tma_prefetch(&tm_tv);
-      // Q: NT tiles x 2 column chunks; box = {64, g, 1, 128/g} over
-      // [B*R, Hkv, g, d] -> rows (node, j) of this KV head.
-      mbar_expect_tx(&sm.q_full, NT * kTileBytes);
-      const int nodes_per_tile = kTileM / g;
-      for (int t = 0; t < NT; ++t) {
-        const int node0 = (row0 + t * kTileM) / g;
-        for (int c = 0; c < 2; ++c)
-          tma_load_4d(sm.q[t] + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, 0, kvh, b * p.r_max + node0);
-      }
-      (void)nodes_per_tile;
       const int bs = p.block_size;
       const int pages_per_tile = kTileN / bs;
-      const int n_valid_pages = (C + bs - 1) / bs;
-      const int32_t *bt = p.block_table + (int64_t)b * p.max_blocks;
-      for (int it = 0; it < n_tiles; ++it) {
-        const int s = it & 1;
-        const uint32_t ph = (it >> 1) & 1;
-        const bool pref = it < (t_end_pref - t_begin);
-        const int tile = t_begin + it;
-        // K
-        mbar_wait(&sm.k_empty[s], ph ^ 1);
-        mbar_expect_tx(&sm.k_full[s], kTileBytes);
-        if (pref) {
-          for (int pg = 0; pg < pages_per_tile; ++pg) {
-            const int lp = tile * pages_per_tile + pg;
-            const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;  // OOB page -> zero fill
-            const int rowc = (page * p.hkv + kvh) * bs;
-            for (int c = 0; c < 2; ++c) tma_load_2d(sm.k[s] + c * kChunkBytes + pg * bs * 128, &tm_k, &sm.k_full[s], c * 64, rowc);
-          }
-        } else {
-          const int st = it - (t_end_pref - t_begin);
+      uint32_t g_tile = 0, g_q = 0;
+      ItemIter iter(sp, blockIdx.x);
+      Item item;
+      while (iter.next(sp, item)) {
+        const ItemGeo geo = item_geo(sp, item, g);
+        if (!geo.active) continue;
+        // Q tiles of this unit once the previous unit's S MMAs are done
+        mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
+        mbar_expect_tx(&sm.q_full, NT * kTileBytes);
+        for (int t = 0; t < NT; ++t) {
+          const int node0 = (geo.row0 + t * kTileM) / g;
           for (int c = 0; c < 2; ++c)
-            tma_load_3d(sm.k[s] + c * kChunkBytes, &tm_tk, &sm.k_full[s], c * 64, kvh, b * p.r_max + st * kTileN);
+            tma_load_4d(sm.q[t] + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, 0, geo.kvh,
+                        geo.b * p.r_max + node0);
         }
-        // V
-        mbar_wait(&sm.v_empty[s], ph ^ 1);
-        mbar_expect_tx(&sm.v_full[s], kTileBytes);
-        if (pref) {
-          for (int pg = 0; pg < pages_per_tile; ++pg) {
-            const int lp = tile * pages_per_tile + pg;
-            const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;
-            const int rowc = (page * p.hkv + kvh) * bs;
-            for (int c = 0; c < 2; ++c) tma_load_2d(sm.v[s] + c * kChunkBytes + pg * bs * 128, &tm_v, &sm.v_full[s], c * 64, rowc);
+        ++g_q;
+        const int n_valid_pages = (geo.C + bs - 1) / bs;
+        const int32_t *bt = p.block_table + (int64_t)geo.b * p.max_blocks;
+        for (int it = 0; it < geo.n_tiles; ++it, ++g_tile) {
+          const int s = g_tile & 1;
+          const uint32_t ph = (g_tile >> 1) & 1;
+          const bool pref = it < geo.n_pref;
+          const int tile = pref ? geo.pa + it : geo.sa + (it - geo.n_pref);
+          for (int kv = 0; kv < 2; ++kv) {
+            uint64_t *emp = kv ? &sm.v_empty[s] : &sm.k_empty[s];
+            uint64_t *ful = kv ? &sm.v_full[s] : &sm.k_full[s];
+            uint8_t *dst = kv ? sm.v[s] : sm.k[s];
+            mbar_wait(emp, ph ^ 1);
+            mbar_expect_tx(ful, kTileBytes);
+            if (pref) {
+              const CUtensorMap *m = kv ? &tm_v : &tm_k;
+              for (int pg = 0; pg < pages_per_tile; ++pg) {
+                const int lp = tile * pages_per_tile + pg;
+                const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;  // OOB page -> zero fill
+                const int rowc = (page * p.hkv + geo.kvh) * bs;
+                for (int c = 0; c < 2; ++c) tma_load_2d(dst + c * kChunkBytes + pg * bs * 128, m, ful, c * 64, rowc);
+              }
+            } else {
+              const CUtensorMap *m = kv ? &tm_tv : &tm_tk;
+              for (int c = 0; c < 2; ++c)
+                tma_load_3d(dst + c * kChunkBytes, m, ful, c * 64, geo.kvh, geo.b * p.r_max + tile * kTileN);
+            }
           }
-        } else {
-          const int st = it - (t_end_pref - t_begin);
-          for (int c = 0; c < 2; ++c)
-            tma_load_3d(sm.v[s] + c * kChunkBytes, &tm_tv, &sm.v_full[s], c * 64, kvh, b * p.r_max + st * kTileN);
         }
       }
     }
@@ -348,36 +440,47 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
                  idesc_o, (acc || k > 0) ? 1u : 0u);
         }
       };
-      mbar_wait(&sm.q_full, 0);
-      mbar_wait(&sm.k_full[0], 0);
-      tc_fence_after();
-      for (int t = 0; t < NT; ++t) {
-        issue_s(t, 0);
-        tc_commit(&sm.s_full[t]);
-      }
-      tc_commit(&sm.k_empty[0]);
-      for (int it = 0; it < n_tiles; ++it) {
-        const int s = it & 1;
-        const uint32_t ph = (it >> 1) & 1;
-        mbar_wait(&sm.v_full[s], ph);
+      uint32_t g_tile = 0, g_q = 0;
+      ItemIter iter(sp, blockIdx.x);
+      Item item;
+      while (iter.next(sp, item)) {
+        const ItemGeo geo = item_geo(sp, item, g);
+        if (!geo.active) continue;
+        mbar_wait(&sm.q_full, g_q & 1);
+        mbar_wait(&sm.k_full[g_tile & 1], (g_tile >> 1) & 1);
         tc_fence_after();
         for (int t = 0; t < NT; ++t) {
-          mbar_wait(&sm.p_full[t], it & 1);
-          tc_fence_after();
-          issue_pv(t, s, it > 0);
-          tc_commit(&sm.o_done[t]);
-          if (it + 1 < n_tiles) {
-            const int s2 = (it + 1) & 1;
-            if (t == 0) {
-              mbar_wait(&sm.k_full[s2], ((it + 1) >> 1) & 1);
-              tc_fence_after();
-            }
-            issue_s(t, s2);
-            tc_commit(&sm.s_full[t]);
-            if (t == NT - 1) tc_commit(&sm.k_empty[s2]);
-          }
+          issue_s(t, g_tile & 1);
+          tc_commit(&sm.s_full[t]);
         }
-        tc_commit(&sm.v_empty[s]);
+        tc_commit(&sm.k_empty[g_tile & 1]);
+        for (int it = 0; it < geo.n_tiles; ++it) {
+          const uint32_t gt = g_tile + it;
+          const int s = gt & 1;
+          mbar_wait(&sm.v_full[s], (gt >> 1) & 1);
+          tc_fence_after();
+          for (int t = 0; t < NT; ++t) {
+            mbar_wait(&sm.p_full[t], gt & 1);
+            if (it == 0) mbar_wait(&sm.o_free[t], (g_q & 1) ^ 1);  // previous unit's epilogue read O_t
+            tc_fence_after();
+            issue_pv(t, s, it > 0);
+            tc_commit(&sm.o_done[t]);
+            if (it + 1 < geo.n_tiles) {
+              const int s2 = (gt + 1) & 1;
+              if (t == 0) {
+                mbar_wait(&sm.k_full[s2], ((gt + 1) >> 1) & 1);
+                tc_fence_after();
+              }
+              issue_s(t, s2);
+              tc_commit(&sm.s_full[t]);
+              if (t == NT - 1) tc_commit(&sm.k_empty[s2]);
+            }
+          }
+          tc_commit(&sm.v_empty[s]);
+        }
+        tc_commit(&sm.q_empty);  // all S MMAs of this unit read Q
+        g_tile += geo.n_tiles;
+        ++g_q;
       }
     }
   } else if (warp >= 4) {
@@ -387,145 +490,179 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t t_s = tmem + lane_off + t * 128;
     const uint32_t t_o = tmem + lane_off + 256 + t * 128;
-    const int rho = row0 + t * kTileM + i;
-    const bool row_ok = rho < rows_total;
-    const int node = min(rho / g, max(n_nodes - 1, 0));
-    const uint32_t *mrow = p.mask_words + ((int64_t)b * p.r_max + node) * p.n_words;
-    float m = -INFINITY, l = 0.f;
-    const int n_pref_it = t_end_pref - t_begin;
-    for (int it = 0; it < n_tiles; ++it) {
-      const bool pref = it < n_pref_it;
-      const int key0 = pref ? (t_begin + it) * kTileN : (it - n_pref_it) * kTileN;  // prefix key / suffix row
-      const int kvalid = pref ? C - key0 : n_nodes - key0;                         // keys valid in this tile
-      const bool full = pref && kvalid >= kTileN;
-      // visibility bits of the 128 columns: prefix -> keys < ctx; suffix ->
-      // ancestor-or-self bits of this row's node (tree_build mask words)
-      uint32_t vm[4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const int lim = kvalid - 32 * w;
-        const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
-        uint32_t bits = 0xffffffffu;
-        if (!pref) {
-          const int wi = (key0 >> 5) + w;
-          bits = (wi < p.n_words && row_ok) ? mrow[wi] : 0u;
+    const int local = t * kTileM + i;  // row within the unit
+    uint32_t g_tile = 0;
+    ItemIter iter(sp, blockIdx.x);
+    Item item;
+    while (iter.next(sp, item)) {
+      const ItemGeo geo = item_geo(sp, item, g);
+      const int rho = geo.row0 + local;
+      const bool row_ok = rho < geo.rows_total;
+      const bool in_range = rho < p.r_max * g;
+      const int node_o = rho / g;
+      const int hq_idx = geo.kvh * g + (rho % g);
+      if (!geo.active) {
+        // padding rows / an empty split piece: zeros and -inf
+        if (!item.whole) {
+          float *o = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim;
+          for (int c = 0; c < kHeadDim; c += 4) *reinterpret_cast<float4 *>(o + c) = make_float4(0, 0, 0, 0);
+          sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = -INFINITY;
+        } else if (in_range) {
+          __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
+                             (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim;
+          for (int c = 0; c < kHeadDim; c += 8) *reinterpret_cast<uint4 *>(o + c) = make_uint4(0, 0, 0, 0);
+          if (p.lse) p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = -INFINITY;
         }
-        vm[w] = bits & low;
+        continue;
       }
-      mbar_wait(&sm.s_full[t], it & 1);
-      tc_fence_after();
-      // the whole S row (128 fp32) in registers: one TMEM pass
-      uint32_t r[128];
-      SDB_TMEM_LD32(t_s + 0, (r + 0));
-      SDB_TMEM_LD32(t_s + 32, (r + 32));
-      SDB_TMEM_LD32(t_s + 64, (r + 64));
-      SDB_TMEM_LD32(t_s + 96, (r + 96));
-      tmem_wait_ld();
-      if (!full) {
-        // invisible keys -> -inf (prefix tail beyond ctx, or not an ancestor)
+      const int node = min(rho / g, max(geo.n_nodes - 1, 0));
+      const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
+      float m = -INFINITY, l = 0.f;
+      for (int it = 0; it < geo.n_tiles; ++it) {
+        const uint32_t gt = g_tile + it;
+        const bool pref = it < geo.n_pref;
+        const int key0 = pref ? (geo.pa + it) * kTileN : (geo.sa + it - geo.n_pref) * kTileN;
+        const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
+        const bool full = pref && kvalid >= kTileN;
+        // visibility bits of the 128 columns: prefix -> keys < ctx; suffix ->
+        // ancestor-or-self bits of this row's node (tree_build mask words)
+        uint32_t vm[4];
 #pragma unroll
-        for (int e = 0; e < 128; ++e)
-          if (!((vm[e >> 5] >> (e & 31)) & 1u)) r[e] = 0xff800000u;
-      }
-      // row max with 8 independent chains, on raw scores (scale > 0)
-      float mx8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mx8[k] = __uint_as_float(r[k]);
-#pragma unroll
-      for (int e = 8; e < 128; e += 8) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], __uint_as_float(r[e + k]));
-      }
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
-      // lazy rescale: move the reference max only when it grows by > 2^8; the
-      // O / l correction is applied after P is written (frees the S registers)
-      float corr = 1.f;
-      bool rescale = false;
-      if (it == 0) {
-        m = mx;
-      } else if (mx > m + kRescaleThreshold) {
-        corr = ex2(m - mx);
-        rescale = true;
-        m = mx;
-      }
-      const float neg_mu = (m == -INFINITY) ? 0.f : -m;
-      // P = exp2(s * scale_log2 - m), packed bf16 in place into r[0..63]
-      float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int e = 0; e < 128; e += 2) {
-        const float p0 = ex2(fmaf(__uint_as_float(r[e]), sl2, neg_mu));
-        const float p1 = ex2(fmaf(__uint_as_float(r[e + 1]), sl2, neg_mu));
-        l8[(e >> 1) & 7] += p0 + p1;
-        r[e >> 1] = pack_bf16(p0, p1);
-      }
-      l = l * corr + (((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7])));
-      SDB_TMEM_ST32(t_s + 0, (r + 0));
-      SDB_TMEM_ST32(t_s + 32, (r + 32));
-      if (rescale) {
-        // PV(it-1) has completed: s_full(it) was committed after it
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          SDB_TMEM_LD32(t_o + c * 32, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-          SDB_TMEM_ST32(t_o + c * 32, o);
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&sm.p_full[t]);
-    }
-    // epilogue: wait for the last PV, normalise, store
-    mbar_wait(&sm.o_done[t], (n_tiles - 1) & 1);
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    const float lse_n = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
-    const int hq_idx = kvh * g + (rho % g);
-    const int node_o = rho / g;
-    const bool in_range = rho < p.r_max * g;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t r[32];
-      SDB_TMEM_LD32(t_o + c * 32, r);
-      tmem_wait_ld();
-      if (!in_range) continue;
-      if (p.num_splits == 1) {
-        __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
-                           (((int64_t)b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim + c * 32;
-#pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          uint4 v;
-          if (row_ok) {
-            v.x = pack_bf16(__uint_as_float(r[e + 0]) * inv, __uint_as_float(r[e + 1]) * inv);
-            v.y = pack_bf16(__uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
-            v.z = pack_bf16(__uint_as_float(r[e + 4]) * inv, __uint_as_float(r[e + 5]) * inv);
-            v.w = pack_bf16(__uint_as_float(r[e + 6]) * inv, __uint_as_float(r[e + 7]) * inv);
-          } else {
-            v = make_uint4(0, 0, 0, 0);
+        for (int w = 0; w < 4; ++w) {
+          const int lim = kvalid - 32 * w;
+          const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+          uint32_t bits = 0xffffffffu;
+          if (!pref) {
+            const int wi = (key0 >> 5) + w;
+            bits = (wi < p.n_words && row_ok) ? mrow[wi] : 0u;
           }
-          *reinterpret_cast<uint4 *>(o + e) = v;
+          vm[w] = bits & low;
         }
-      } else if (row_ok) {
-        const int64_t total = (int64_t)p.batch * p.r_max * p.hq;
-        const int64_t wid = ((int64_t)b * p.r_max + node_o) * p.hq + hq_idx;
-        float *o = p.ws_out + (split * total + wid) * kHeadDim + c * 32;
+        mbar_wait(&sm.s_full[t], gt & 1);
+        tc_fence_after();
+        uint32_t r[128];
+        SDB_TMEM_LD32(t_s + 0, (r + 0));
+        SDB_TMEM_LD32(t_s + 32, (r + 32));
+        SDB_TMEM_LD32(t_s + 64, (r + 64));
+        SDB_TMEM_LD32(t_s + 96, (r + 96));
+        tmem_wait_ld();
+        if (!full) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 4)
-          *reinterpret_cast<float4 *>(o + e) =
-              make_float4(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv,
-                          __uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+          for (int e = 0; e < 128; ++e)
+            if (!((vm[e >> 5] >> (e & 31)) & 1u)) r[e] = 0xff800000u;
+        }
+        // row max on raw scores (scale > 0): 4 chains of 3-input max
+        float c0 = fmaxf(__uint_as_float(r[0]), __uint_as_float(r[1]));
+        float c1 = fmaxf(__uint_as_float(r[2]), __uint_as_float(r[3]));
+        float c2 = fmaxf(__uint_as_float(r[4]), __uint_as_float(r[5]));
+        float c3 = fmaxf(__uint_as_float(r[6]), __uint_as_float(r[7]));
+#pragma unroll
+        for (int e = 8; e < 128; e += 8) {
+          c0 = fmax3(c0, __uint_as_float(r[e + 0]), __uint_as_float(r[e + 1]));
+          c1 = fmax3(c1, __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+          c2 = fmax3(c2, __uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
+          c3 = fmax3(c3, __uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
+        }
+        const float mx = fmax3(fmaxf(c0, c1), c2, c3) * sl2;
+        // lazy rescale: move the reference max only when it grows by > 2^8; the
+        // O / l correction is applied after P is written (frees the S registers)
+        float corr = 1.f;
+        bool rescale = false;
+        if (it == 0) {
+          m = mx;
+        } else if (mx > m + kRescaleThreshold) {
+          corr = ex2(m - mx);
+          rescale = true;
+          m = mx;
+        }
+        const float neg_mu = (m == -INFINITY) ? 0.f : -m;
+        // P = exp2(s * scale_log2 - m) (FFMA2); EMU of every 4 pairs on the FMA
+        // pipe; row sum on FADD2; packed bf16 in place into r[0..63]
+        const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
+        uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          float x0, x1, p0, p1;
+          f2unpack(ffma2(f2pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
+          if ((e & 3) >= 4 - EMU) {
+            ex2_emu2(x0, x1, p0, p1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          acc2[e & 3] = fadd2(acc2[e & 3], f2pack(p0, p1));
+          r[e] = pack_bf16(p0, p1);
+        }
+        float s0, s1, s2, s3, s4, s5, s6, s7;
+        f2unpack(acc2[0], s0, s1);
+        f2unpack(acc2[1], s2, s3);
+        f2unpack(acc2[2], s4, s5);
+        f2unpack(acc2[3], s6, s7);
+        l = l * corr + (((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)));
+        SDB_TMEM_ST32(t_s + 0, (r + 0));
+        SDB_TMEM_ST32(t_s + 32, (r + 32));
+        if (rescale) {
+          // PV(it-1) has completed: s_full(it) was committed after it
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            SDB_TMEM_LD32(t_o + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            SDB_TMEM_ST32(t_o + c * 32, o);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[t]);
       }
-    }
-    if (in_range) {
-      if (p.num_splits == 1) {
-        if (p.lse) p.lse[((int64_t)b * p.hq + hq_idx) * p.r_max + node_o] = row_ok ? lse_n : -INFINITY;
-      } else if (row_ok) {
-        const int64_t total = (int64_t)p.batch * p.r_max * p.hq;
-        p.ws_lse[(int64_t)split * total + ((int64_t)b * p.hq + hq_idx) * p.r_max + node_o] = lse_n;
+      // epilogue: wait for the last PV, normalise, store (final or partial)
+      mbar_wait(&sm.o_done[t], (g_tile + geo.n_tiles - 1) & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const float lse_n = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        SDB_TMEM_LD32(t_o + c * 32, r);
+        tmem_wait_ld();
+        if (item.whole) {
+          if (!in_range) continue;
+          __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
+                             (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim + c * 32;
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 v;
+            if (row_ok) {
+              v.x = pack_bf16(__uint_as_float(r[e + 0]) * inv, __uint_as_float(r[e + 1]) * inv);
+              v.y = pack_bf16(__uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+              v.z = pack_bf16(__uint_as_float(r[e + 4]) * inv, __uint_as_float(r[e + 5]) * inv);
+              v.w = pack_bf16(__uint_as_float(r[e + 6]) * inv, __uint_as_float(r[e + 7]) * inv);
+            } else {
+              v = make_uint4(0, 0, 0, 0);
+            }
+            *reinterpret_cast<uint4 *>(o + e) = v;
+          }
+        } else {
+          float *o = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim + c * 32;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4 *>(o + e) =
+                make_float4(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv,
+                            __uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+        }
       }
+      // O_t may now be overwritten by the next unit's first PV
+      tc_fence_before();
+      mbar_arrive(&sm.o_free[t]);
+      if (item.whole) {
+        if (in_range && p.lse)
+          p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = row_ok ? lse_n : -INFINITY;
+      } else {
+        sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = row_ok ? lse_n : -INFINITY;
+      }
+      g_tile += geo.n_tiles;
     }
   }
   tc_fence_before();
@@ -535,6 +672,71 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+}
+
+// Stream-K fix-up: the slot holding the FIRST piece of a split unit merges
+// all pieces of that unit (same math as merge_partials, attention.py:108-124).
+// grid (n_ctas * 2, rows_unit / 4), 4 warps, one warp per row.
+__global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params sp) {
+  const TreeAttnParams &p = sp.p;
+  const int slot = blockIdx.x, k = slot >> 1, j = slot & 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int local = blockIdx.y * 4 + warp;
+  if (local >= sp.rows_unit) return;
+  const int64_t s = seg_begin(sp, k), e = seg_begin(sp, k + 1);
+  if (s >= e) return;
+  int unit, t0, t1;
+  if (j == 0) {
+    unit = (int)(s / sp.w_unit);
+    t0 = (int)(s % sp.w_unit);
+    t1 = (int)min((int64_t)sp.w_unit, t0 + (e - s));
+  } else {
+    unit = (int)((e - 1) / sp.w_unit);
+    if (unit == (int)(s / sp.w_unit)) return;  // single item: already slot 0
+    t0 = 0;
+    t1 = (int)(e - (int64_t)unit * sp.w_unit);
+  }
+  if (t0 != 0 || t1 == sp.w_unit) return;  // not the first piece of a split unit
+  const int g = p.hq / p.hkv;
+  const int per_b = p.hkv * sp.m_blocks;
+  const int b = unit / per_b, kvh = (unit % per_b) / sp.m_blocks;
+  const int rho = (unit % sp.m_blocks) * sp.rows_unit + local;
+  if (rho >= p.r_max * g) return;
+  const int n_nodes = min(p.n_rows[b], p.r_max);
+  const int node = rho / g, hq_idx = kvh * g + rho % g;
+  __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + (((int64_t)b * p.r_max + node) * p.hq + hq_idx) * kHeadDim;
+  float *lse_out = p.lse ? p.lse + ((int64_t)b * p.hq + hq_idx) * p.r_max + node : nullptr;
+  if (rho >= n_nodes * g) {
+    for (int c = lane * 4; c < kHeadDim; c += 128) *reinterpret_cast<uint2 *>(out + c) = make_uint2(0, 0);
+    if (lse_out && lane == 0) *lse_out = -INFINITY;
+    return;
+  }
+  const int64_t unit_end = (int64_t)(unit + 1) * sp.w_unit;
+  float mx = -INFINITY;
+  for (int kk = k; kk < sp.n_ctas && seg_begin(sp, kk) < unit_end; ++kk) {
+    const int sl = kk == k ? slot : kk * 2;
+    mx = fmaxf(mx, sp.part_lse[(int64_t)sl * sp.rows_unit + local]);
+  }
+  float wsum = 0.f;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int kk = k; kk < sp.n_ctas && seg_begin(sp, kk) < unit_end; ++kk) {
+    const int sl = kk == k ? slot : kk * 2;
+    const float l = sp.part_lse[(int64_t)sl * sp.rows_unit + local];
+    if (l == -INFINITY) continue;
+    const float w = __expf(l - mx);
+    wsum += w;
+    const float4 o = *reinterpret_cast<const float4 *>(sp.part_out + ((int64_t)sl * sp.rows_unit + local) * kHeadDim + lane * 4);
+    acc[0] = fmaf(w, o.x, acc[0]);
+    acc[1] = fmaf(w, o.y, acc[1]);
+    acc[2] = fmaf(w, o.z, acc[2]);
+    acc[3] = fmaf(w, o.w, acc[3]);
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  uint2 v;
+  v.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+  v.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+  *reinterpret_cast<uint2 *>(out + lane * 4) = v;
+  if (lse_out && lane == 0) *lse_out = wsum > 0.f ? mx + logf(wsum) : -INFINITY;
 }
 
 // ---------------------------------------------------------------------------
@@ -578,15 +780,41 @@ bool tree_attn_sm100_supported(const TreeAttnParams &p) {
        reinterpret_cast<uintptr_t>(p.v_cache) | reinterpret_cast<uintptr_t>(p.tree_k) |
        reinterpret_cast<uintptr_t>(p.tree_v)) & 15)
     return false;
-  if (p.n_words > 4) return false;  // suffix tile bit rows: <= 128 tree rows per tile word window
-  if (p.r_max > 128) return false;
+  if (p.r_max > 128) return false;  // one suffix tile (<= 4 mask words)
   int dev = 0, major = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   return major == 10 && sm100::encode_fn() != nullptr;
 }
 
-int launch_tree_attn_sm100(const TreeAttnParams &p, cudaStream_t stream) {
+// Stream-K plan: units x nominal tiles split evenly over the persistent CTAs.
+static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100Params &sp) {
+  using namespace sm100;
+  const int g = p.hq / p.hkv;
+  const int rows = p.r_max * g;
+  const int nt = rows > kTileM ? 2 : 1;
+  sp.p = p;
+  sp.rows_unit = nt * kTileM;
+  sp.m_blocks = cdiv(rows, sp.rows_unit);
+  sp.units = p.batch * p.hkv * sp.m_blocks;
+  sp.w_pref = cdiv(max(p.max_ctx, 0), kTileN);
+  sp.w_unit = sp.w_pref + cdiv(p.r_max, kTileN);
+  sp.total = (int64_t)sp.units * sp.w_unit;
+  int n = ctas_override > 0 ? ctas_override : num_sms();
+  // at least ~2 tiles per CTA
+  n = (int)std::max<int64_t>(1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : sp.total / 2));
+  sp.n_ctas = n;
+  sp.part_out = nullptr;
+  sp.part_lse = nullptr;
+}
+
+int64_t tree_attn_sm100_workspace(const TreeAttnParams &p, int ctas_override) {
+  sm100::Sm100Params sp;
+  sm100_plan(p, ctas_override, sp);
+  return (int64_t)sp.n_ctas * 2 * sp.rows_unit * (sm100::kHeadDim + 1) * (int64_t)sizeof(float) + 256;
+}
+
+int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *workspace, cudaStream_t stream) {
   using namespace sm100;
   const int g = p.hq / p.hkv;
   const int d = kHeadDim;
@@ -611,23 +839,33 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, cudaStream_t stream) {
     if (!make_map(&mtk, p.tree_k, 3, dims, strides, box)) return SDB_E_UNSUPPORTED;
     if (!make_map(&mtv, p.tree_v, 3, dims, strides, box)) return SDB_E_UNSUPPORTED;
   }
-  const int rows = p.r_max * g;
-  const int nt = rows > kTileM ? 2 : 1;
   Sm100Params sp;
-  sp.p = p;
-  sp.m_blocks = cdiv(rows, nt * kTileM);
-  dim3 grid(p.num_splits, sp.m_blocks, p.batch * p.hkv);
-  if (nt == 2) {
-    const size_t smem = sizeof(Smem<2>) + 1024;
-    cudaFuncSetAttribute(tree_attn_tcgen05_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tree_attn_tcgen05_kernel<2><<<grid, 384, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);
-  } else {
-    const size_t smem = sizeof(Smem<1>) + 1024;
-    cudaFuncSetAttribute(tree_attn_tcgen05_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tree_attn_tcgen05_kernel<1><<<grid, 256, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);
+  sm100_plan(p, ctas_override, sp);
+  sp.part_out = reinterpret_cast<float *>(workspace);
+  sp.part_lse = sp.part_out + (int64_t)sp.n_ctas * 2 * sp.rows_unit * kHeadDim;
+  static int emu = -1;
+  if (emu < 0) {
+    const char *e = getenv("SDB_ATTN_EMU");
+    emu = e ? atoi(e) : 1;
+    emu = emu < 0 ? 0 : (emu > 2 ? 2 : emu);
   }
+  dim3 grid(sp.n_ctas);
+#define SDB_LAUNCH_TC(NT, EMU)                                                                               \
+  do {                                                                                                       \
+    const size_t smem = sizeof(Smem<NT>) + 1024;                                                             \
+    cudaFuncSetAttribute(tree_attn_tcgen05_kernel<NT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    tree_attn_tcgen05_kernel<NT, EMU><<<grid, 128 + NT * 128, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);   \
+  } while (0)
+  if (sp.rows_unit == 2 * kTileM) {
+    if (emu == 0) SDB_LAUNCH_TC(2, 0); else if (emu == 2) SDB_LAUNCH_TC(2, 2); else SDB_LAUNCH_TC(2, 1);
+  } else {
+    if (emu == 0) SDB_LAUNCH_TC(1, 0); else if (emu == 2) SDB_LAUNCH_TC(1, 2); else SDB_LAUNCH_TC(1, 1);
+  }
+#undef SDB_LAUNCH_TC
   SDB_CHECK_LAUNCH();
-  if (p.num_splits > 1) return launch_tree_attn_combine_bf16(p, stream);
+  dim3 fgrid(sp.n_ctas * 2, cdiv(sp.rows_unit, 4));
+  tree_attn_fixup_kernel<<<fgrid, 128, 0, stream>>>(sp);
+  SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
 

@@ -49,7 +49,8 @@ static bool use_sm100(const sdb_tree_attn_args *a, const TreeAttnParams &p) {
   return tree_attn_sm100_supported(p);
 }
 
-static int64_t workspace_for(const TreeAttnParams &p) {
+static int64_t workspace_for(const TreeAttnParams &p, bool sm100, int ctas_override) {
+  if (sm100) return tree_attn_sm100_workspace(p, ctas_override);
   if (p.num_splits <= 1) return 0;
   const int64_t rows = (int64_t)p.batch * p.r_max * p.hq;
   return (int64_t)p.num_splits * rows * (p.head_dim + 1) * (int64_t)sizeof(float) + 256;
@@ -67,8 +68,8 @@ static int resolve(const sdb_tree_attn_args *a, TreeAttnParams &p, bool &sm100) 
   p.num_splits = 1;
   sm100 = use_sm100(a, p);
   if (a->kernel == 1 && !sm100) return SDB_E_UNSUPPORTED;
-  const int rows_per_cta = sm100 ? ((a->r_max * (a->hq / a->hkv) > 128) ? 256 : 128) : 32;
-  p.num_splits = a->num_splits > 0 ? a->num_splits : auto_splits(a, rows_per_cta);
+  // SIMT: uniform split-KV; tcgen05: num_splits overrides the persistent CTA count
+  p.num_splits = sm100 ? 1 : (a->num_splits > 0 ? a->num_splits : auto_splits(a, 32));
   return SDB_OK;
 }
 
@@ -79,7 +80,7 @@ extern "C" int64_t sdb_tree_attn_workspace(const sdb_tree_attn_args *a) {
   bool sm100 = false;
   int rc = sdb::resolve(a, p, sm100);
   if (rc != SDB_OK) return rc;
-  return sdb::workspace_for(p);
+  return sdb::workspace_for(p, sm100, a->num_splits);
 }
 
 extern "C" int sdb_tree_attn(const sdb_tree_attn_args *a, void *stream) {
@@ -88,9 +89,13 @@ extern "C" int sdb_tree_attn(const sdb_tree_attn_args *a, void *stream) {
   int rc = sdb::resolve(a, p, sm100);
   if (rc != SDB_OK) return rc;
   if (a->batch == 0) return SDB_OK;
-  int64_t need = sdb::workspace_for(p);
+  int64_t need = sdb::workspace_for(p, sm100, a->num_splits);
   if (need > 0) {
     if (!a->workspace || a->workspace_bytes < need) return SDB_E_WORKSPACE;
+  }
+  cudaStream_t s = sdb::as_stream(stream);
+  if (sm100) return sdb::launch_tree_attn_sm100(p, a->num_splits, a->workspace, s);
+  if (need > 0) {
     const int64_t rows = (int64_t)p.batch * p.r_max * p.hq;
     p.ws_out = reinterpret_cast<float *>(a->workspace);
     p.ws_lse = p.ws_out + (int64_t)p.num_splits * rows * p.head_dim;
@@ -98,8 +103,6 @@ extern "C" int sdb_tree_attn(const sdb_tree_attn_args *a, void *stream) {
     p.ws_out = nullptr;
     p.ws_lse = nullptr;
   }
-  cudaStream_t s = sdb::as_stream(stream);
-  if (sm100) return sdb::launch_tree_attn_sm100(p, s);
   if (a->dtype == SDB_DTYPE_BF16) return sdb::launch_tree_attn_simt<__nv_bfloat16>(p, s);
   return sdb::launch_tree_attn_simt<float>(p, s);
 }

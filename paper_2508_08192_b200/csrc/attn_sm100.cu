@@ -292,10 +292,13 @@ struct ItemGeo {
 __device__ __forceinline__ ItemGeo item_geo(const Sm100Params &sp, const Item &it, int g) {
   const TreeAttnParams &p = sp.p;
   ItemGeo o;
-  const int per_b = p.hkv * sp.m_blocks;
-  o.b = it.unit / per_b;
-  o.kvh = (it.unit % per_b) / sp.m_blocks;
-  o.row0 = (it.unit % sp.m_blocks) * sp.rows_unit;
+  // unit = mblk * (B * Hkv) + b * Hkv + kvh: the row blocks of one KV head run
+  // on CTAs ~n_ctas / m_blocks apart at the same time, so its K/V stream is
+  // read from HBM once and served from L2 to the other row blocks.
+  const int bh = p.batch * p.hkv;
+  o.b = (it.unit % bh) / p.hkv;
+  o.kvh = it.unit % p.hkv;
+  o.row0 = (it.unit / bh) * sp.rows_unit;
   o.n_nodes = min(p.n_rows[o.b], p.r_max);
   o.rows_total = o.n_nodes * g;
   o.C = p.ctx_len[o.b];
@@ -698,9 +701,9 @@ __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params 
   }
   if (t0 != 0 || t1 == sp.w_unit) return;  // not the first piece of a split unit
   const int g = p.hq / p.hkv;
-  const int per_b = p.hkv * sp.m_blocks;
-  const int b = unit / per_b, kvh = (unit % per_b) / sp.m_blocks;
-  const int rho = (unit % sp.m_blocks) * sp.rows_unit + local;
+  const int bh = p.batch * p.hkv;
+  const int b = (unit % bh) / p.hkv, kvh = unit % p.hkv;
+  const int rho = (unit / bh) * sp.rows_unit + local;
   if (rho >= p.r_max * g) return;
   const int n_nodes = min(p.n_rows[b], p.r_max);
   const int node = rho / g, hq_idx = kvh * g + rho % g;

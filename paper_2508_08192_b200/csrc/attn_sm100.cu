@@ -249,6 +249,7 @@ struct Sm100Params {
   int64_t total;   // units * w_unit
   float *part_out; // [n_ctas * 2][rows_unit][128] partial outputs of split units
   float *part_lse; // [n_ctas * 2][rows_unit]
+  int64_t *seg;    // [n_ctas + 1] segment starts, written by the main kernel for the fix-up
 };
 
 __host__ __device__ __forceinline__ int64_t seg_begin(const Sm100Params &sp, int k) {
@@ -339,6 +340,8 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
   const float sl2 = p.scale * 1.4426950408889634f;
 
   if (threadIdx.x == 0) {
+    sp.seg[blockIdx.x] = seg_begin(sp, blockIdx.x);
+    if (blockIdx.x == 0) sp.seg[sp.n_ctas] = sp.total;
     mbar_init(&sm.q_full, 1);
     mbar_init(&sm.q_empty, 1);
     for (int s = 0; s < 2; ++s) {
@@ -677,29 +680,22 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
   }
 }
 
-// Stream-K fix-up: the slot holding the FIRST piece of a split unit merges
-// all pieces of that unit (same math as merge_partials, attention.py:108-124).
-// grid (n_ctas * 2, rows_unit / 4), 4 warps, one warp per row.
+// Stream-K fix-up: one block row per CTA boundary k (1..n_ctas-1).  A
+// boundary strictly inside unit u splits it; the FIRST boundary inside u
+// merges all of u's pieces (same math as merge_partials,
+// attention.py:108-124).  grid (n_ctas - 1, rows_unit / 4), one warp per row.
 __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params sp) {
   const TreeAttnParams &p = sp.p;
-  const int slot = blockIdx.x, k = slot >> 1, j = slot & 1;
+  const int k = blockIdx.x + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int local = blockIdx.y * 4 + warp;
   if (local >= sp.rows_unit) return;
-  const int64_t s = seg_begin(sp, k), e = seg_begin(sp, k + 1);
-  if (s >= e) return;
-  int unit, t0, t1;
-  if (j == 0) {
-    unit = (int)(s / sp.w_unit);
-    t0 = (int)(s % sp.w_unit);
-    t1 = (int)min((int64_t)sp.w_unit, t0 + (e - s));
-  } else {
-    unit = (int)((e - 1) / sp.w_unit);
-    if (unit == (int)(s / sp.w_unit)) return;  // single item: already slot 0
-    t0 = 0;
-    t1 = (int)(e - (int64_t)unit * sp.w_unit);
-  }
-  if (t0 != 0 || t1 == sp.w_unit) return;  // not the first piece of a split unit
+  const int64_t ck = sp.seg[k];
+  const int W = sp.w_unit;
+  const int unit = (int)(ck / W);
+  const int64_t ustart = (int64_t)unit * W, uend = ustart + W;
+  if (ck == ustart) return;              // boundary between units: nothing split here
+  if (sp.seg[k - 1] > ustart) return;    // an earlier boundary inside u merges it
   const int g = p.hq / p.hkv;
   const int bh = p.batch * p.hkv;
   const int b = (unit % bh) / p.hkv, kvh = unit % p.hkv;
@@ -710,25 +706,27 @@ __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params 
   __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + (((int64_t)b * p.r_max + node) * p.hq + hq_idx) * kHeadDim;
   float *lse_out = p.lse ? p.lse + ((int64_t)b * p.hq + hq_idx) * p.r_max + node : nullptr;
   if (rho >= n_nodes * g) {
-    for (int c = lane * 4; c < kHeadDim; c += 128) *reinterpret_cast<uint2 *>(out + c) = make_uint2(0, 0);
+    *reinterpret_cast<uint2 *>(out + lane * 4) = make_uint2(0, 0);
     if (lse_out && lane == 0) *lse_out = -INFINITY;
     return;
   }
-  const int64_t unit_end = (int64_t)(unit + 1) * sp.w_unit;
-  float mx = -INFINITY;
-  for (int kk = k; kk < sp.n_ctas && seg_begin(sp, kk) < unit_end; ++kk) {
-    const int sl = kk == k ? slot : kk * 2;
-    mx = fmaxf(mx, sp.part_lse[(int64_t)sl * sp.rows_unit + local]);
-  }
+  // pieces: CTA k-1 (its first item iff its segment starts at the unit start,
+  // else its last item), then the first item of every later CTA starting in u
+  const int first_slot = (k - 1) * 2 + (sp.seg[k - 1] == ustart ? 0 : 1);
+  int kk_end = k;
+  while (kk_end < sp.n_ctas && sp.seg[kk_end] < uend) ++kk_end;  // CTAs k..kk_end-1 start inside u
+  float mx = sp.part_lse[(int64_t)first_slot * sp.rows_unit + local];
+  for (int kk = k; kk < kk_end; ++kk) mx = fmaxf(mx, sp.part_lse[(int64_t)(kk * 2) * sp.rows_unit + local]);
   float wsum = 0.f;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int kk = k; kk < sp.n_ctas && seg_begin(sp, kk) < unit_end; ++kk) {
-    const int sl = kk == k ? slot : kk * 2;
+  for (int kk = k - 1; kk < kk_end; ++kk) {
+    const int sl = kk == k - 1 ? first_slot : kk * 2;
     const float l = sp.part_lse[(int64_t)sl * sp.rows_unit + local];
     if (l == -INFINITY) continue;
     const float w = __expf(l - mx);
     wsum += w;
-    const float4 o = *reinterpret_cast<const float4 *>(sp.part_out + ((int64_t)sl * sp.rows_unit + local) * kHeadDim + lane * 4);
+    const float4 o =
+        *reinterpret_cast<const float4 *>(sp.part_out + ((int64_t)sl * sp.rows_unit + local) * kHeadDim + lane * 4);
     acc[0] = fmaf(w, o.x, acc[0]);
     acc[1] = fmaf(w, o.y, acc[1]);
     acc[2] = fmaf(w, o.z, acc[2]);
@@ -809,12 +807,14 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   sp.n_ctas = n;
   sp.part_out = nullptr;
   sp.part_lse = nullptr;
+  sp.seg = nullptr;
 }
 
 int64_t tree_attn_sm100_workspace(const TreeAttnParams &p, int ctas_override) {
   sm100::Sm100Params sp;
   sm100_plan(p, ctas_override, sp);
-  return (int64_t)sp.n_ctas * 2 * sp.rows_unit * (sm100::kHeadDim + 1) * (int64_t)sizeof(float) + 256;
+  return (int64_t)sp.n_ctas * 2 * sp.rows_unit * (sm100::kHeadDim + 1) * (int64_t)sizeof(float) +
+         (int64_t)(sp.n_ctas + 1) * 8 + 256;
 }
 
 int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *workspace, cudaStream_t stream) {
@@ -846,6 +846,7 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *wor
   sm100_plan(p, ctas_override, sp);
   sp.part_out = reinterpret_cast<float *>(workspace);
   sp.part_lse = sp.part_out + (int64_t)sp.n_ctas * 2 * sp.rows_unit * kHeadDim;
+  sp.seg = reinterpret_cast<int64_t *>(sp.part_lse + (int64_t)sp.n_ctas * 2 * sp.rows_unit);
   static int emu = -1;
   if (emu < 0) {
     const char *e = getenv("SDB_ATTN_EMU");
@@ -866,9 +867,11 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *wor
   }
 #undef SDB_LAUNCH_TC
   SDB_CHECK_LAUNCH();
-  dim3 fgrid(sp.n_ctas * 2, cdiv(sp.rows_unit, 4));
-  tree_attn_fixup_kernel<<<fgrid, 128, 0, stream>>>(sp);
-  SDB_CHECK_LAUNCH();
+  if (sp.n_ctas > 1) {
+    dim3 fgrid(sp.n_ctas - 1, cdiv(sp.rows_unit, 4));
+    tree_attn_fixup_kernel<<<fgrid, 128, 0, stream>>>(sp);
+    SDB_CHECK_LAUNCH();
+  }
   return SDB_OK;
 }
 

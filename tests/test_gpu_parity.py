@@ -534,3 +534,21 @@ def test_tcgen05_matches_simt_on_device():
         torch.cuda.synchronize()
         assert (o1.float() - o2.float()).abs().max().item() < 2e-2
         assert (l1 - l2).abs().max().item() < 2e-3
+
+
+@pytest.mark.parametrize("ctas", [0, 7, 148])
+def test_tcgen05_small_batch_stream_k(ctas):
+    """bs1 (8B shapes, 32q/8kv): each unit spans many persistent CTAs, so the
+    fix-up merges long chains of partial pieces."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    c = _rand_paged_case(1, 32, 8, 128, 4096, 64, TREE64, seed=3, ragged=False)
+    out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                     c["nr"], 128 ** -0.5, num_splits=ctas, kernel=1)
+    torch.cuda.synchronize()
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(c["q"]), f64(c["kp"]), f64(c["vp"]), c["table_np"],
+                                                   c["ctx_np"], f64(c["tk"]), f64(c["tv"]), [c["aug"]], 128 ** -0.5)
+    err = np.abs(out.float().cpu().numpy() - want_o)
+    assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+    assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3

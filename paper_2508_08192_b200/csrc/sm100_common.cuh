@@ -1,0 +1,477 @@
+// Shared device helpers of the sm_100a tree-verify attention kernels
+// (1-CTA attn_sm100.cu and 2-CTA attn_sm100_2cta.cu): mbarrier / TMA /
+// tcgen05 wrappers, packed-fp32 math, the stream-K work decomposition and the
+// per-tile softmax.
+#pragma once
+
+#include <cuda.h>
+
+#include "attn_internal.cuh"
+
+namespace sdb {
+namespace sm100 {
+
+constexpr int kTileN = 128;     // keys per KV tile
+constexpr int kTileM = 128;     // query rows per tile
+constexpr int kHeadDim = 128;   // d
+constexpr int kChunkBytes = kTileM * 128;  // 128 rows x 64 bf16 (one SW128 column chunk)
+constexpr int kTileBytes = 2 * kChunkBytes;  // 128 x 128 bf16
+constexpr float kRescaleThreshold = 8.0f;   // log2 units (factor 256)
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap *m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *m, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *m, uint64_t *bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *m, uint64_t *bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// ---- tcgen05 --------------------------------------------------------------
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+#define SDB_TMEM_LD32(taddr, r)                                                                                    \
+  asm volatile(                                                                                                    \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                               \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),         \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),    \
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),  \
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])   \
+      : "r"(taddr))
+
+#define SDB_TMEM_ST32(taddr, r)                                                                                    \
+  asm volatile(                                                                                                    \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),                                \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),          \
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),  \
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), \
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
+
+#define SDB_TMEM_ST16(taddr, r)                                                                                    \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
+               "%16};" ::"r"(taddr),                                                                               \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), \
+               "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]))
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// ---- packed fp32x2 math (FFMA2 / FADD2) and 3-input max (FMNMX3), sm_100 ----
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// exp2 of two values on the FMA pipe (offloads the MUFU): 2^x = 2^floor(x) *
+// p(frac(x)), p a cubic fit of 2^f on [0, 1) with p(0) = 1 (max relative
+// error 8.6e-5, far below the bf16 rounding of P).
+__device__ __forceinline__ void ex2_emu2(float x, float y, float &ox, float &oy) {
+  constexpr float kRound = 12582912.0f;  // 2^23 + 2^22
+  const uint64_t xy = f2pack(fmaxf(x, -127.f), fmaxf(y, -127.f));
+  const uint64_t rr = fadd2_rm(xy, f2pack(kRound, kRound));  // floor(x) in the low mantissa bits
+  const uint64_t fl = fadd2(rr, f2pack(-kRound, -kRound));
+  float fx, fy;
+  {
+    float a, b, c, d;
+    f2unpack(xy, a, b);
+    f2unpack(fl, c, d);
+    fx = a - c;
+    fy = b - d;
+  }
+  const uint64_t f = f2pack(fx, fy);
+  uint64_t pp = f2pack(0.07706617563962936f, 0.07706617563962936f);
+  pp = ffma2(pp, f, f2pack(0.22764593362808228f, 0.22764593362808228f));
+  pp = ffma2(pp, f, f2pack(0.6951165795326233f, 0.6951165795326233f));
+  pp = ffma2(pp, f, f2pack(1.0f, 1.0f));
+  float px, py, rx, ry;
+  f2unpack(pp, px, py);
+  f2unpack(rr, rx, ry);
+  ox = __uint_as_float(__float_as_uint(px) + (__float_as_uint(rx) << 23));
+  oy = __uint_as_float(__float_as_uint(py) + (__float_as_uint(ry) << 23));
+}
+
+// Shared-memory matrix descriptor (SM100 UMMA, version 1, 128-byte swizzle).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::f16, bf16 x bf16 -> fp32, M = 128, N = 128.
+__host__ __device__ constexpr uint32_t make_idesc(bool b_mn_major) {
+  return (1u << 4)                      // D format f32
+         | (1u << 7)                    // A bf16
+         | (1u << 10)                   // B bf16
+         | ((b_mn_major ? 1u : 0u) << 16)  // B major
+         | ((uint32_t)(kTileN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+}
+
+struct Sm100Params {
+  TreeAttnParams p;
+  int cta_group;   // 1: one CTA per unit (M = 128 MMAs); 2: CTA pair (M = 256, cta_group::2)
+  int nt;          // query tiles per CTA (ping-pong depth)
+  int m_blocks;    // row blocks (rows_unit query rows) per (b, kvh)
+  int units;       // m_blocks * batch * hkv
+  int w_pref;      // nominal prefix tiles per unit: ceil(max_ctx / 128)
+  int w_unit;      // nominal tiles per unit: w_pref + ceil(r_max / 128)
+  int n_workers;   // stream-K workers (CTAs, or CTA pairs)
+  int rows_unit;   // nt * 128 * cta_group
+  int64_t total;   // units * w_unit
+  float *part_out; // [n_workers * 2][rows_unit][128] partial outputs of split units
+  float *part_lse; // [n_workers * 2][rows_unit]
+  int64_t *seg;    // [n_workers + 1] segment starts, written by the main kernel for the fix-up
+};
+
+__host__ __device__ __forceinline__ int64_t seg_begin(const Sm100Params &sp, int k) {
+  return sp.total * k / sp.n_workers;
+}
+
+// One contiguous piece of a unit's nominal tile range owned by a worker.
+struct Item {
+  int unit, t0, t1, slot;
+  bool whole;
+};
+
+// Items of worker k: walk [seg_begin(k), seg_begin(k+1)).
+struct ItemIter {
+  int64_t cur, end;
+  int idx, k;
+  __device__ ItemIter(const Sm100Params &sp, int k_) : idx(0), k(k_) {
+    cur = seg_begin(sp, k_);
+    end = seg_begin(sp, k_ + 1);
+  }
+  __device__ bool next(const Sm100Params &sp, Item &it) {
+    if (cur >= end) return false;
+    it.unit = (int)(cur / sp.w_unit);
+    it.t0 = (int)(cur % sp.w_unit);
+    it.t1 = (int)min((int64_t)sp.w_unit, it.t0 + (end - cur));
+    it.whole = it.t0 == 0 && it.t1 == sp.w_unit;
+    cur += it.t1 - it.t0;
+    it.slot = k * 2 + (idx == 0 ? 0 : 1);
+    ++idx;
+    return true;
+  }
+};
+
+// Per-item geometry: which (b, kvh, rows) and which actual KV tiles.
+struct ItemGeo {
+  int b, kvh, row0, n_nodes, rows_total, C;
+  int pa, n_pref, sa, n_suf, n_tiles;
+  bool active;
+};
+
+__device__ __forceinline__ ItemGeo item_geo(const Sm100Params &sp, const Item &it, int g) {
+  const TreeAttnParams &p = sp.p;
+  ItemGeo o;
+  // unit = mblk * (B * Hkv) + b * Hkv + kvh: the row blocks of one KV head run
+  // on workers ~n_workers / m_blocks apart at the same time, so its K/V stream
+  // is read from HBM once and served from L2 to the other row blocks.
+  const int bh = p.batch * p.hkv;
+  o.b = (it.unit % bh) / p.hkv;
+  o.kvh = it.unit % p.hkv;
+  o.row0 = (it.unit / bh) * sp.rows_unit;
+  o.n_nodes = min(p.n_rows[o.b], p.r_max);
+  o.rows_total = o.n_nodes * g;
+  o.C = p.ctx_len[o.b];
+  const int pb = (o.C + kTileN - 1) / kTileN;
+  const int sb = (o.n_nodes + kTileN - 1) / kTileN;
+  o.pa = min(it.t0, pb);
+  const int pe = min(min(it.t1, sp.w_pref), pb);
+  o.n_pref = max(0, pe - o.pa);
+  o.sa = min(max(it.t0 - sp.w_pref, 0), sb);
+  const int se = min(max(it.t1 - sp.w_pref, 0), sb);
+  o.n_suf = max(0, se - o.sa);
+  o.n_tiles = o.n_pref + o.n_suf;
+  o.active = o.n_tiles > 0 && o.row0 < o.rows_total;
+  return o;
+}
+
+// ---------------------------------------------------------------------------
+// Softmax of one S tile row held by this thread (TMEM lane), P written back
+// over S.  Updates the running reference max m (log2 units) and sum l.
+// On return P is stored (tcgen05.wait::st done) and tcgen05.fence::before
+// issued; the caller signals the MMA issuer.
+// ---------------------------------------------------------------------------
+template <int EMU>
+__device__ __forceinline__ void softmax_tile(uint32_t t_s, uint32_t t_o, float sl2, bool first, bool pref,
+                                             int kvalid, const uint32_t *mrow, int key0, int n_words, bool row_ok,
+                                             float &m, float &l) {
+  const bool full = pref && kvalid >= kTileN;
+  // visibility bits of the 128 columns: prefix -> keys < ctx; suffix ->
+  // ancestor-or-self bits of this row's node (tree_build mask words)
+  uint32_t vm[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int lim = kvalid - 32 * w;
+    const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+    uint32_t bits = 0xffffffffu;
+    if (!pref) {
+      const int wi = (key0 >> 5) + w;
+      bits = (wi < n_words && row_ok) ? mrow[wi] : 0u;
+    }
+    vm[w] = bits & low;
+  }
+  uint32_t r[128];
+  SDB_TMEM_LD32(t_s + 0, (r + 0));
+  SDB_TMEM_LD32(t_s + 32, (r + 32));
+  SDB_TMEM_LD32(t_s + 64, (r + 64));
+  SDB_TMEM_LD32(t_s + 96, (r + 96));
+  tmem_wait_ld();
+  if (!full) {
+#pragma unroll
+    for (int e = 0; e < 128; ++e)
+      if (!((vm[e >> 5] >> (e & 31)) & 1u)) r[e] = 0xff800000u;
+  }
+  // row max on raw scores (scale > 0): 4 chains of 3-input max
+  float c0 = fmaxf(__uint_as_float(r[0]), __uint_as_float(r[1]));
+  float c1 = fmaxf(__uint_as_float(r[2]), __uint_as_float(r[3]));
+  float c2 = fmaxf(__uint_as_float(r[4]), __uint_as_float(r[5]));
+  float c3 = fmaxf(__uint_as_float(r[6]), __uint_as_float(r[7]));
+#pragma unroll
+  for (int e = 8; e < 128; e += 8) {
+    c0 = fmax3(c0, __uint_as_float(r[e + 0]), __uint_as_float(r[e + 1]));
+    c1 = fmax3(c1, __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+    c2 = fmax3(c2, __uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
+    c3 = fmax3(c3, __uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
+  }
+  const float mx = fmax3(fmaxf(c0, c1), c2, c3) * sl2;
+  // lazy rescale: move the reference max only when it grows by > 2^8; the
+  // O / l correction is applied after P is written (frees the S registers)
+  float corr = 1.f;
+  bool rescale = false;
+  if (first) {
+    m = mx;
+  } else if (mx > m + kRescaleThreshold) {
+    corr = ex2(m - mx);
+    rescale = true;
+    m = mx;
+  }
+  const float neg_mu = (m == -INFINITY) ? 0.f : -m;
+  // P = exp2(s * scale_log2 - m) (FFMA2); EMU of every 4 pairs on the FMA
+  // pipe; row sum on FADD2; packed bf16 in place into r[0..63]
+  const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
+  uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int e = 0; e < 64; ++e) {
+    float x0, x1, p0, p1;
+    f2unpack(ffma2(f2pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
+    if ((e & 3) >= 4 - EMU) {
+      ex2_emu2(x0, x1, p0, p1);
+    } else {
+      p0 = ex2(x0);
+      p1 = ex2(x1);
+    }
+    acc2[e & 3] = fadd2(acc2[e & 3], f2pack(p0, p1));
+    r[e] = pack_bf16(p0, p1);
+  }
+  float s0, s1, s2, s3, s4, s5, s6, s7;
+  f2unpack(acc2[0], s0, s1);
+  f2unpack(acc2[1], s2, s3);
+  f2unpack(acc2[2], s4, s5);
+  f2unpack(acc2[3], s6, s7);
+  l = l * corr + (((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)));
+  SDB_TMEM_ST32(t_s + 0, (r + 0));
+  SDB_TMEM_ST32(t_s + 32, (r + 32));
+  if (rescale) {
+    // the previous PV has completed: this tile's S was committed after it
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      SDB_TMEM_LD32(t_o + c * 32, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+      SDB_TMEM_ST32(t_o + c * 32, o);
+    }
+  }
+  tmem_wait_st();
+  tc_fence_before();
+}
+
+// Normalise this thread's O row (TMEM) and store it: final bf16 output +
+// LSE for a whole unit, fp32 partial for a split one.
+__device__ __forceinline__ void epilogue_row(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,
+                                             int local, uint32_t t_o, float m, float l) {
+  const TreeAttnParams &p = sp.p;
+  const int rho = geo.row0 + local;
+  const bool row_ok = rho < geo.rows_total;
+  const bool in_range = rho < p.r_max * g;
+  const int node_o = rho / g;
+  const int hq_idx = geo.kvh * g + (rho % g);
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  const float lse_n = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t r[32];
+    SDB_TMEM_LD32(t_o + c * 32, r);
+    tmem_wait_ld();
+    if (item.whole) {
+      if (!in_range) continue;
+      __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
+                         (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim + c * 32;
+#pragma unroll
+      for (int e = 0; e < 32; e += 8) {
+        uint4 v;
+        if (row_ok) {
+          v.x = pack_bf16(__uint_as_float(r[e + 0]) * inv, __uint_as_float(r[e + 1]) * inv);
+          v.y = pack_bf16(__uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+          v.z = pack_bf16(__uint_as_float(r[e + 4]) * inv, __uint_as_float(r[e + 5]) * inv);
+          v.w = pack_bf16(__uint_as_float(r[e + 6]) * inv, __uint_as_float(r[e + 7]) * inv);
+        } else {
+          v = make_uint4(0, 0, 0, 0);
+        }
+        *reinterpret_cast<uint4 *>(o + e) = v;
+      }
+    } else {
+      float *o = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim + c * 32;
+#pragma unroll
+      for (int e = 0; e < 32; e += 4)
+        *reinterpret_cast<float4 *>(o + e) =
+            make_float4(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv,
+                        __uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+    }
+  }
+  if (item.whole) {
+    if (in_range && p.lse)
+      p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = row_ok ? lse_n : -INFINITY;
+  } else {
+    sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = row_ok ? lse_n : -INFINITY;
+  }
+}
+
+// Zeros / -inf for a row of an inactive item (padding rows of a whole unit, or
+// every row of an empty split piece).
+__device__ __forceinline__ void inactive_row(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,
+                                             int local) {
+  const TreeAttnParams &p = sp.p;
+  const int rho = geo.row0 + local;
+  if (!item.whole) {
+    float *o = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim;
+    for (int c = 0; c < kHeadDim; c += 4) *reinterpret_cast<float4 *>(o + c) = make_float4(0, 0, 0, 0);
+    sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = -INFINITY;
+  } else if (rho < p.r_max * g) {
+    const int node_o = rho / g, hq_idx = geo.kvh * g + (rho % g);
+    __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
+                       (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim;
+    for (int c = 0; c < kHeadDim; c += 8) *reinterpret_cast<uint4 *>(o + c) = make_uint4(0, 0, 0, 0);
+    if (p.lse) p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = -INFINITY;
+  }
+}
+
+int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const CUtensorMap &mtk,
+                const CUtensorMap &mtv, const Sm100Params &sp, int emu, cudaStream_t stream);
+
+}  // namespace sm100
+}  // namespace sdb

@@ -552,3 +552,23 @@ def test_tcgen05_small_batch_stream_k(ctas):
     err = np.abs(out.float().cpu().numpy() - want_o)
     assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
     assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
+
+
+@pytest.mark.parametrize("group", ["1", "2"])
+def test_tcgen05_single_cta_and_pair_kernels_agree(group, monkeypatch):
+    """Force the 1-CTA (M=128) or the CTA-pair (cta_group::2, M=256) kernel on
+    the same 70B-shaped inputs; both must match the float64 oracle."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    monkeypatch.setenv("SDB_ATTN_CTA_GROUP", group)
+    c = _rand_paged_case(3, 64, 8, 128, 2048, 32, TREE64, seed=21)
+    out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                     c["nr"], 128 ** -0.5, kernel=1)
+    torch.cuda.synchronize()
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(c["q"]), f64(c["kp"]), f64(c["vp"]), c["table_np"],
+                                                   c["ctx_np"], f64(c["tk"]), f64(c["tv"]), [c["aug"]] * 3,
+                                                   128 ** -0.5)
+    err = np.abs(out.float().cpu().numpy() - want_o)
+    assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+    assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3

@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libspecdec_b200.so")
+LIB_PATH = os.environ.get("SDB_LIB") or os.path.join(_HERE, "_lib", "libspecdec_b200.so")
 
 SDB_OK = 0
 SDB_ERR_BAD_PARENT = 1

@@ -20,6 +20,19 @@ namespace sdb {
 namespace sm100 {
 
 constexpr int kStages2 = 3;
+
+#ifdef SDB_TRACE
+// [event][iteration] clock64 stamps of worker 0 (debug builds only)
+__device__ unsigned long long g_trace[16][256];
+#define TRACE(ev, it)                                                                   \
+  do {                                                                                  \
+    if (worker == 0 && (it) < 256) g_trace[ev][it] = clock64();                         \
+  } while (0)
+#else
+#define TRACE(ev, it) \
+  do {                \
+  } while (0)
+#endif
 constexpr int kHalfBytes = kTileBytes / 2;    // 16 KB: K half [64 keys][128 d] or V half [128 keys][64 d]
 constexpr int kKChunk = kHalfBytes / 2;       // 8 KB: one 64-column chunk of the K half
 
@@ -39,7 +52,7 @@ __device__ __forceinline__ uint32_t leader_addr(const void *p) {
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {
   asm volatile(
       "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, 0;\n"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar))
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
@@ -47,7 +60,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
       "{\n"
       ".reg .pred P1;\n"
       "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@P1 bra DONE;\n"
       "bra LAB_WAIT;\n"
       "DONE:\n"
@@ -270,10 +283,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
         for (int it = 0; it < geo.n_tiles; ++it) {
           const uint32_t gt = g_tile + it;
           const int s = gt % kStages2;
+          TRACE(12, gt);
           mbar_wait(&sm.v_full[s], (gt / kStages2) & 1);
+          TRACE(13, gt);
           tc_fence_after();
           for (int t = 0; t < NT; ++t) {
+            TRACE(0 + t * 3, gt);
             mbar_wait_cluster(&sm.p_full[t], gt & 1);
+            TRACE(1 + t * 3, gt);
             if (it == 0) mbar_wait_cluster(&sm.o_free[t], (g_q & 1) ^ 1);
             tc_fence_after();
             issue_pv(t, s, it > 0);
@@ -288,6 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
               tc_commit2(&sm.s_full[t]);
               if (t == NT - 1) tc_commit2(&sm.k_empty[s2]);
             }
+            TRACE(2 + t * 3, gt);
           }
           tc_commit2(&sm.v_empty[s]);
         }
@@ -323,9 +341,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
         const bool pref = it < geo.n_pref;
         const int key0 = pref ? (geo.pa + it) * kTileN : (geo.sa + it - geo.n_pref) * kTileN;
         const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
+        if (rank == 0 && (warp & 3) == 0 && lane == 0) TRACE(6 + t * 3, gt);
         mbar_wait(&sm.s_full[t], gt & 1);
         tc_fence_after();
+        if (rank == 0 && (warp & 3) == 0 && lane == 0) TRACE(7 + t * 3, gt);
         softmax_tile<EMU>(t_s, t_o, sl2, it == 0, pref, kvalid, mrow, key0, p.n_words, row_ok, m, l);
+        if (rank == 0 && (warp & 3) == 0 && lane == 0) TRACE(8 + t * 3, gt);
         if (rank == 0)
           mbar_arrive(&sm.p_full[t]);
         else
@@ -373,3 +394,9 @@ int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap 
 
 }  // namespace sm100
 }  // namespace sdb
+
+#ifdef SDB_TRACE
+extern "C" int sdb_debug_trace(unsigned long long *host_out) {
+  return cudaMemcpyFromSymbol(host_out, sdb::sm100::g_trace, sizeof(sdb::sm100::g_trace)) == cudaSuccess ? 0 : -4;
+}
+#endif

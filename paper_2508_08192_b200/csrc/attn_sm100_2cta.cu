@@ -130,10 +130,11 @@ struct alignas(1024) Smem2 {
   uint64_t k_full[kStages2], k_empty[kStages2], v_full[kStages2], v_empty[kStages2];
   uint64_t s_full[NT], p_full[NT], o_done[NT], o_free[NT];
   uint32_t tmem_base;
+  float xch[NT][3][2][128];  // half-row exchange: [0/1] row max by tile parity, [2] row sum
 };
 
 template <int NT, int EMU>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 256, 1)
     tree_attn_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_tk,
                                   const __grid_constant__ CUtensorMap tm_tv, const Sm100Params sp) {
@@ -161,9 +162,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
     }
     for (int t = 0; t < NT; ++t) {
       mbar_init(&sm.s_full[t], 1);
-      mbar_init(&sm.p_full[t], 256);
+      mbar_init(&sm.p_full[t], 512);  // 2 CTAs x 256 softmax threads
       mbar_init(&sm.o_done[t], 1);
-      mbar_init(&sm.o_free[t], 256);
+      mbar_init(&sm.o_free[t], 512);
     }
     fence_barrier_init();
   }
@@ -316,9 +317,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
     }
   } else if (warp >= 4) {
     // ===================== softmax (both CTAs, own 128 rows per tile) ==========
-    const int t = (warp - 4) >> 2;
-    const int i = ((warp & 3) << 5) + lane;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    // 8 warps per query tile: lane group (warp % 4) x column half (0/1)
+    const int t = (warp - 4) >> 3;
+    const int ww = (warp - 4) & 7;
+    const int lg = ww & 3, half = ww >> 2;
+    const int i = (lg << 5) + lane;
+    const int bar_id = 1 + t * 4 + lg;
+    const uint32_t lane_off = (uint32_t)(lg * 32) << 16;
     const uint32_t t_s = tmem + lane_off + t * 128;
     const uint32_t t_o = tmem + lane_off + 256 + t * 128;
     const int local = t * 2 * kTileM + (int)rank * kTileM + i;  // row within the unit
@@ -328,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
     while (iter.next(sp, item)) {
       const ItemGeo geo = item_geo(sp, item, g);
       if (!geo.active) {
-        inactive_row(sp, item, geo, g, local);
+        if (half == 0) inactive_row(sp, item, geo, g, local);
         continue;
       }
       const int rho = geo.row0 + local;
@@ -341,12 +346,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
         const bool pref = it < geo.n_pref;
         const int key0 = pref ? (geo.pa + it) * kTileN : (geo.sa + it - geo.n_pref) * kTileN;
         const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
-        if (rank == 0 && (warp & 3) == 0 && lane == 0) TRACE(6 + t * 3, gt);
+        if (rank == 0 && ww == 0 && lane == 0) TRACE(6 + t * 3, gt);
         mbar_wait(&sm.s_full[t], gt & 1);
         tc_fence_after();
-        if (rank == 0 && (warp & 3) == 0 && lane == 0) TRACE(7 + t * 3, gt);
-        softmax_tile<EMU>(t_s, t_o, sl2, it == 0, pref, kvalid, mrow, key0, p.n_words, row_ok, m, l);
-        if (rank == 0 && (warp & 3) == 0 && lane == 0) TRACE(8 + t * 3, gt);
+        if (rank == 0 && ww == 0 && lane == 0) TRACE(7 + t * 3, gt);
+        softmax_half_tile<EMU>(t_s, t_o, half, sl2, it == 0, pref, kvalid, mrow, key0, p.n_words, row_ok,
+                               &sm.xch[t][gt & 1][0][0], i,
+                               bar_id, m, l);
+        if (rank == 0 && ww == 0 && lane == 0) TRACE(8 + t * 3, gt);
         if (rank == 0)
           mbar_arrive(&sm.p_full[t]);
         else
@@ -354,8 +361,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 128, 1)
       }
       mbar_wait(&sm.o_done[t], (g_tile + geo.n_tiles - 1) & 1);
       tc_fence_after();
-      epilogue_row(sp, item, geo, g, local, t_o, m, l);
+      // combine the two partial row sums (the max m is identical in both halves)
+      sm.xch[t][2][half][i] = l;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      const float l_full = l + sm.xch[t][2][half ^ 1][i];
+      epilogue_half_row(sp, item, geo, g, local, half, t_o, m, l_full);
       tc_fence_before();
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // xch reuse
       if (rank == 0)
         mbar_arrive(&sm.o_free[t]);
       else
@@ -380,7 +392,7 @@ int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap 
     const size_t smem = sizeof(Smem2<NT>) + 1024;                                                                \
     cudaFuncSetAttribute(tree_attn_tcgen05_pair_kernel<NT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                          (int)smem);                                                                             \
-    tree_attn_tcgen05_pair_kernel<NT, EMU><<<grid, 128 + NT * 128, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);   \
+    tree_attn_tcgen05_pair_kernel<NT, EMU><<<grid, 128 + NT * 256, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);   \
   } while (0)
   if (sp.nt == 2) {
     if (emu == 0) SDB_LAUNCH_PAIR(2, 0); else if (emu == 2) SDB_LAUNCH_PAIR(2, 2); else SDB_LAUNCH_PAIR(2, 1);

@@ -400,6 +400,155 @@ __device__ __forceinline__ void softmax_tile(uint32_t t_s, uint32_t t_o, float s
   tc_fence_before();
 }
 
+// Half-row variant: two warps share a TMEM lane group, each owning 64 of the
+// 128 columns of a row (more softmax warps per SMSP to hide latency).  The
+// partner's partial row max is exchanged through shared memory under a
+// 64-thread named barrier; the row sum stays partial (combined in the
+// epilogue).  P for columns [64h, 64h+64) lands in packed columns
+// [32h, 32h+32) -- both halves have loaded their S before the exchange.
+template <int EMU>
+__device__ __forceinline__ void softmax_half_tile(uint32_t t_s, uint32_t t_o, int half, float sl2, bool first,
+                                                  bool pref, int kvalid, const uint32_t *mrow, int key0, int n_words,
+                                                  bool row_ok, float *xch, int xch_row, int bar_id, float &m,
+                                                  float &l) {
+  const bool full = pref && kvalid >= kTileN;
+  uint32_t vm[2];
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const int lim = kvalid - 32 * (2 * half + w);
+    const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+    uint32_t bits = 0xffffffffu;
+    if (!pref) {
+      const int wi = (key0 >> 5) + 2 * half + w;
+      bits = (wi < n_words && row_ok) ? mrow[wi] : 0u;
+    }
+    vm[w] = bits & low;
+  }
+  uint32_t r[64];
+  SDB_TMEM_LD32(t_s + 64 * half, (r + 0));
+  SDB_TMEM_LD32(t_s + 64 * half + 32, (r + 32));
+  tmem_wait_ld();
+  if (!full) {
+#pragma unroll
+    for (int e = 0; e < 64; ++e)
+      if (!((vm[e >> 5] >> (e & 31)) & 1u)) r[e] = 0xff800000u;
+  }
+  float c0 = fmaxf(__uint_as_float(r[0]), __uint_as_float(r[1]));
+  float c1 = fmaxf(__uint_as_float(r[2]), __uint_as_float(r[3]));
+  float c2 = fmaxf(__uint_as_float(r[4]), __uint_as_float(r[5]));
+  float c3 = fmaxf(__uint_as_float(r[6]), __uint_as_float(r[7]));
+#pragma unroll
+  for (int e = 8; e < 64; e += 8) {
+    c0 = fmax3(c0, __uint_as_float(r[e + 0]), __uint_as_float(r[e + 1]));
+    c1 = fmax3(c1, __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+    c2 = fmax3(c2, __uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
+    c3 = fmax3(c3, __uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
+  }
+  const float mh = fmax3(fmaxf(c0, c1), c2, c3);
+  xch[half * 128 + xch_row] = mh;
+  asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+  const float mx = fmaxf(mh, xch[(half ^ 1) * 128 + xch_row]) * sl2;
+  float corr = 1.f;
+  bool rescale = false;
+  if (first) {
+    m = mx;
+  } else if (mx > m + kRescaleThreshold) {
+    corr = ex2(m - mx);
+    rescale = true;
+    m = mx;
+  }
+  const float neg_mu = (m == -INFINITY) ? 0.f : -m;
+  const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
+  uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    float x0, x1, p0, p1;
+    f2unpack(ffma2(f2pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
+    if ((e & 3) >= 4 - EMU) {
+      ex2_emu2(x0, x1, p0, p1);
+    } else {
+      p0 = ex2(x0);
+      p1 = ex2(x1);
+    }
+    acc2[e & 3] = fadd2(acc2[e & 3], f2pack(p0, p1));
+    r[e] = pack_bf16(p0, p1);
+  }
+  float s0, s1, s2, s3, s4, s5, s6, s7;
+  f2unpack(acc2[0], s0, s1);
+  f2unpack(acc2[1], s2, s3);
+  f2unpack(acc2[2], s4, s5);
+  f2unpack(acc2[3], s6, s7);
+  l = l * corr + (((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)));
+  SDB_TMEM_ST32(t_s + 32 * half, (r + 0));
+  if (rescale) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t o[32];
+      SDB_TMEM_LD32(t_o + 64 * half + c * 32, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+      SDB_TMEM_ST32(t_o + 64 * half + c * 32, o);
+    }
+  }
+  tmem_wait_st();
+  tc_fence_before();
+}
+
+// Epilogue for a half row: this thread's 64 O columns, with the row sum
+// combined from both halves (l_full).
+__device__ __forceinline__ void epilogue_half_row(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,
+                                                  int local, int half, uint32_t t_o, float m, float l_full) {
+  const TreeAttnParams &p = sp.p;
+  const int rho = geo.row0 + local;
+  const bool row_ok = rho < geo.rows_total;
+  const bool in_range = rho < p.r_max * g;
+  const int node_o = rho / g;
+  const int hq_idx = geo.kvh * g + (rho % g);
+  const float inv = l_full > 0.f ? 1.f / l_full : 0.f;
+  const float lse_n = l_full > 0.f ? (m + __log2f(l_full)) * 0.6931471805599453f : -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    SDB_TMEM_LD32(t_o + 64 * half + c * 32, r);
+    tmem_wait_ld();
+    const int col0 = 64 * half + c * 32;
+    if (item.whole) {
+      if (!in_range) continue;
+      __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
+                         (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim + col0;
+#pragma unroll
+      for (int e = 0; e < 32; e += 8) {
+        uint4 v;
+        if (row_ok) {
+          v.x = pack_bf16(__uint_as_float(r[e + 0]) * inv, __uint_as_float(r[e + 1]) * inv);
+          v.y = pack_bf16(__uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+          v.z = pack_bf16(__uint_as_float(r[e + 4]) * inv, __uint_as_float(r[e + 5]) * inv);
+          v.w = pack_bf16(__uint_as_float(r[e + 6]) * inv, __uint_as_float(r[e + 7]) * inv);
+        } else {
+          v = make_uint4(0, 0, 0, 0);
+        }
+        *reinterpret_cast<uint4 *>(o + e) = v;
+      }
+    } else {
+      float *o = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim + col0;
+#pragma unroll
+      for (int e = 0; e < 32; e += 4)
+        *reinterpret_cast<float4 *>(o + e) =
+            make_float4(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv,
+                        __uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+    }
+  }
+  if (half == 0) {
+    if (item.whole) {
+      if (in_range && p.lse)
+        p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = row_ok ? lse_n : -INFINITY;
+    } else {
+      sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = row_ok ? lse_n : -INFINITY;
+    }
+  }
+}
+
 // Normalise this thread's O row (TMEM) and store it: final bf16 output +
 // LSE for a whole unit, fp32 partial for a split one.
 __device__ __forceinline__ void epilogue_row(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,

@@ -144,26 +144,31 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // Whole warp walks the schedule (uniform descriptors); one elected lane
+    // issues (see attn_sm100_2cta.cu: a lone issuing thread costs ~16
+    // instructions per tcgen05.mma).
+    {
       constexpr uint32_t idesc_s = make_idesc(false);
       constexpr uint32_t idesc_o = make_idesc(true);
-      const uint32_t q_base = smem_u32(sm.q[0]);
-      auto issue_s = [&](int t, int s) {
-        const uint32_t qa = q_base + t * kTileBytes;
-        const uint32_t ka = smem_u32(sm.k[s]);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint64_t q_desc = sw128_desc(smem_u32(sm.q[0]), 16, 1024);
+      const uint64_t k_desc = sw128_desc(smem_u32(sm.k[0]), 16, 1024);
+      const uint64_t v_desc = sw128_desc(smem_u32(sm.v[0]), kChunkBytes, 1024);
+      auto issue_s = [&](int t, int st) {
+        const uint64_t qd = q_desc + (uint64_t)((t * kTileBytes) >> 4);
+        const uint64_t kd = k_desc + (uint64_t)((st * kTileBytes) >> 4);
 #pragma unroll
         for (int k = 0; k < kHeadDim / 16; ++k) {
-          const uint32_t off = (k >> 2) * kChunkBytes + (k & 3) * 32;
-          mma_ss(tmem + t * 128, sw128_desc(qa + off, 16, 1024), sw128_desc(ka + off, 16, 1024), idesc_s, k > 0);
+          const uint64_t off = (uint64_t)(((k >> 2) * kChunkBytes + (k & 3) * 32) >> 4);
+          mma_ss(tm + t * 128, qd + off, kd + off, idesc_s, k > 0);
         }
       };
-      auto issue_pv = [&](int t, int s, bool acc) {
-        const uint32_t va = smem_u32(sm.v[s]);
+      auto issue_pv = [&](int t, int st, bool acc) {
+        const uint64_t vd = v_desc + (uint64_t)((st * kTileBytes) >> 4);
 #pragma unroll
-        for (int k = 0; k < kTileN / 16; ++k) {
-          mma_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, sw128_desc(va + k * 2048, kChunkBytes, 1024),
-                 idesc_o, (acc || k > 0) ? 1u : 0u);
-        }
+        for (int k = 0; k < kTileN / 16; ++k)
+          mma_ts(tm + 256 + t * 128, tm + t * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), idesc_o,
+                 (acc || k > 0) ? 1u : 0u);
       };
       uint32_t g_tile = 0, g_q = 0;
       ItemIter iter(sp, blockIdx.x);
@@ -171,40 +176,52 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
       while (iter.next(sp, item)) {
         const ItemGeo geo = item_geo(sp, item, g);
         if (!geo.active) continue;
+        const int n_tiles = __shfl_sync(0xffffffffu, geo.n_tiles, 0);
         mbar_wait(&sm.q_full, g_q & 1);
         mbar_wait(&sm.k_full[g_tile & 1], (g_tile >> 1) & 1);
         tc_fence_after();
-        for (int t = 0; t < NT; ++t) {
-          issue_s(t, g_tile & 1);
-          tc_commit(&sm.s_full[t]);
+        if (elect_one()) {
+          for (int t = 0; t < NT; ++t) {
+            issue_s(t, g_tile & 1);
+            tc_commit(&sm.s_full[t]);
+          }
+          tc_commit(&sm.k_empty[g_tile & 1]);
         }
-        tc_commit(&sm.k_empty[g_tile & 1]);
-        for (int it = 0; it < geo.n_tiles; ++it) {
+        __syncwarp();
+        for (int it = 0; it < n_tiles; ++it) {
           const uint32_t gt = g_tile + it;
-          const int s = gt & 1;
-          mbar_wait(&sm.v_full[s], (gt >> 1) & 1);
+          const int st = gt & 1;
+          mbar_wait(&sm.v_full[st], (gt >> 1) & 1);
           tc_fence_after();
           for (int t = 0; t < NT; ++t) {
             mbar_wait(&sm.p_full[t], gt & 1);
             if (it == 0) mbar_wait(&sm.o_free[t], (g_q & 1) ^ 1);  // previous unit's epilogue read O_t
             tc_fence_after();
-            issue_pv(t, s, it > 0);
-            tc_commit(&sm.o_done[t]);
-            if (it + 1 < geo.n_tiles) {
+            if (elect_one()) {
+              issue_pv(t, st, it > 0);
+              tc_commit(&sm.o_done[t]);
+            }
+            __syncwarp();
+            if (it + 1 < n_tiles) {
               const int s2 = (gt + 1) & 1;
               if (t == 0) {
                 mbar_wait(&sm.k_full[s2], ((gt + 1) >> 1) & 1);
                 tc_fence_after();
               }
-              issue_s(t, s2);
-              tc_commit(&sm.s_full[t]);
-              if (t == NT - 1) tc_commit(&sm.k_empty[s2]);
+              if (elect_one()) {
+                issue_s(t, s2);
+                tc_commit(&sm.s_full[t]);
+                if (t == NT - 1) tc_commit(&sm.k_empty[s2]);
+              }
+              __syncwarp();
             }
           }
-          tc_commit(&sm.v_empty[s]);
+          if (elect_one()) tc_commit(&sm.v_empty[st]);
+          __syncwarp();
         }
-        tc_commit(&sm.q_empty);  // all S MMAs of this unit read Q
-        g_tile += geo.n_tiles;
+        if (elect_one()) tc_commit(&sm.q_empty);  // all S MMAs of this unit read Q
+        __syncwarp();
+        g_tile += n_tiles;
         ++g_q;
       }
     }

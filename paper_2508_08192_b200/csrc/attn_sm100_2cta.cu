@@ -128,13 +128,163 @@ struct alignas(1024) Smem2 {
   uint8_t v[kStages2][kHalfBytes];
   uint64_t q_full, q_empty;
   uint64_t k_full[kStages2], k_empty[kStages2], v_full[kStages2], v_empty[kStages2];
-  uint64_t s_full[NT], p_full[NT], o_done[NT], o_free[NT];
+  uint64_t s_full[2], p_full[2];  // per TMEM S buffer
+  uint64_t o_done[NT], o_free[NT];
   uint32_t tmem_base;
-  float xch[NT][3][2][128];  // half-row exchange: [0/1] row max by tile parity, [2] row sum
+  float xmax[2][4][128];  // quarter-row maxima, double-buffered by item parity
+  float xsum[4][128];     // quarter-row sums (epilogue)
 };
 
+constexpr int kSoftmaxWarps = 16;  // 4 TMEM lane groups x 4 column quarters
+constexpr int kPairThreads = 128 + kSoftmaxWarps * 32;
+
+// Softmax of one item for this thread's row, columns [32 qtr, 32 qtr + 32) of
+// the S buffer at t_s.  The row max is combined with the 3 other quarters of
+// the row (same TMEM lane group) through shared memory under a 128-thread
+// named barrier; the row sum stays partial (combined in the epilogue; every
+// quarter applies the same max, so partial sums add).  P (bf16) for the
+// quarter lands in packed columns [16 qtr, 16 qtr + 16) -- every quarter has
+// loaded its S before the barrier.  O columns [32 qtr, +32) are rescaled in
+// place when the max grows by more than 2^8: the previous PV into this O
+// completed before this S was committed (in-order tensor pipe).
+template <int EMU>
+__device__ __forceinline__ void softmax_quarter(uint32_t t_s, uint32_t t_o, int qtr, float sl2, bool first, bool pref,
+                                                int kvalid, const uint32_t *mrow, int key0, int n_words, bool row_ok,
+                                                float *xmax, int row, int bar_id, float &m, float &l) {
+  const bool full = pref && kvalid >= kTileN;
+  uint32_t r[32];
+  SDB_TMEM_LD32(t_s + 32 * qtr, r);
+  uint32_t vm = 0xffffffffu;
+  if (!full) {
+    const int lim = kvalid - 32 * qtr;
+    const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+    uint32_t bits = 0xffffffffu;
+    if (!pref) {
+      const int wi = (key0 >> 5) + qtr;
+      bits = (wi < n_words && row_ok) ? mrow[wi] : 0u;
+    }
+    vm = bits & low;
+  }
+  tmem_wait_ld();
+  if (!full) {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (!((vm >> e) & 1u)) r[e] = 0xff800000u;
+  }
+  float c0 = fmax3(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]));
+  float c1 = fmax3(__uint_as_float(r[3]), __uint_as_float(r[4]), __uint_as_float(r[5]));
+  float c2 = fmax3(__uint_as_float(r[6]), __uint_as_float(r[7]), __uint_as_float(r[8]));
+  float c3 = fmax3(__uint_as_float(r[9]), __uint_as_float(r[10]), __uint_as_float(r[11]));
+#pragma unroll
+  for (int e = 12; e < 28; e += 8) {
+    c0 = fmax3(c0, __uint_as_float(r[e + 0]), __uint_as_float(r[e + 1]));
+    c1 = fmax3(c1, __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+    c2 = fmax3(c2, __uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
+    c3 = fmax3(c3, __uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
+  }
+  c0 = fmax3(c0, __uint_as_float(r[28]), __uint_as_float(r[29]));
+  c1 = fmax3(c1, __uint_as_float(r[30]), __uint_as_float(r[31]));
+  xmax[qtr * 128 + row] = fmax3(fmaxf(c0, c1), c2, c3);
+  asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+  const float mx = fmaxf(fmaxf(xmax[row], xmax[128 + row]), fmaxf(xmax[256 + row], xmax[384 + row])) * sl2;
+  float corr = 1.f;
+  bool rescale = false;
+  if (first) {
+    m = mx;
+  } else if (mx > m + kRescaleThreshold) {
+    corr = ex2(m - mx);
+    rescale = true;
+    m = mx;
+  }
+  const float neg_mu = (m == -INFINITY) ? 0.f : -m;
+  const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
+  uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    float x0, x1, p0, p1;
+    f2unpack(ffma2(f2pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
+    if ((e & 3) >= 4 - EMU) {
+      ex2_emu2(x0, x1, p0, p1);
+    } else {
+      p0 = ex2(x0);
+      p1 = ex2(x1);
+    }
+    acc2[e & 3] = fadd2(acc2[e & 3], f2pack(p0, p1));
+    r[e] = pack_bf16(p0, p1);
+  }
+  float s0, s1, s2, s3, s4, s5, s6, s7;
+  f2unpack(fadd2(acc2[0], acc2[1]), s0, s1);
+  f2unpack(fadd2(acc2[2], acc2[3]), s2, s3);
+  l = l * corr + ((s0 + s1) + (s2 + s3));
+  (void)s4; (void)s5; (void)s6; (void)s7;
+  SDB_TMEM_ST16(t_s + 16 * qtr, r);
+  if (rescale) {
+    uint32_t o[32];
+    SDB_TMEM_LD32(t_o + 32 * qtr, o);
+    tmem_wait_ld();
+#pragma unroll
+    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+    SDB_TMEM_ST32(t_o + 32 * qtr, o);
+  }
+  tmem_wait_st();
+  tc_fence_before();
+}
+
+// Epilogue for a quarter row: O columns [32 qtr, +32) normalised by the full
+// row sum; quarter 0 also writes the LSE.
+__device__ __forceinline__ void epilogue_quarter(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,
+                                                 int local, int qtr, uint32_t t_o, float m, float l_full) {
+  const TreeAttnParams &p = sp.p;
+  const int rho = geo.row0 + local;
+  const bool row_ok = rho < geo.rows_total;
+  const bool in_range = rho < p.r_max * g;
+  const int node_o = rho / g;
+  const int hq_idx = geo.kvh * g + (rho % g);
+  const float inv = l_full > 0.f ? 1.f / l_full : 0.f;
+  const float lse_n = l_full > 0.f ? (m + __log2f(l_full)) * 0.6931471805599453f : -INFINITY;
+  uint32_t r[32];
+  SDB_TMEM_LD32(t_o + 32 * qtr, r);
+  tmem_wait_ld();
+  const int col0 = 32 * qtr;
+  if (item.whole) {
+    if (in_range) {
+      __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
+                         (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim + col0;
+#pragma unroll
+      for (int e = 0; e < 32; e += 8) {
+        uint4 v;
+        if (row_ok) {
+          v.x = pack_bf16(__uint_as_float(r[e + 0]) * inv, __uint_as_float(r[e + 1]) * inv);
+          v.y = pack_bf16(__uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+          v.z = pack_bf16(__uint_as_float(r[e + 4]) * inv, __uint_as_float(r[e + 5]) * inv);
+          v.w = pack_bf16(__uint_as_float(r[e + 6]) * inv, __uint_as_float(r[e + 7]) * inv);
+        } else {
+          v = make_uint4(0, 0, 0, 0);
+        }
+        *reinterpret_cast<uint4 *>(o + e) = v;
+      }
+      if (qtr == 0 && p.lse)
+        p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = row_ok ? lse_n : -INFINITY;
+    }
+  } else {
+    float *o = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim + col0;
+#pragma unroll
+    for (int e = 0; e < 32; e += 4)
+      *reinterpret_cast<float4 *>(o + e) = make_float4(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv,
+                                                       __uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+    if (qtr == 0) sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = row_ok ? lse_n : -INFINITY;
+  }
+}
+
+// Work items of a unit: (KV tile j, query tile t), n = j * NT + t, processed
+// in that order by all 16 softmax warps.  TMEM: two S buffers [0,128) and
+// [128,256) alternate by global item parity, O_t at [256 + 128 t, +128).  The
+// MMA issuer keeps the tensor pipe one item ahead: after P(n) it issues
+// PV(n) then S(n + 2) (into the buffer P(n) just vacated -- in-order pipe),
+// so S(n + 1) is already computed when the softmax finishes item n and the
+// softmax warps run items back to back.
 template <int NT, int EMU>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     tree_attn_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_tk,
                                   const __grid_constant__ CUtensorMap tm_tv, const Sm100Params sp) {
@@ -160,11 +310,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 256, 1)
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.s_full[b], 1);
+      mbar_init(&sm.p_full[b], 2 * kSoftmaxWarps);  // one arrival per softmax warp of both CTAs
+    }
     for (int t = 0; t < NT; ++t) {
-      mbar_init(&sm.s_full[t], 1);
-      mbar_init(&sm.p_full[t], 512);  // 2 CTAs x 256 softmax threads
       mbar_init(&sm.o_done[t], 1);
-      mbar_init(&sm.o_free[t], 512);
+      mbar_init(&sm.o_free[t], 2 * kSoftmaxWarps);
     }
     fence_barrier_init();
   }
@@ -246,133 +398,164 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + NT * 256, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
-    if (rank == 0 && lane == 0) {
+    // The whole warp walks the schedule (warp-uniform control flow and
+    // descriptors in uniform registers); one elected lane issues.  A single
+    // divergent issuing thread made ptxas wrap every tcgen05.mma in an
+    // R2UR / ELECT loop (~16 instructions per MMA), which starved the tensor
+    // pipe once the softmax warps saturated the issue slots.
+    if (rank == 0) {
       constexpr uint32_t idesc_s = make_idesc2(false);
       constexpr uint32_t idesc_o = make_idesc2(true);
-      const uint32_t q_base = smem_u32(sm.q[0]);
-      auto issue_s = [&](int t, int s) {
-        const uint32_t qa = q_base + t * kTileBytes;
-        const uint32_t ka = smem_u32(sm.k[s]);
-#pragma unroll
-        for (int k = 0; k < kHeadDim / 16; ++k) {
-          mma2_ss(tmem + t * 128, sw128_desc(qa + (k >> 2) * kChunkBytes + (k & 3) * 32, 16, 1024),
-                  sw128_desc(ka + (k >> 2) * kKChunk + (k & 3) * 32, 16, 1024), idesc_s, k > 0);
-        }
-      };
-      auto issue_pv = [&](int t, int s, bool acc) {
-        const uint32_t va = smem_u32(sm.v[s]);
-#pragma unroll
-        for (int k = 0; k < kTileN / 16; ++k) {
-          mma2_ts(tmem + 256 + t * 128, tmem + t * 128 + k * 8, sw128_desc(va + k * 2048, kHalfBytes, 1024), idesc_o,
-                  (acc || k > 0) ? 1u : 0u);
-        }
-      };
-      uint32_t g_tile = 0, g_q = 0;
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint64_t q_desc = sw128_desc(smem_u32(sm.q[0]), 16, 1024);
+      const uint64_t k_desc = sw128_desc(smem_u32(sm.k[0]), 16, 1024);
+      const uint64_t v_desc = sw128_desc(smem_u32(sm.v[0]), kHalfBytes, 1024);
+      uint32_t g_tile = 0, g_q = 0, g_item = 0;
       ItemIter iter(sp, worker);
       Item item;
       while (iter.next(sp, item)) {
         const ItemGeo geo = item_geo(sp, item, g);
         if (!geo.active) continue;
-        mbar_wait(&sm.q_full, g_q & 1);
-        mbar_wait(&sm.k_full[g_tile % kStages2], (g_tile / kStages2) & 1);
-        tc_fence_after();
-        for (int t = 0; t < NT; ++t) {
-          issue_s(t, g_tile % kStages2);
-          tc_commit2(&sm.s_full[t]);
-        }
-        tc_commit2(&sm.k_empty[g_tile % kStages2]);
-        for (int it = 0; it < geo.n_tiles; ++it) {
-          const uint32_t gt = g_tile + it;
-          const int s = gt % kStages2;
-          TRACE(12, gt);
-          mbar_wait(&sm.v_full[s], (gt / kStages2) & 1);
-          TRACE(13, gt);
-          tc_fence_after();
-          for (int t = 0; t < NT; ++t) {
-            TRACE(0 + t * 3, gt);
-            mbar_wait_cluster(&sm.p_full[t], gt & 1);
-            TRACE(1 + t * 3, gt);
-            if (it == 0) mbar_wait_cluster(&sm.o_free[t], (g_q & 1) ^ 1);
+        const int n_tiles = __shfl_sync(0xffffffffu, geo.n_tiles, 0);
+        const int N = NT * n_tiles;
+        // S(n) = Q_t K_j^T into S buffer (g_item + n) & 1 (descriptor start
+        // addresses are in 16-byte units, low 14 bits: smem < 256 KB, no carry)
+        auto issue_item_s = [&](int n) {
+          const int j = n / NT, t = n % NT;
+          const uint32_t gt = g_tile + j;
+          const int st = gt % kStages2;
+          if (t == 0) {
+            mbar_wait(&sm.k_full[st], (gt / kStages2) & 1);
             tc_fence_after();
-            issue_pv(t, s, it > 0);
-            tc_commit2(&sm.o_done[t]);
-            if (it + 1 < geo.n_tiles) {
-              const int s2 = (gt + 1) % kStages2;
-              if (t == 0) {
-                mbar_wait(&sm.k_full[s2], ((gt + 1) / kStages2) & 1);
-                tc_fence_after();
-              }
-              issue_s(t, s2);
-              tc_commit2(&sm.s_full[t]);
-              if (t == NT - 1) tc_commit2(&sm.k_empty[s2]);
-            }
-            TRACE(2 + t * 3, gt);
           }
-          tc_commit2(&sm.v_empty[s]);
+          if (elect_one()) {
+            const uint32_t d = tm + ((g_item + n) & 1) * 128;
+            const uint64_t qd = q_desc + (uint64_t)((t * kTileBytes) >> 4);
+            const uint64_t kd = k_desc + (uint64_t)((st * kHalfBytes) >> 4);
+#pragma unroll
+            for (int k = 0; k < kHeadDim / 16; ++k)
+              mma2_ss(d, qd + (uint64_t)(((k >> 2) * kChunkBytes + (k & 3) * 32) >> 4),
+                      kd + (uint64_t)(((k >> 2) * kKChunk + (k & 3) * 32) >> 4), idesc_s, k > 0);
+            tc_commit2(&sm.s_full[(g_item + n) & 1]);
+            if (t == NT - 1) tc_commit2(&sm.k_empty[st]);
+          }
+          __syncwarp();
+        };
+        mbar_wait(&sm.q_full, g_q & 1);
+        tc_fence_after();
+        issue_item_s(0);
+        if (N > 1) issue_item_s(1);
+        for (int n = 0; n < N; ++n) {
+          const int j = n / NT, t = n % NT;
+          const uint32_t gt = g_tile + j;
+          const int st = gt % kStages2;
+          const uint32_t gi = g_item + n;
+          if (t == 0) mbar_wait(&sm.v_full[st], (gt / kStages2) & 1);
+          TRACE(0, gi);
+          mbar_wait_cluster(&sm.p_full[gi & 1], (gi >> 1) & 1);
+          TRACE(1, gi);
+          if (j == 0) mbar_wait_cluster(&sm.o_free[t], (g_q & 1) ^ 1);  // previous unit's epilogue read O_t
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a = tm + (gi & 1) * 128;
+            const uint64_t vd = v_desc + (uint64_t)((st * kHalfBytes) >> 4);
+#pragma unroll
+            for (int k = 0; k < kTileN / 16; ++k)
+              mma2_ts(tm + 256 + t * 128, a + k * 8, vd + (uint64_t)((k * 2048) >> 4), idesc_o,
+                      (j > 0 || k > 0) ? 1u : 0u);
+            tc_commit2(&sm.o_done[t]);
+            if (t == NT - 1) tc_commit2(&sm.v_empty[st]);
+          }
+          __syncwarp();
+          if (n + 2 < N) issue_item_s(n + 2);
+          TRACE(2, gi);
         }
-        tc_commit2(&sm.q_empty);
-        g_tile += geo.n_tiles;
+        if (elect_one()) tc_commit2(&sm.q_empty);
+        __syncwarp();
+        g_tile += n_tiles;
+        g_item += N;
         ++g_q;
       }
     }
   } else if (warp >= 4) {
-    // ===================== softmax (both CTAs, own 128 rows per tile) ==========
-    // 8 warps per query tile: lane group (warp % 4) x column half (0/1)
-    const int t = (warp - 4) >> 3;
-    const int ww = (warp - 4) & 7;
-    const int lg = ww & 3, half = ww >> 2;
-    const int i = (lg << 5) + lane;
-    const int bar_id = 1 + t * 4 + lg;
+    // ===================== softmax (both CTAs, all 16 warps per item) =========
+    const int lg = warp & 3;            // TMEM lane group (warp % 4 by hardware rule)
+    const int qtr = (warp - 4) >> 2;    // column quarter
+    const int i = (lg << 5) + lane;     // row within the CTA's 128-row half of a query tile
+    const int bar_id = 1 + lg;
     const uint32_t lane_off = (uint32_t)(lg * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + t * 128;
-    const uint32_t t_o = tmem + lane_off + 256 + t * 128;
-    const int local = t * 2 * kTileM + (int)rank * kTileM + i;  // row within the unit
-    uint32_t g_tile = 0;
+    uint32_t g_item = 0, g_o = 0;
     ItemIter iter(sp, worker);
     Item item;
     while (iter.next(sp, item)) {
       const ItemGeo geo = item_geo(sp, item, g);
+      int local[NT];
+      bool row_ok[NT];
+      const uint32_t *mrow[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        local[t] = t * 2 * kTileM + (int)rank * kTileM + i;
+        const int rho = geo.row0 + local[t];
+        row_ok[t] = rho < geo.rows_total;
+        const int node = min(rho / g, max(geo.n_nodes - 1, 0));
+        mrow[t] = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
+      }
       if (!geo.active) {
-        if (half == 0) inactive_row(sp, item, geo, g, local);
+        if (qtr == 0)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) inactive_row(sp, item, geo, g, local[t]);
         continue;
       }
-      const int rho = geo.row0 + local;
-      const bool row_ok = rho < geo.rows_total;
-      const int node = min(rho / g, max(geo.n_nodes - 1, 0));
-      const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
-      float m = -INFINITY, l = 0.f;
-      for (int it = 0; it < geo.n_tiles; ++it) {
-        const uint32_t gt = g_tile + it;
-        const bool pref = it < geo.n_pref;
-        const int key0 = pref ? (geo.pa + it) * kTileN : (geo.sa + it - geo.n_pref) * kTileN;
-        const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
-        if (rank == 0 && ww == 0 && lane == 0) TRACE(6 + t * 3, gt);
-        mbar_wait(&sm.s_full[t], gt & 1);
-        tc_fence_after();
-        if (rank == 0 && ww == 0 && lane == 0) TRACE(7 + t * 3, gt);
-        softmax_half_tile<EMU>(t_s, t_o, half, sl2, it == 0, pref, kvalid, mrow, key0, p.n_words, row_ok,
-                               &sm.xch[t][gt & 1][0][0], i,
-                               bar_id, m, l);
-        if (rank == 0 && ww == 0 && lane == 0) TRACE(8 + t * 3, gt);
-        if (rank == 0)
-          mbar_arrive(&sm.p_full[t]);
-        else
-          mbar_arrive_leader(&sm.p_full[t]);
+      float m[NT], l[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        m[t] = -INFINITY;
+        l[t] = 0.f;
       }
-      mbar_wait(&sm.o_done[t], (g_tile + geo.n_tiles - 1) & 1);
-      tc_fence_after();
-      // combine the two partial row sums (the max m is identical in both halves)
-      sm.xch[t][2][half][i] = l;
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-      const float l_full = l + sm.xch[t][2][half ^ 1][i];
-      epilogue_half_row(sp, item, geo, g, local, half, t_o, m, l_full);
-      tc_fence_before();
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // xch reuse
-      if (rank == 0)
-        mbar_arrive(&sm.o_free[t]);
-      else
-        mbar_arrive_leader(&sm.o_free[t]);
-      g_tile += geo.n_tiles;
+      for (int j = 0; j < geo.n_tiles; ++j) {
+        const bool pref = j < geo.n_pref;
+        const int key0 = pref ? (geo.pa + j) * kTileN : (geo.sa + j - geo.n_pref) * kTileN;
+        const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const uint32_t gi = g_item + j * NT + t;
+          if (rank == 0 && warp == 4 && lane == 0) TRACE(3, gi);
+          mbar_wait(&sm.s_full[gi & 1], (gi >> 1) & 1);
+          tc_fence_after();
+          if (rank == 0 && warp == 4 && lane == 0) TRACE(4, gi);
+          softmax_quarter<EMU>(tmem + lane_off + (gi & 1) * 128, tmem + lane_off + 256 + t * 128, qtr, sl2, j == 0,
+                               pref, kvalid, mrow[t], key0, p.n_words, row_ok[t], &sm.xmax[gi & 1][0][0], i, bar_id,
+                               m[t], l[t]);
+          __syncwarp();
+          if (lane == 0) {
+            if (rank == 0)
+              mbar_arrive(&sm.p_full[gi & 1]);
+            else
+              mbar_arrive_leader(&sm.p_full[gi & 1]);
+          }
+          if (rank == 0 && warp == 4 && lane == 0) TRACE(5, gi);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        mbar_wait(&sm.o_done[t], (g_o + geo.n_tiles - 1) & 1);
+        tc_fence_after();
+        sm.xsum[qtr][i] = l[t];
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        const float l_full = (sm.xsum[0][i] + sm.xsum[1][i]) + (sm.xsum[2][i] + sm.xsum[3][i]);
+        epilogue_quarter(sp, item, geo, g, local[t], qtr, tmem + lane_off + 256 + t * 128, m[t], l_full);
+        tc_fence_before();
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");  // xsum reuse
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0)
+            mbar_arrive(&sm.o_free[t]);
+          else
+            mbar_arrive_leader(&sm.o_free[t]);
+        }
+      }
+      g_o += geo.n_tiles;
+      g_item += NT * geo.n_tiles;
     }
   }
   tc_fence_before();
@@ -392,7 +575,7 @@ int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap 
     const size_t smem = sizeof(Smem2<NT>) + 1024;                                                                \
     cudaFuncSetAttribute(tree_attn_tcgen05_pair_kernel<NT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                          (int)smem);                                                                             \
-    tree_attn_tcgen05_pair_kernel<NT, EMU><<<grid, 128 + NT * 256, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);   \
+    tree_attn_tcgen05_pair_kernel<NT, EMU><<<grid, kPairThreads, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);   \
   } while (0)
   if (sp.nt == 2) {
     if (emu == 0) SDB_LAUNCH_PAIR(2, 0); else if (emu == 2) SDB_LAUNCH_PAIR(2, 2); else SDB_LAUNCH_PAIR(2, 1);

@@ -1,0 +1,139 @@
+// Throughput of the exp2 paths on one SM (results per clock per SM):
+// MUFU.EX2 f32, ex2.approx.f16x2, ex2.approx.ftz.bf16x2, FFMA2.
+// usage: nvcc -gencode arch=compute_100a,code=sm_100a -O3 mufu_bench.cu -o mufu && ./mufu
+#include <cstdio>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+constexpr int ITERS = 4096;
+
+__global__ void k_f32(float *out, long long *cyc) {
+  float a[8];
+  for (int i = 0; i < 8; ++i) a[i] = -0.001f * (threadIdx.x + i);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+__global__ void k_f16x2(float *out, long long *cyc) {
+  uint32_t a[8];
+  for (int i = 0; i < 8; ++i) {
+    __half2 h = __floats2half2_rn(-0.001f * threadIdx.x, -0.002f * i);
+    a[i] = *reinterpret_cast<uint32_t *>(&h);
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(a[i]));
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += __low2float(*reinterpret_cast<__half2 *>(&a[i]));
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+__global__ void k_bf16x2(float *out, long long *cyc) {
+  uint32_t a[8];
+  for (int i = 0; i < 8; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(-0.001f * threadIdx.x, -0.002f * i);
+    a[i] = *reinterpret_cast<uint32_t *>(&h);
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(a[i]));
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += __low2float(*reinterpret_cast<__nv_bfloat162 *>(&a[i]));
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+__global__ void k_ffma2(float *out, long long *cyc) {
+  uint64_t a[8];
+  for (int i = 0; i < 8; ++i) a[i] = (uint64_t)__float_as_uint(0.001f * i) | ((uint64_t)__float_as_uint(0.5f) << 32);
+  const uint64_t b = (uint64_t)__float_as_uint(0.999f) | ((uint64_t)__float_as_uint(0.999f) << 32);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(a[i]) : "l"(b));
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += __uint_as_float((uint32_t)a[i]);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+// mixed: f16x2 conversion path per 2 elements: cvt f32x2->f16x2, ex2 f16x2, unpack to f32 x2
+__global__ void k_f16path(float *out, long long *cyc) {
+  float a[16];
+  for (int i = 0; i < 16; ++i) a[i] = -0.001f * (threadIdx.x + i);
+  float acc = 0.f;
+  uint32_t pk = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      uint32_t h;
+      asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(a[i + 1]), "f"(a[i]));
+      asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h));
+      float lo, hi;
+      asm volatile("{.reg .f16 l, h;\nmov.b32 {l, h}, %2;\ncvt.f32.f16 %0, l;\ncvt.f32.f16 %1, h;}" : "=f"(lo), "=f"(hi) : "r"(h));
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(hi), "f"(lo));
+      acc += lo + hi;
+      a[i] += 1e-7f;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc + pk;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <typename K>
+void run(const char *name, K kern, double results_per_thread_iter, int threads) {
+  float *out;
+  long long *cyc;
+  cudaMalloc(&out, 148 * 1024 * 4);
+  cudaMalloc(&cyc, 148 * 8);
+  kern<<<148, threads>>>(out, cyc);
+  kern<<<148, threads>>>(out, cyc);
+  cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  double c = 0;
+  for (int i = 0; i < 148; ++i) c += h[i];
+  c /= 148;
+  double res = results_per_thread_iter * ITERS * threads;
+  printf("%-10s threads %4d: %.2f results/clk/SM  (%.0f cycles)\n", name, threads, res / c, c);
+  cudaFree(out);
+  cudaFree(cyc);
+}
+
+int main() {
+  for (int t : {256, 512, 1024}) {
+    run("ex2.f32", k_f32, 8, t);
+    run("ex2.f16x2", k_f16x2, 16, t);
+    run("ex2.bf16x2", k_bf16x2, 16, t);
+    run("ffma2", k_ffma2, 16, t);
+    run("f16path", k_f16path, 16, t);
+  }
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

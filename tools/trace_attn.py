@@ -32,21 +32,15 @@ fn.argtypes = [ctypes.c_void_p]
 assert fn(buf.ctypes.data) == 0
 t0 = buf[buf > 0].min()
 b = buf.astype(np.int64) - int(t0)
-names = ["mma_pwait0", "mma_pok0", "mma_issued0", "mma_pwait1", "mma_pok1", "mma_issued1",
-         "sm0_swait", "sm0_sok", "sm0_done", "sm1_swait", "sm1_sok", "sm1_done", "mma_vwait", "mma_vok"]
-n = int((buf[7] > 0).sum())
-print("iterations traced", n)
-for it in range(min(n, 40)):
-    row = " ".join(f"{names[e][:9]}={b[e, it]:>8d}" for e in (12, 13, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11))
-    print(it, row)
-it = np.arange(5, min(n, 60))
-per_it = np.diff(b[7, 5:min(n, 60)])
-print("cycle per iteration (sm0 S-ready to S-ready): median", np.median(per_it))
-print("softmax0 duration (sok->done): median", np.median(b[8, it] - b[7, it]))
-print("softmax1 duration: median", np.median(b[11, it] - b[10, it]))
-print("sm0 waiting for S (swait->sok): median", np.median(b[7, it] - b[6, it]))
-print("mma waiting P0 (pwait->pok): median", np.median(b[1, it] - b[0, it]))
-print("mma waiting P1: median", np.median(b[4, it] - b[3, it]))
-print("P0 arrive -> mma sees it (sm0_done -> mma_pok0): median", np.median(b[1, it] - b[8, it]))
-print("mma issue PV0+S0 -> sm0 S ready next (issued0[it] -> sok[it+1]): median", np.median(b[7, it + 1] - b[2, it]))
-print("mma v wait: median", np.median(b[13, it] - b[12, it]))
+names = ["mma_pwait", "mma_pok", "mma_issued", "sm_swait", "sm_sok", "sm_done"]
+n = int((buf[4] > 0).sum())
+print("items traced", n)
+for it in range(min(n, 24)):
+    print(it, " ".join(f"{names[e]}={b[e, it]:>8d}" for e in range(6)))
+it = np.arange(8, min(n, 200))
+print("item period (sm S-ready to S-ready): median", np.median(np.diff(b[4, 8:min(n, 200)])))
+print("softmax duration (sok->done): median", np.median(b[5, it] - b[4, it]))
+print("softmax waiting for S (swait->sok): median", np.median(b[4, it] - b[3, it]))
+print("mma waiting P (pwait->pok): median", np.median(b[1, it] - b[0, it]))
+print("mma PV+S issue (pok->issued): median", np.median(b[2, it] - b[1, it]))
+print("P arrive -> mma sees it: median", np.median(b[1, it] - b[5, it]))

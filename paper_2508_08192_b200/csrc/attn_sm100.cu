@@ -395,7 +395,8 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   sp.p = p;
   sp.cta_group = (force_group == 1 || force_group == 2) ? force_group : (rows > kTileM ? 2 : 1);
   const int per_tile = kTileM * sp.cta_group;
-  sp.nt = rows > per_tile ? 2 : 1;
+  // pair kernel: one 256-row query tile per unit (three S slots fill TMEM)
+  sp.nt = (sp.cta_group == 1 && rows > per_tile) ? 2 : 1;
   sp.rows_unit = sp.nt * per_tile;
   sp.m_blocks = cdiv(rows, sp.rows_unit);
   sp.units = p.batch * p.hkv * sp.m_blocks;
@@ -459,7 +460,13 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *wor
     emu = emu < 0 ? 0 : (emu > 2 ? 2 : emu);
   }
   if (cg == 2) {
-    int rc = launch_2cta(mq, mk, mv, mtk, mtv, sp, emu, stream);
+    static int emu8 = -1;  // pair kernel: exp2 pairs of every 8 emulated on the FMA pipe
+    if (emu8 < 0) {
+      const char *e = getenv("SDB_ATTN_EMU8");
+      emu8 = e ? atoi(e) : 1;
+      emu8 = emu8 < 0 ? 0 : (emu8 > 4 ? 4 : emu8);
+    }
+    int rc = launch_2cta(mq, mk, mv, mtk, mtv, sp, emu8, stream);
     if (rc != SDB_OK) return rc;
   } else {
     dim3 grid(sp.n_workers);

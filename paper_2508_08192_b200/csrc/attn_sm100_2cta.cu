@@ -19,7 +19,8 @@
 namespace sdb {
 namespace sm100 {
 
-constexpr int kStages2 = 3;
+constexpr int kStagesK = 6;  // K ring: S(n) is issued ~3 items before its PV, so K needs the deeper ring
+constexpr int kStagesV = 4;
 
 #ifdef SDB_TRACE
 // [event][iteration] clock64 stamps of worker 0 (debug builds only)
@@ -121,119 +122,83 @@ __host__ __device__ constexpr uint32_t make_idesc2(bool b_mn_major) {
          ((uint32_t)(256 >> 4) << 24);
 }
 
-template <int NT>
 struct alignas(1024) Smem2 {
-  uint8_t q[NT][kTileBytes];
-  uint8_t k[kStages2][kHalfBytes];
-  uint8_t v[kStages2][kHalfBytes];
+  uint8_t q[kTileBytes];  // this CTA's 128 query rows
+  uint8_t k[kStagesK][kHalfBytes];
+  uint8_t v[kStagesV][kHalfBytes];
   uint64_t q_full, q_empty;
-  uint64_t k_full[kStages2], k_empty[kStages2], v_full[kStages2], v_empty[kStages2];
-  uint64_t s_full[2], p_full[2];  // per TMEM S buffer
-  uint64_t o_done[NT], o_free[NT];
+  uint64_t k_full[kStagesK], k_empty[kStagesK], v_full[kStagesV], v_empty[kStagesV];
+  uint64_t s_full[3], p_full[3], o_done[3];  // per TMEM S slot
+  uint64_t o_free;
   uint32_t tmem_base;
-  float xmax[2][4][128];  // quarter-row maxima, double-buffered by item parity
-  float xsum[4][128];     // quarter-row sums (epilogue)
+  float mref[3][128];  // running reference max after each item (log2 units), by slot
+  float lsum[3][128];  // per-warpgroup partial row sums at the end of a unit
+  float msum[3][128];  // ... and the reference max they are relative to
 };
 
-constexpr int kSoftmaxWarps = 16;  // 4 TMEM lane groups x 4 column quarters
-constexpr int kPairThreads = 128 + kSoftmaxWarps * 32;
+constexpr int kSoftmaxWG = 3;                       // softmax warpgroups (one per S slot)
+constexpr int kPairThreads = 128 + kSoftmaxWG * 128;
+constexpr int kSBase = 128;                          // TMEM: O [0,128), S slot s at 128 + 128 s
+constexpr int kBarUnit = 1 + 4 * kSoftmaxWG;         // named barrier: unit end, all softmax warps
 
-// Softmax of one item for this thread's row, columns [32 qtr, 32 qtr + 32) of
-// the S buffer at t_s.  The row max is combined with the 3 other quarters of
-// the row (same TMEM lane group) through shared memory under a 128-thread
-// named barrier; the row sum stays partial (combined in the epilogue; every
-// quarter applies the same max, so partial sums add).  P (bf16) for the
-// quarter lands in packed columns [16 qtr, 16 qtr + 16) -- every quarter has
-// loaded its S before the barrier.  O columns [32 qtr, +32) are rescaled in
-// place when the max grows by more than 2^8: the previous PV into this O
-// completed before this S was committed (in-order tensor pipe).
-template <int EMU>
-__device__ __forceinline__ void softmax_quarter(uint32_t t_s, uint32_t t_o, int qtr, float sl2, bool first, bool pref,
-                                                int kvalid, const uint32_t *mrow, int key0, int n_words, bool row_ok,
-                                                float *xmax, int row, int bar_id, float &m, float &l) {
-  const bool full = pref && kvalid >= kTileN;
-  uint32_t r[32];
-  SDB_TMEM_LD32(t_s + 32 * qtr, r);
-  uint32_t vm = 0xffffffffu;
-  if (!full) {
-    const int lim = kvalid - 32 * qtr;
-    const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
-    uint32_t bits = 0xffffffffu;
-    if (!pref) {
-      const int wi = (key0 >> 5) + qtr;
-      bits = (wi < n_words && row_ok) ? mrow[wi] : 0u;
-    }
-    vm = bits & low;
-  }
-  tmem_wait_ld();
-  if (!full) {
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if (!((vm >> e) & 1u)) r[e] = 0xff800000u;
-  }
-  float c0 = fmax3(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]));
-  float c1 = fmax3(__uint_as_float(r[3]), __uint_as_float(r[4]), __uint_as_float(r[5]));
-  float c2 = fmax3(__uint_as_float(r[6]), __uint_as_float(r[7]), __uint_as_float(r[8]));
-  float c3 = fmax3(__uint_as_float(r[9]), __uint_as_float(r[10]), __uint_as_float(r[11]));
-#pragma unroll
-  for (int e = 12; e < 28; e += 8) {
-    c0 = fmax3(c0, __uint_as_float(r[e + 0]), __uint_as_float(r[e + 1]));
-    c1 = fmax3(c1, __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
-    c2 = fmax3(c2, __uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
-    c3 = fmax3(c3, __uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
-  }
-  c0 = fmax3(c0, __uint_as_float(r[28]), __uint_as_float(r[29]));
-  c1 = fmax3(c1, __uint_as_float(r[30]), __uint_as_float(r[31]));
-  xmax[qtr * 128 + row] = fmax3(fmaxf(c0, c1), c2, c3);
-  asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-  const float mx = fmaxf(fmaxf(xmax[row], xmax[128 + row]), fmaxf(xmax[256 + row], xmax[384 + row])) * sl2;
-  float corr = 1.f;
-  bool rescale = false;
-  if (first) {
-    m = mx;
-  } else if (mx > m + kRescaleThreshold) {
-    corr = ex2(m - mx);
-    rescale = true;
-    m = mx;
-  }
-  const float neg_mu = (m == -INFINITY) ? 0.f : -m;
-  const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
-  uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+// 32 S values of one row (fp32 bits in r[0..31]) -> P = exp2(s * sl2 - m),
+// packed bf16 into r[0..15]; returns the sum of the 32 probabilities.
+// EMU8 of every 8 pairs run a cubic exp2 on the FMA pipe (offloads MUFU).
+template <int EMU8>
+__device__ __forceinline__ float exp_pack32(uint32_t *r, uint64_t sc2, uint64_t nm2) {
+  uint64_t acc2[2] = {0ull, 0ull};
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     float x0, x1, p0, p1;
     f2unpack(ffma2(f2pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
-    if ((e & 3) >= 4 - EMU) {
+    if ((e & 7) < EMU8) {
       ex2_emu2(x0, x1, p0, p1);
     } else {
       p0 = ex2(x0);
       p1 = ex2(x1);
     }
-    acc2[e & 3] = fadd2(acc2[e & 3], f2pack(p0, p1));
+    acc2[e & 1] = fadd2(acc2[e & 1], f2pack(p0, p1));
     r[e] = pack_bf16(p0, p1);
   }
-  float s0, s1, s2, s3, s4, s5, s6, s7;
+  float s0, s1;
   f2unpack(fadd2(acc2[0], acc2[1]), s0, s1);
-  f2unpack(fadd2(acc2[2], acc2[3]), s2, s3);
-  l = l * corr + ((s0 + s1) + (s2 + s3));
-  (void)s4; (void)s5; (void)s6; (void)s7;
-  SDB_TMEM_ST16(t_s + 16 * qtr, r);
-  if (rescale) {
-    uint32_t o[32];
-    SDB_TMEM_LD32(t_o + 32 * qtr, o);
-    tmem_wait_ld();
-#pragma unroll
-    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-    SDB_TMEM_ST32(t_o + 32 * qtr, o);
-  }
-  tmem_wait_st();
-  tc_fence_before();
+  return s0 + s1;
 }
 
-// Epilogue for a quarter row: O columns [32 qtr, +32) normalised by the full
-// row sum; quarter 0 also writes the LSE.
-__device__ __forceinline__ void epilogue_quarter(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,
-                                                 int local, int qtr, uint32_t t_o, float m, float l_full) {
+// Visibility bits of the 32 columns [c0, c0 + 32) of a key tile for this
+// row: prefix tiles -> keys < ctx; the suffix (tree) tile -> ancestor-or-self.
+__device__ __forceinline__ uint32_t vis_word(bool pref, int kvalid, const uint32_t *mrow, int key0, int n_words,
+                                             bool row_ok, int c0) {
+  const int lim = kvalid - c0;
+  const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+  uint32_t bits = 0xffffffffu;
+  if (!pref) {
+    const int wi = (key0 + c0) >> 5;
+    bits = (wi < n_words && row_ok) ? mrow[wi] : 0u;
+  }
+  return bits & low;
+}
+__device__ __forceinline__ void apply_mask32(uint32_t *r, uint32_t w) {
+#pragma unroll
+  for (int e = 0; e < 32; ++e)
+    if (!((w >> e) & 1u)) r[e] = 0xff800000u;
+}
+__device__ __forceinline__ float max32(const uint32_t *r) {
+  float c0 = fmax3(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]));
+  float c1 = fmax3(__uint_as_float(r[3]), __uint_as_float(r[4]), __uint_as_float(r[5]));
+#pragma unroll
+  for (int e = 6; e < 30; e += 4) {
+    c0 = fmax3(c0, __uint_as_float(r[e + 0]), __uint_as_float(r[e + 1]));
+    c1 = fmax3(c1, __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+  }
+  return fmax3(c0, c1, fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31])));
+}
+
+// Epilogue: O columns [32 c, 32 c + 32) of this row normalised by the row sum
+// (bf16 output of a whole unit, fp32 partial of a split one); chunk 0 writes
+// the LSE.
+__device__ __forceinline__ void epilogue_chunk(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,
+                                               int local, int c, uint32_t t_o, float m, float l_full) {
   const TreeAttnParams &p = sp.p;
   const int rho = geo.row0 + local;
   const bool row_ok = rho < geo.rows_total;
@@ -243,9 +208,9 @@ __device__ __forceinline__ void epilogue_quarter(const Sm100Params &sp, const It
   const float inv = l_full > 0.f ? 1.f / l_full : 0.f;
   const float lse_n = l_full > 0.f ? (m + __log2f(l_full)) * 0.6931471805599453f : -INFINITY;
   uint32_t r[32];
-  SDB_TMEM_LD32(t_o + 32 * qtr, r);
+  SDB_TMEM_LD32(t_o + 32 * c, r);
   tmem_wait_ld();
-  const int col0 = 32 * qtr;
+  const int col0 = 32 * c;
   if (item.whole) {
     if (in_range) {
       __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
@@ -263,7 +228,7 @@ __device__ __forceinline__ void epilogue_quarter(const Sm100Params &sp, const It
         }
         *reinterpret_cast<uint4 *>(o + e) = v;
       }
-      if (qtr == 0 && p.lse)
+      if (c == 0 && p.lse)
         p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = row_ok ? lse_n : -INFINITY;
     }
   } else {
@@ -272,24 +237,27 @@ __device__ __forceinline__ void epilogue_quarter(const Sm100Params &sp, const It
     for (int e = 0; e < 32; e += 4)
       *reinterpret_cast<float4 *>(o + e) = make_float4(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv,
                                                        __uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
-    if (qtr == 0) sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = row_ok ? lse_n : -INFINITY;
+    if (c == 0) sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = row_ok ? lse_n : -INFINITY;
   }
 }
 
-// Work items of a unit: (KV tile j, query tile t), n = j * NT + t, processed
-// in that order by all 16 softmax warps.  TMEM: two S buffers [0,128) and
-// [128,256) alternate by global item parity, O_t at [256 + 128 t, +128).  The
-// MMA issuer keeps the tensor pipe one item ahead: after P(n) it issues
-// PV(n) then S(n + 2) (into the buffer P(n) just vacated -- in-order pipe),
-// so S(n + 1) is already computed when the softmax finishes item n and the
-// softmax warps run items back to back.
-template <int NT, int EMU>
+// Items of a unit are its KV tiles n = 0 .. N-1 (one 256-row query tile per
+// pair, 128 rows per CTA).  Item n lives in TMEM S slot gi % 3 (gi = the
+// worker's running item count) and is softmaxed by warpgroup gi % 3, so the
+// three warpgroups work on three consecutive items at once and each has about
+// two items of tensor-pipe time to finish its own.  The online-softmax
+// reference max is handed from item to item along a chain of named barriers
+// (only the max: it is known after the first pass over S); each warpgroup
+// keeps its partial row sum relative to the last reference it saw, and the
+// partial sums are combined at the end of the unit.  The MMA issuer runs
+// PV(n) and then S(n + 3) into the slot P(n) just vacated (in-order pipe).
+template <int EMU8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     tree_attn_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_tk,
                                   const __grid_constant__ CUtensorMap tm_tv, const Sm100Params sp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Smem2<NT> &sm = *reinterpret_cast<Smem2<NT> *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Smem2 &sm = *reinterpret_cast<Smem2 *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const TreeAttnParams &p = sp.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = p.hq / p.hkv;
@@ -304,20 +272,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     }
     mbar_init(&sm.q_full, 1);
     mbar_init(&sm.q_empty, 1);
-    for (int s = 0; s < kStages2; ++s) {
+    for (int s = 0; s < kStagesK; ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < kStagesV; ++s) {
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.s_full[b], 1);
-      mbar_init(&sm.p_full[b], 2 * kSoftmaxWarps);  // one arrival per softmax warp of both CTAs
+    for (int s = 0; s < 3; ++s) {
+      mbar_init(&sm.s_full[s], 1);
+      mbar_init(&sm.p_full[s], 2 * 4);  // the 4 warps of the slot's warpgroup in both CTAs
+      mbar_init(&sm.o_done[s], 1);
     }
-    for (int t = 0; t < NT; ++t) {
-      mbar_init(&sm.o_done[t], 1);
-      mbar_init(&sm.o_free[t], 2 * kSoftmaxWarps);
-    }
+    mbar_init(&sm.o_free, 2 * 4 * kSoftmaxWG);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -329,14 +297,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 0) {
-    // ===================== TMA producer (both CTAs) =====================
+  if (warp == 0 || warp == 2) {
+    // ============ TMA producers (both CTAs): warp 0 Q + K ring, warp 2 V ring ============
+    // Each CTA loads its own half of every tile; completion bytes land on the
+    // leader's barriers.  Separate K and V producers so a K load never waits
+    // behind a V slot (and vice versa).
     if (lane == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      tma_prefetch(&tm_tk);
-      tma_prefetch(&tm_tv);
+      const bool kprod = warp == 0;
+      if (kprod) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_tk);
+      } else {
+        tma_prefetch(&tm_v);
+        tma_prefetch(&tm_tv);
+      }
       const int bs = p.block_size;
       const int seg_rows = bs < 64 ? bs : 64;
       const uint32_t l_qfull = leader_addr(&sm.q_full);
@@ -346,52 +321,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       while (iter.next(sp, item)) {
         const ItemGeo geo = item_geo(sp, item, g);
         if (!geo.active) continue;
-        mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
-        if (rank == 0) mbar_expect_tx(&sm.q_full, 2 * NT * kTileBytes);
-        for (int t = 0; t < NT; ++t) {
-          const int node0 = (geo.row0 + t * 2 * kTileM + (int)rank * kTileM) / g;
+        if (kprod) {
+          mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&sm.q_full, 2 * kTileBytes);
+          const int node0 = (geo.row0 + (int)rank * kTileM) / g;
           for (int c = 0; c < 2; ++c)
-            tma2_4d(sm.q[t] + c * kChunkBytes, &tm_q, l_qfull, c * 64, 0, geo.kvh, geo.b * p.r_max + node0);
+            tma2_4d(sm.q + c * kChunkBytes, &tm_q, l_qfull, c * 64, 0, geo.kvh, geo.b * p.r_max + node0);
         }
         ++g_q;
         const int n_valid_pages = (geo.C + bs - 1) / bs;
         const int32_t *bt = p.block_table + (int64_t)geo.b * p.max_blocks;
         for (int it = 0; it < geo.n_tiles; ++it, ++g_tile) {
-          const int s = g_tile % kStages2;
-          const uint32_t ph = (g_tile / kStages2) & 1;
           const bool pref = it < geo.n_pref;
           const int tile = pref ? geo.pa + it : geo.sa + (it - geo.n_pref);
-          // K half: keys [tile*128 + rank*64, +64), all 128 head-dim columns
-          mbar_wait(&sm.k_empty[s], ph ^ 1);
-          if (rank == 0) mbar_expect_tx(&sm.k_full[s], 2 * kHalfBytes);
-          const uint32_t l_kfull = leader_addr(&sm.k_full[s]);
-          if (pref) {
-            for (int r0 = 0; r0 < 64; r0 += seg_rows) {
-              const int key = tile * kTileN + (int)rank * 64 + r0;
-              const int lp = key / bs;
-              const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;  // OOB page -> zero fill
-              const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
-              for (int c = 0; c < 2; ++c) tma2_2d(sm.k[s] + c * kKChunk + r0 * 128, &tm_k, l_kfull, c * 64, rowc);
+          if (kprod) {
+            // K half: keys [tile*128 + rank*64, +64), all 128 head-dim columns
+            const int s = g_tile % kStagesK;
+            mbar_wait(&sm.k_empty[s], ((g_tile / kStagesK) & 1) ^ 1);
+            if (rank == 0) mbar_expect_tx(&sm.k_full[s], 2 * kHalfBytes);
+            const uint32_t l_kfull = leader_addr(&sm.k_full[s]);
+            if (pref) {
+              for (int r0 = 0; r0 < 64; r0 += seg_rows) {
+                const int key = tile * kTileN + (int)rank * 64 + r0;
+                const int lp = key / bs;
+                const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;  // OOB page -> zero fill
+                const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
+                for (int c = 0; c < 2; ++c) tma2_2d(sm.k[s] + c * kKChunk + r0 * 128, &tm_k, l_kfull, c * 64, rowc);
+              }
+            } else {
+              for (int c = 0; c < 2; ++c)
+                tma2_3d(sm.k[s] + c * kKChunk, &tm_tk, l_kfull, c * 64, geo.kvh,
+                        geo.b * p.r_max + tile * kTileN + (int)rank * 64);
             }
           } else {
-            for (int c = 0; c < 2; ++c)
-              tma2_3d(sm.k[s] + c * kKChunk, &tm_tk, l_kfull, c * 64, geo.kvh,
-                      geo.b * p.r_max + tile * kTileN + (int)rank * 64);
-          }
-          // V half: all 128 keys, head-dim columns [rank*64, +64)
-          mbar_wait(&sm.v_empty[s], ph ^ 1);
-          if (rank == 0) mbar_expect_tx(&sm.v_full[s], 2 * kHalfBytes);
-          const uint32_t l_vfull = leader_addr(&sm.v_full[s]);
-          if (pref) {
-            for (int r0 = 0; r0 < kTileN; r0 += seg_rows) {
-              const int key = tile * kTileN + r0;
-              const int lp = key / bs;
-              const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;
-              const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
-              tma2_2d(sm.v[s] + r0 * 128, &tm_v, l_vfull, (int)rank * 64, rowc);
+            // V half: all 128 keys, head-dim columns [rank*64, +64)
+            const int s = g_tile % kStagesV;
+            mbar_wait(&sm.v_empty[s], ((g_tile / kStagesV) & 1) ^ 1);
+            if (rank == 0) mbar_expect_tx(&sm.v_full[s], 2 * kHalfBytes);
+            const uint32_t l_vfull = leader_addr(&sm.v_full[s]);
+            if (pref) {
+              for (int r0 = 0; r0 < kTileN; r0 += seg_rows) {
+                const int key = tile * kTileN + r0;
+                const int lp = key / bs;
+                const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;
+                const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
+                tma2_2d(sm.v[s] + r0 * 128, &tm_v, l_vfull, (int)rank * 64, rowc);
+              }
+            } else {
+              tma2_3d(sm.v[s], &tm_tv, l_vfull, (int)rank * 64, geo.kvh, geo.b * p.r_max + tile * kTileN);
             }
-          } else {
-            tma2_3d(sm.v[s], &tm_tv, l_vfull, (int)rank * 64, geo.kvh, geo.b * p.r_max + tile * kTileN);
           }
         }
       }
@@ -407,7 +385,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       constexpr uint32_t idesc_s = make_idesc2(false);
       constexpr uint32_t idesc_o = make_idesc2(true);
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-      const uint64_t q_desc = sw128_desc(smem_u32(sm.q[0]), 16, 1024);
+      const uint64_t q_desc = sw128_desc(smem_u32(sm.q), 16, 1024);
       const uint64_t k_desc = sw128_desc(smem_u32(sm.k[0]), 16, 1024);
       const uint64_t v_desc = sw128_desc(smem_u32(sm.v[0]), kHalfBytes, 1024);
       uint32_t g_tile = 0, g_q = 0, g_item = 0;
@@ -416,146 +394,220 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       while (iter.next(sp, item)) {
         const ItemGeo geo = item_geo(sp, item, g);
         if (!geo.active) continue;
-        const int n_tiles = __shfl_sync(0xffffffffu, geo.n_tiles, 0);
-        const int N = NT * n_tiles;
-        // S(n) = Q_t K_j^T into S buffer (g_item + n) & 1 (descriptor start
+        const int N = __shfl_sync(0xffffffffu, geo.n_tiles, 0);
+        // S(n) = Q K_n^T into slot (g_item + n) % 3 (descriptor start
         // addresses are in 16-byte units, low 14 bits: smem < 256 KB, no carry)
-        auto issue_item_s = [&](int n) {
-          const int j = n / NT, t = n % NT;
-          const uint32_t gt = g_tile + j;
-          const int st = gt % kStages2;
-          if (t == 0) {
-            mbar_wait(&sm.k_full[st], (gt / kStages2) & 1);
-            tc_fence_after();
-          }
+        auto issue_s = [&](int n) {
+          const uint32_t gt = g_tile + n;
+          const int st = gt % kStagesK;
+          const int slot = (g_item + n) % 3;
+          mbar_wait(&sm.k_full[st], (gt / kStagesK) & 1);
+          tc_fence_after();
           if (elect_one()) {
-            const uint32_t d = tm + ((g_item + n) & 1) * 128;
-            const uint64_t qd = q_desc + (uint64_t)((t * kTileBytes) >> 4);
             const uint64_t kd = k_desc + (uint64_t)((st * kHalfBytes) >> 4);
 #pragma unroll
             for (int k = 0; k < kHeadDim / 16; ++k)
-              mma2_ss(d, qd + (uint64_t)(((k >> 2) * kChunkBytes + (k & 3) * 32) >> 4),
+              mma2_ss(tm + kSBase + slot * 128, q_desc + (uint64_t)(((k >> 2) * kChunkBytes + (k & 3) * 32) >> 4),
                       kd + (uint64_t)(((k >> 2) * kKChunk + (k & 3) * 32) >> 4), idesc_s, k > 0);
-            tc_commit2(&sm.s_full[(g_item + n) & 1]);
-            if (t == NT - 1) tc_commit2(&sm.k_empty[st]);
+            tc_commit2(&sm.s_full[slot]);
+            tc_commit2(&sm.k_empty[st]);
           }
           __syncwarp();
         };
         mbar_wait(&sm.q_full, g_q & 1);
         tc_fence_after();
-        issue_item_s(0);
-        if (N > 1) issue_item_s(1);
+        for (int n = 0; n < 3 && n < N; ++n) issue_s(n);
         for (int n = 0; n < N; ++n) {
-          const int j = n / NT, t = n % NT;
-          const uint32_t gt = g_tile + j;
-          const int st = gt % kStages2;
+          const uint32_t gt = g_tile + n;
+          const int st = gt % kStagesV;
           const uint32_t gi = g_item + n;
-          if (t == 0) mbar_wait(&sm.v_full[st], (gt / kStages2) & 1);
+          const int slot = gi % 3;
+          mbar_wait(&sm.v_full[st], (gt / kStagesV) & 1);
           TRACE(0, gi);
-          mbar_wait_cluster(&sm.p_full[gi & 1], (gi >> 1) & 1);
+          mbar_wait_cluster(&sm.p_full[slot], (gi / 3) & 1);
           TRACE(1, gi);
-          if (j == 0) mbar_wait_cluster(&sm.o_free[t], (g_q & 1) ^ 1);  // previous unit's epilogue read O_t
+          if (n == 0) mbar_wait_cluster(&sm.o_free, (g_q & 1) ^ 1);  // previous unit's epilogue read O
           tc_fence_after();
           if (elect_one()) {
-            const uint32_t a = tm + (gi & 1) * 128;
+            // P of keys 16k .. 16k+15 at slot columns 32 (k/2) + 8 (k%2)
+            const uint32_t a = tm + kSBase + slot * 128;
             const uint64_t vd = v_desc + (uint64_t)((st * kHalfBytes) >> 4);
 #pragma unroll
             for (int k = 0; k < kTileN / 16; ++k)
-              mma2_ts(tm + 256 + t * 128, a + k * 8, vd + (uint64_t)((k * 2048) >> 4), idesc_o,
-                      (j > 0 || k > 0) ? 1u : 0u);
-            tc_commit2(&sm.o_done[t]);
-            if (t == NT - 1) tc_commit2(&sm.v_empty[st]);
+              mma2_ts(tm, a + 32 * (k >> 1) + 8 * (k & 1), vd + (uint64_t)((k * 2048) >> 4), idesc_o,
+                      (n > 0 || k > 0) ? 1u : 0u);
+            tc_commit2(&sm.o_done[slot]);
+            tc_commit2(&sm.v_empty[st]);
           }
           __syncwarp();
-          if (n + 2 < N) issue_item_s(n + 2);
+          if (n + 3 < N) issue_s(n + 3);
           TRACE(2, gi);
         }
         if (elect_one()) tc_commit2(&sm.q_empty);
         __syncwarp();
-        g_tile += n_tiles;
+        g_tile += N;
         g_item += N;
         ++g_q;
       }
     }
   } else if (warp >= 4) {
-    // ===================== softmax (both CTAs, all 16 warps per item) =========
-    const int lg = warp & 3;            // TMEM lane group (warp % 4 by hardware rule)
-    const int qtr = (warp - 4) >> 2;    // column quarter
-    const int i = (lg << 5) + lane;     // row within the CTA's 128-row half of a query tile
-    const int bar_id = 1 + lg;
+    // ===================== softmax: 3 warpgroups, one row per thread ===========
+    const int wg = (warp - 4) >> 2;
+    const int lg = warp & 3;         // TMEM lane group (warp % 4 by hardware rule)
+    const int i = (lg << 5) + lane;  // row within the CTA's 128 rows == TMEM lane
     const uint32_t lane_off = (uint32_t)(lg * 32) << 16;
-    uint32_t g_item = 0, g_o = 0;
+    const int local = (int)rank * kTileM + i;  // row within the 256-row unit
+    const int bar_in = 1 + wg * 4 + lg;                          // max handoff into this warpgroup
+    const int bar_out = 1 + ((wg + 1) % kSoftmaxWG) * 4 + lg;   // ... and out of it
+    const bool tr = rank == 0 && lg == 0 && lane == 0;
+    uint32_t g_item = 0;
     ItemIter iter(sp, worker);
     Item item;
     while (iter.next(sp, item)) {
       const ItemGeo geo = item_geo(sp, item, g);
-      int local[NT];
-      bool row_ok[NT];
-      const uint32_t *mrow[NT];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        local[t] = t * 2 * kTileM + (int)rank * kTileM + i;
-        const int rho = geo.row0 + local[t];
-        row_ok[t] = rho < geo.rows_total;
-        const int node = min(rho / g, max(geo.n_nodes - 1, 0));
-        mrow[t] = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
-      }
       if (!geo.active) {
-        if (qtr == 0)
-#pragma unroll
-          for (int t = 0; t < NT; ++t) inactive_row(sp, item, geo, g, local[t]);
+        if (wg == 0) inactive_row(sp, item, geo, g, local);
         continue;
       }
-      float m[NT], l[NT];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        m[t] = -INFINITY;
-        l[t] = 0.f;
-      }
-      for (int j = 0; j < geo.n_tiles; ++j) {
-        const bool pref = j < geo.n_pref;
-        const int key0 = pref ? (geo.pa + j) * kTileN : (geo.sa + j - geo.n_pref) * kTileN;
+      const int rho = geo.row0 + local;
+      const bool row_ok = rho < geo.rows_total;
+      const int node = min(rho / g, max(geo.n_nodes - 1, 0));
+      const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
+      const int N = geo.n_tiles;
+      float m_w = -INFINITY, l_w = 0.f;
+      bool seen = false;
+      for (int n = (int)((wg + 3 - g_item % 3) % 3); n < N; n += 3) {
+        const uint32_t gi = g_item + n;
+        const int slot = wg;
+        const bool pref = n < geo.n_pref;
+        const int key0 = pref ? (geo.pa + n) * kTileN : (geo.sa + n - geo.n_pref) * kTileN;
         const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const uint32_t gi = g_item + j * NT + t;
-          if (rank == 0 && warp == 4 && lane == 0) TRACE(3, gi);
-          mbar_wait(&sm.s_full[gi & 1], (gi >> 1) & 1);
-          tc_fence_after();
-          if (rank == 0 && warp == 4 && lane == 0) TRACE(4, gi);
-          softmax_quarter<EMU>(tmem + lane_off + (gi & 1) * 128, tmem + lane_off + 256 + t * 128, qtr, sl2, j == 0,
-                               pref, kvalid, mrow[t], key0, p.n_words, row_ok[t], &sm.xmax[gi & 1][0][0], i, bar_id,
-                               m[t], l[t]);
-          __syncwarp();
-          if (lane == 0) {
-            if (rank == 0)
-              mbar_arrive(&sm.p_full[gi & 1]);
-            else
-              mbar_arrive_leader(&sm.p_full[gi & 1]);
-          }
-          if (rank == 0 && warp == 4 && lane == 0) TRACE(5, gi);
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        mbar_wait(&sm.o_done[t], (g_o + geo.n_tiles - 1) & 1);
+        const bool full = pref && kvalid >= kTileN;
+        if (tr) TRACE(3, gi);
+        mbar_wait(&sm.s_full[slot], (gi / 3) & 1);
         tc_fence_after();
-        sm.xsum[qtr][i] = l[t];
-        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-        const float l_full = (sm.xsum[0][i] + sm.xsum[1][i]) + (sm.xsum[2][i] + sm.xsum[3][i]);
-        epilogue_quarter(sp, item, geo, g, local[t], qtr, tmem + lane_off + 256 + t * 128, m[t], l_full);
+        if (tr) TRACE(4, gi);
+        const uint32_t t_s = tmem + lane_off + kSBase + slot * 128;
+        uint32_t vm[4] = {~0u, ~0u, ~0u, ~0u};
+        if (!full) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) vm[c] = vis_word(pref, kvalid, mrow, key0, p.n_words, row_ok, 32 * c);
+        }
+        // pass 1: row max over four 32-column chunks, each load overlapped
+        // with the max of the previous chunk (chunk 3 stays in registers)
+        uint32_t r[32], r2[32];
+        SDB_TMEM_LD32(t_s + 0, r2);
+        SDB_TMEM_WAIT_LD_REGS(r2);
+        SDB_TMEM_LD32(t_s + 32, r);
+        if (!full) apply_mask32(r2, vm[0]);
+        float mx = max32(r2);
+        SDB_TMEM_WAIT_LD_REGS(r);
+        SDB_TMEM_LD32(t_s + 64, r2);
+        if (!full) apply_mask32(r, vm[1]);
+        mx = fmaxf(mx, max32(r));
+        SDB_TMEM_WAIT_LD_REGS(r2);
+        SDB_TMEM_LD32(t_s + 96, r);
+        if (!full) apply_mask32(r2, vm[2]);
+        mx = fmaxf(mx, max32(r2));
+        SDB_TMEM_WAIT_LD_REGS(r);
+        if (!full) apply_mask32(r, vm[3]);
+        mx = fmaxf(mx, max32(r));
+        mx *= sl2;
+        if (tr) TRACE(6, gi);
+        // reference max chain (lazy: moves only when the max grows by > 2^8)
+        float m_prev = -INFINITY;
+        if (gi > 0) {
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+          m_prev = sm.mref[(gi + 2) % 3][i];
+        }
+        if (tr) TRACE(7, gi);
+        const float m_ref = (n == 0 || mx > m_prev + kRescaleThreshold) ? mx : m_prev;
+        sm.mref[slot][i] = m_ref;
+        asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
+        const bool resc = n > 0 && m_ref != m_prev;
+        if (__any_sync(0xffffffffu, resc)) {
+          // O holds items < n relative to m_prev: wait for PV(n - 1), rescale in place
+          const float corr = resc ? ex2(m_prev - m_ref) : 1.f;
+          mbar_wait(&sm.o_done[(gi + 2) % 3], ((gi - 1) / 3) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            SDB_TMEM_LD32(tmem + lane_off + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            SDB_TMEM_ST32(tmem + lane_off + c * 32, o);
+          }
+        }
+        if (!seen) {
+          m_w = m_ref;
+          seen = true;
+        } else if (m_ref != m_w) {
+          l_w *= ex2(m_w - m_ref);
+          m_w = m_ref;
+        }
+        const float neg_mu = (m_ref == -INFINITY) ? 0.f : -m_ref;
+        const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
+        // pass 2: P of chunk c (keys 32c .. 32c+31) packed into columns
+        // [32c, 32c + 16) of the slot -- inside the chunk's own, already
+        // consumed S columns.  Chunk 3 first (still in registers); each
+        // reload is overlapped with the exps of the previous chunk.
+        SDB_TMEM_LD32(t_s + 0, r2);
+        float rs = exp_pack32<EMU8>(r, sc2, nm2);
+        SDB_TMEM_ST16(t_s + 96, r);
+        SDB_TMEM_WAIT_LD_REGS(r2);
+        SDB_TMEM_LD32(t_s + 32, r);
+        if (!full) apply_mask32(r2, vm[0]);
+        rs += exp_pack32<EMU8>(r2, sc2, nm2);
+        SDB_TMEM_ST16(t_s + 0, r2);
+        SDB_TMEM_WAIT_LD_REGS(r);
+        SDB_TMEM_LD32(t_s + 64, r2);
+        if (!full) apply_mask32(r, vm[1]);
+        rs += exp_pack32<EMU8>(r, sc2, nm2);
+        SDB_TMEM_ST16(t_s + 32, r);
+        SDB_TMEM_WAIT_LD_REGS(r2);
+        if (!full) apply_mask32(r2, vm[2]);
+        rs += exp_pack32<EMU8>(r2, sc2, nm2);
+        SDB_TMEM_ST16(t_s + 64, r2);
+        l_w += rs;
+        tmem_wait_st();
         tc_fence_before();
-        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");  // xsum reuse
         __syncwarp();
         if (lane == 0) {
           if (rank == 0)
-            mbar_arrive(&sm.o_free[t]);
+            mbar_arrive(&sm.p_full[slot]);
           else
-            mbar_arrive_leader(&sm.o_free[t]);
+            mbar_arrive_leader(&sm.p_full[slot]);
         }
+        if (tr) TRACE(5, gi);
       }
-      g_o += geo.n_tiles;
-      g_item += NT * geo.n_tiles;
+      // ---- unit end: combine the partial row sums, normalise, store ----
+      sm.lsum[wg][i] = l_w;
+      sm.msum[wg][i] = seen ? m_w : -INFINITY;
+      asm volatile("bar.sync %0, %1;" ::"r"(kBarUnit), "r"(kSoftmaxWG * 128) : "memory");
+      const uint32_t gl = g_item + N - 1;  // the unit's last item
+      const float m_fin = sm.mref[gl % 3][i];
+      float l_full = 0.f;
+#pragma unroll
+      for (int w = 0; w < kSoftmaxWG; ++w) {
+        const float mw = sm.msum[w][i];
+        if (mw != -INFINITY) l_full += sm.lsum[w][i] * ex2(mw - m_fin);
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(kBarUnit), "r"(kSoftmaxWG * 128) : "memory");
+      mbar_wait(&sm.o_done[gl % 3], (gl / 3) & 1);
+      tc_fence_after();
+      for (int c = wg; c < 4; c += kSoftmaxWG)
+        epilogue_chunk(sp, item, geo, g, local, c, tmem + lane_off, m_fin, l_full);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0)
+          mbar_arrive(&sm.o_free);
+        else
+          mbar_arrive_leader(&sm.o_free);
+      }
+      g_item += N;
     }
   }
   tc_fence_before();
@@ -570,17 +622,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const CUtensorMap &mtk,
                 const CUtensorMap &mtv, const Sm100Params &sp, int emu, cudaStream_t stream) {
   dim3 grid(sp.n_workers * 2);
-#define SDB_LAUNCH_PAIR(NT, EMU)                                                                                 \
-  do {                                                                                                           \
-    const size_t smem = sizeof(Smem2<NT>) + 1024;                                                                \
-    cudaFuncSetAttribute(tree_attn_tcgen05_pair_kernel<NT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                         (int)smem);                                                                             \
-    tree_attn_tcgen05_pair_kernel<NT, EMU><<<grid, kPairThreads, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);   \
+  const size_t smem = sizeof(Smem2) + 1024;
+#define SDB_LAUNCH_PAIR(EMU8)                                                                                      \
+  do {                                                                                                             \
+    cudaFuncSetAttribute(tree_attn_tcgen05_pair_kernel<EMU8>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                         (int)smem);                                                                               \
+    tree_attn_tcgen05_pair_kernel<EMU8><<<grid, kPairThreads, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);         \
   } while (0)
-  if (sp.nt == 2) {
-    if (emu == 0) SDB_LAUNCH_PAIR(2, 0); else if (emu == 2) SDB_LAUNCH_PAIR(2, 2); else SDB_LAUNCH_PAIR(2, 1);
-  } else {
-    if (emu == 0) SDB_LAUNCH_PAIR(1, 0); else if (emu == 2) SDB_LAUNCH_PAIR(1, 2); else SDB_LAUNCH_PAIR(1, 1);
+  // emu: pairs of every 8 whose exp2 runs on the FMA pipe
+  switch (emu) {
+    case 0: SDB_LAUNCH_PAIR(0); break;
+    case 2: SDB_LAUNCH_PAIR(2); break;
+    case 3: SDB_LAUNCH_PAIR(3); break;
+    case 4: SDB_LAUNCH_PAIR(4); break;
+    default: SDB_LAUNCH_PAIR(1); break;
   }
 #undef SDB_LAUNCH_PAIR
   SDB_CHECK_LAUNCH();

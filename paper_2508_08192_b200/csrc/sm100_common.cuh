@@ -136,6 +136,18 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
                "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), \
                "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]))
 
+// tcgen05.wait::ld that also "redefines" the 32 destination registers of
+// the loads it waits for, so the compiler cannot hoist their uses above it
+// (the loads complete asynchronously; a plain wait carries no register
+// dependence).  Used when a load is overlapped with compute on other data.
+#define SDB_TMEM_WAIT_LD_REGS(r)                                                                                  \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                                    \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),  \
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),         \
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),       \
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),       \
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])::"memory")
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -180,27 +192,25 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return d;
 }
 
-// exp2 of two values on the FMA pipe (offloads the MUFU): 2^x = 2^floor(x) *
-// p(frac(x)), p a cubic fit of 2^f on [0, 1) with p(0) = 1 (max relative
-// error 8.6e-5, far below the bf16 rounding of P).
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// exp2 of two values on the FMA pipe (offloads the MUFU): 2^x = 2^n * p(f),
+// n = round(x), f = x - n in [-1/2, 1/2], p a cubic fit of 2^f (max relative
+// error 7.7e-5, far below the bf16 rounding of P).  x is clamped at -126 so
+// the exponent add stays in range (2^-126 underflows to ~0 in P anyway).
+// 10 instructions per pair: 2 FMNMX, 3 FADD2, 3 FFMA2, 2 IMAD.
 __device__ __forceinline__ void ex2_emu2(float x, float y, float &ox, float &oy) {
-  constexpr float kRound = 12582912.0f;  // 2^23 + 2^22
-  const uint64_t xy = f2pack(fmaxf(x, -127.f), fmaxf(y, -127.f));
-  const uint64_t rr = fadd2_rm(xy, f2pack(kRound, kRound));  // floor(x) in the low mantissa bits
-  const uint64_t fl = fadd2(rr, f2pack(-kRound, -kRound));
-  float fx, fy;
-  {
-    float a, b, c, d;
-    f2unpack(xy, a, b);
-    f2unpack(fl, c, d);
-    fx = a - c;
-    fy = b - d;
-  }
-  const uint64_t f = f2pack(fx, fy);
-  uint64_t pp = f2pack(0.07706617563962936f, 0.07706617563962936f);
-  pp = ffma2(pp, f, f2pack(0.22764593362808228f, 0.22764593362808228f));
-  pp = ffma2(pp, f, f2pack(0.6951165795326233f, 0.6951165795326233f));
-  pp = ffma2(pp, f, f2pack(1.0f, 1.0f));
+  constexpr float kRound = 12582912.0f;  // 2^23 + 2^22: x + kRound rounds x to an integer
+  const uint64_t xy = f2pack(fmaxf(x, -126.f), fmaxf(y, -126.f));
+  const uint64_t rr = fadd2(xy, f2pack(kRound, kRound));  // n in the low mantissa bits
+  const uint64_t f = fsub2(xy, fadd2(rr, f2pack(-kRound, -kRound)));
+  uint64_t pp = ffma2(f2pack(0.05508868f, 0.05508868f), f, f2pack(0.24260405f, 0.24260405f));
+  pp = ffma2(pp, f, f2pack(0.69327624f, 0.69327624f));
+  pp = ffma2(pp, f, f2pack(0.99992894f, 0.99992894f));
   float px, py, rx, ry;
   f2unpack(pp, px, py);
   f2unpack(rr, rx, ry);

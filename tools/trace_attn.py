@@ -40,7 +40,14 @@ for it in range(min(n, 24)):
 it = np.arange(8, min(n, 200))
 print("item period (sm S-ready to S-ready): median", np.median(np.diff(b[4, 8:min(n, 200)])))
 print("softmax duration (sok->done): median", np.median(b[5, it] - b[4, it]))
+print("softmax WG item duration (sok->done): median", np.median(b[5, it] - b[4, it]))
 print("softmax waiting for S (swait->sok): median", np.median(b[4, it] - b[3, it]))
 print("mma waiting P (pwait->pok): median", np.median(b[1, it] - b[0, it]))
 print("mma PV+S issue (pok->issued): median", np.median(b[2, it] - b[1, it]))
 print("P arrive -> mma sees it: median", np.median(b[1, it] - b[5, it]))
+print("mma issued(n) -> pwait(n+1) (V wait + loop): median", np.median(b[0, it + 1] - b[2, it]))
+per = b[:, it]
+print("period mma: median", np.median(np.diff(b[1, 8:min(n, 200)])))
+print("softmax: S ready -> max pass done: median", np.median(b[6, it] - b[4, it]))
+print("softmax: max done -> chain ok: median", np.median(b[7, it] - b[6, it]))
+print("softmax: chain ok -> P arrived: median", np.median(b[5, it] - b[7, it]))

@@ -226,6 +226,13 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # all host cores for the numpy/BLAS reference (torchrun exports OMP_NUM_THREADS=1)
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(os.cpu_count() or 1)
+    except Exception:  # noqa: BLE001 - threadpoolctl is optional
+        pass
     samples = []
     for i in range(args.warmup + args.steps):
         ta, tacc, fa, facc = cpu_sample(cfg, seed=i)
@@ -274,10 +281,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SDB_BENCH_BACKEND=gloo exercises the sharded multi-rank path on a
+    # one-GPU box (ranks share cuda:0); the product path is NCCL.
+    backend = os.environ.get("SDB_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _lib.load()
     shard = shard_for(rank, world, cfg["Hq"], cfg["Hkv"], cfg["V"])
     x, R = make_inputs(cfg, shard, dev)
@@ -293,9 +307,21 @@ def main():
     for _ in range(args.warmup):
         ver.step(x)
     torch.cuda.synchronize()
-    use_graph = world == 1
+    # CUDA graph of the whole step (NCCL all-reduce included for N > 1: the
+    # communicator is warm after the eager warm-up steps); gloo cannot be
+    # captured and runs eagerly.
+    use_graph = world == 1 or backend == "nccl"
     if use_graph:
-        ver.capture(x)
+        try:
+            ver.capture(x)
+        except Exception as e:  # noqa: BLE001 - fall back to eager steps, reported in config.graph
+            print(f"[bench] rank {rank}: graph capture failed ({e}); timing eager steps", file=sys.stderr)
+            use_graph = False
+            torch.cuda.synchronize()
+        if world > 1:  # every rank times the same mode
+            ok = torch.tensor([1 if use_graph else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            use_graph = bool(ok.item())
     torch.cuda.synchronize()
 
     def barrier():

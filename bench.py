@@ -43,7 +43,11 @@ CONFIGS = {
                V=128256),
     "c4": dict(workload="llama-3.1-405b-attn bs64 ctx32768 tree64 greedy", B=64, Hq=128, Hkv=8, d=128, ctx=32768,
                bs=64, V=128256),
+    # acceptance only (configs[4]): stochastic top-p MSS over 128k logits
+    "c5": dict(workload="stochastic top-p acceptance bs64 tree64 V128256 T1 p0.9", B=64, Hq=64, Hkv=8, d=128,
+               ctx=0, bs=64, V=128256, accept_only=True, mode="stochastic"),
 }
+TEMPERATURE, TOP_P = 1.0, 0.9
 
 
 def _augment(parent):
@@ -106,7 +110,7 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_inputs(cfg, shard, device, seed=0):
+def make_inputs(cfg, shard, device, seed=0, mode="greedy"):
     """Seeded synthetic inputs for one rank's shard (KV heads, vocab range)."""
     import torch
 
@@ -153,13 +157,26 @@ def make_inputs(cfg, shard, device, seed=0):
     parent_row = par.clamp(min=0).long()
     want = torch.gather(am, 1, parent_row)
     tokens = torch.where(rnd < 0.6, want, rtok).to(torch.int32)
+    draft = seeds = steps = None
+    if mode == "stochastic":
+        # draft = target + N(0, 0.5^2); node tokens sampled from
+        # the parent's draft q (stochastic drafting, engine.py:393-394)
+        draft_full = logits_full + 0.5 * torch.randn(B, R, V, generator=gl, device=device)
+        qd = torch.softmax(draft_full / TEMPERATURE, dim=-1)
+        samp = torch.multinomial(qd.reshape(B * R, V), 1, generator=gl).reshape(B, R)
+        tokens = torch.gather(samp, 1, parent_row).to(torch.int32)
+        del qd
+        draft = draft_full[:, :, shard.v_lo:shard.v_hi].contiguous()
+        del draft_full
+        seeds = torch.arange(B, dtype=torch.int64, device=device) + 1000 * (seed + 1)  # sampler.seed + seq
+        steps = torch.full((B,), 2 * 7 + 2, dtype=torch.int64, device=device)          # 2*round + 2
     tokens[:, 0] = 0
     logits = logits_full[:, :, shard.v_lo:shard.v_hi].contiguous()
     del logits_full
     x = StepInputs(parent=par, n_rows=torch.full((B,), R, dtype=torch.int32, device=device),
                    ctx_len=torch.full((B,), C, dtype=torch.int32, device=device), tokens=tokens, q=q.contiguous(),
                    tree_k=tk.contiguous(), tree_v=tv.contiguous(), logits=logits, k_pool=kp.contiguous(),
-                   v_pool=vp.contiguous(), block_table=table)
+                   v_pool=vp.contiguous(), block_table=table, draft_logits=draft, seeds=seeds, steps=steps)
     return x, R
 
 
@@ -174,11 +191,13 @@ def step_bytes_flops(cfg, shard, R, anc_pairs):
     return attn_bytes, accept_bytes, attn_flops
 
 
-def cpu_sample(cfg, seed=0):
+def cpu_sample(cfg, seed=0, mode="greedy"):
     """Reference algorithm (numpy oracle port) on a bounded sample of the
     workload: 1 sequence x 1 KV head group for attention, 1 sequence for
-    greedy acceptance.  Returns (seconds for the sample, extrapolation
-    factors)."""
+    acceptance (greedy: argmax target_dist per row + walk; stochastic:
+    top-p target_dist per row, draft q per parent row, mss_verify).  Returns
+    (attention seconds, acceptance seconds, attention and acceptance
+    extrapolation factors)."""
     import numpy as np
 
     from oracle import specdec_oracle as O
@@ -188,29 +207,39 @@ def cpu_sample(cfg, seed=0):
     g = Hq // Hkv
     aug = tuple(_augment(TREE64))
     R = len(aug)
-    pages = -(-(C + R) // bs)
+    parent = tuple(p - 1 if p > 0 else -1 for p in aug[1:])
+    ta = 0.0
+    if not cfg.get("accept_only"):
+        pages = -(-(C + R) // bs)
 
-    def bf(x):
-        return x.astype(np.float32).astype(np.float64)
+        def bf(x):
+            return x.astype(np.float32).astype(np.float64)
 
-    kp = bf(rng.normal(size=(pages + 1, 1, bs, d)))
-    vp = bf(rng.normal(size=(pages + 1, 1, bs, d)))
-    table = rng.permutation(pages + 1)[:pages]
-    q = bf(rng.normal(size=(R, g * d)))
-    tk = bf(rng.normal(size=(R, d)))
-    tv = bf(rng.normal(size=(R, d)))
+        kp = bf(rng.normal(size=(pages + 1, 1, bs, d)))
+        vp = bf(rng.normal(size=(pages + 1, 1, bs, d)))
+        table = rng.permutation(pages + 1)[:pages]
+        q = bf(rng.normal(size=(R, g * d)))
+        tk = bf(rng.normal(size=(R, d)))
+        tv = bf(rng.normal(size=(R, d)))
+        t0 = time.perf_counter()
+        ck = O.paged_gather(kp, table, C)
+        cv = O.paged_gather(vp, table, C)
+        O.tree_attention(q, ck, cv, tk, tv, aug, d ** -0.5, g, 1)
+        ta = time.perf_counter() - t0
     logits = (2.0 * rng.normal(size=(R, V))).astype(np.float32)
     toks = rng.integers(0, V, size=R)
-    t0 = time.perf_counter()
-    ck = O.paged_gather(kp, table, C)
-    cv = O.paged_gather(vp, table, C)
-    O.tree_attention(q, ck, cv, tk, tv, aug, d ** -0.5, g, 1)
     t1 = time.perf_counter()
-    dists = [O.target_dist(logits[i], 0.0, 1.0) for i in range(R)]
-    am = [int(np.argmax(dd)) for dd in dists]
-    O.greedy_walk(aug[1:] and tuple(p - 1 if p > 0 else -1 for p in aug[1:]), toks[1:], am)
-    t2 = time.perf_counter()
-    return (t1 - t0), (t2 - t1), B * Hkv, B
+    if mode == "greedy":
+        dists = [O.target_dist(logits[i], 0.0, 1.0) for i in range(R)]
+        am = [int(np.argmax(dd)) for dd in dists]
+        O.greedy_walk(parent, toks[1:], am)
+    else:
+        draft = (logits + 0.5 * rng.normal(size=(R, V))).astype(np.float32)
+        tdists = [O.target_dist(logits[i].astype(np.float64), TEMPERATURE, TOP_P) for i in range(R)]
+        qs = {p: O.target_dist(draft[p].astype(np.float64), TEMPERATURE, 1.0) for p in set(aug[1:])}
+        O.mss_verify(parent, toks[1:], [qs[p] for p in aug[1:]], tdists, O.uniform_row(seed, 16, R))
+    tacc = time.perf_counter() - t1
+    return ta, tacc, B * Hkv, B
 
 
 def blas_threads():
@@ -222,7 +251,16 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
-def run_reference(args, cfg):
+def _sample_desc(cfg, mode, cores):
+    acc = ("greedy target_dist + argmax walk" if mode == "greedy"
+           else f"top-p {TOP_P} target_dist per row + draft q per parent row + mss_verify")
+    att = ("" if cfg.get("accept_only") else
+           f"1 sequence x 1 KV-head group ({cfg['Hq'] // cfg['Hkv']} q heads) of the attention extrapolated "
+           f"x{cfg['B'] * cfg['Hkv']}, + ")
+    return f"{att}{acc} for 1 sequence x{cfg['B']}; numpy float64 oracle port, {cores} BLAS threads, extrapolated"
+
+
+def run_reference(args, cfg, mode):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -235,21 +273,47 @@ def run_reference(args, cfg):
         pass
     samples = []
     for i in range(args.warmup + args.steps):
-        ta, tacc, fa, facc = cpu_sample(cfg, seed=i)
+        ta, tacc, fa, facc = cpu_sample(cfg, seed=i, mode=mode)
         if i >= args.warmup:
             samples.append(ta * fa + tacc * facc)
     per_step = statistics.mean(samples)
     us = per_step * 1e6
     cores = blas_threads()
-    sample = (f"1 sequence x 1 KV-head group (8 q heads) of the attention extrapolated x{cfg['B'] * cfg['Hkv']}, "
-              f"+ greedy target_dist/mss walk for 1 sequence x{cfg['B']}; numpy float64, {cores} BLAS threads")
     line = {"impl": "reference", "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "global_batch": cfg["B"], "seq_len": cfg["ctx"]},
-            "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": "port", "sample": sample},
+            "config": {"workload": cfg["workload"], "global_batch": cfg["B"], "seq_len": cfg["ctx"], "mode": mode},
+            "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": "port",
+                             "sample": _sample_desc(cfg, mode, cores)},
             "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def graph_time(fn, iters, stream, use_graph=True):
+    """Mean device time of fn(): captured into a CUDA graph and replayed
+    `iters` times between two events (host launch gaps excluded); eager
+    launches when capture is not possible (gloo collectives)."""
+    import torch
+
+    g = None
+    if use_graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(stream)
+        with torch.cuda.stream(s):
+            fn()
+        stream.wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(iters):
+        g.replay() if g is not None else fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
 
 
 def main():
@@ -259,15 +323,21 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default=None, choices=["greedy", "stochastic"],
+                    help="acceptance mode (default: greedy, c5: stochastic)")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 tcgen05, 2 SIMT")
     ap.add_argument("--splits", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    mode = args.mode or cfg.get("mode", "greedy")
+    accept_only = bool(cfg.get("accept_only"))
+    if mode != "greedy" and not accept_only:
+        cfg["workload"] = cfg["workload"].replace("greedy", f"stochastic T{TEMPERATURE:g} top-p {TOP_P:g}")
     if args.impl == "reference":
-        run_reference(args, cfg)
+        run_reference(args, cfg, mode)
         return
 
     import numpy as np
@@ -275,7 +345,8 @@ def main():
     import torch.distributed as dist
 
     from paper_2508_08192_b200 import _lib
-    from paper_2508_08192_b200.sharding import ShardedGreedyAcceptor, shard_for
+    from paper_2508_08192_b200.kvstore import compact_kv
+    from paper_2508_08192_b200.sharding import ShardedGreedyAcceptor, ShardedStochasticAcceptor, shard_for
     from paper_2508_08192_b200.verify import TreeVerifier
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -294,29 +365,81 @@ def main():
             dist.init_process_group(backend)
     _lib.load()
     shard = shard_for(rank, world, cfg["Hq"], cfg["Hkv"], cfg["V"])
-    x, R = make_inputs(cfg, shard, dev)
+    x, R = make_inputs(cfg, shard, dev, mode=mode)
     from oracle import specdec_oracle as O  # checker only (mask popcount for the FLOP count)
 
-    anc_pairs = int(O.suffix_mask(tuple(_augment(TREE64))).sum())
-    ver = TreeVerifier(scale=cfg["d"] ** -0.5, max_ctx=cfg["ctx"], num_splits=args.splits, kernel=args.kernel)
+    aug = tuple(_augment(TREE64))
+    anc_pairs = int(O.suffix_mask(aug).sum())
+    n_parent_rows = len(set(p for p in aug[1:]))
+    temperature = 0.0 if mode == "greedy" else TEMPERATURE
+    ver = TreeVerifier(scale=cfg["d"] ** -0.5, temperature=temperature, top_p=TOP_P if mode != "greedy" else 1.0,
+                       max_ctx=max(cfg["ctx"], 1), num_splits=args.splits, kernel=args.kernel)
     if world > 1:
-        sharded = ShardedGreedyAcceptor(shard)
-        ver.greedy = lambda logits, parent, n_rows, tokens, stream=None: sharded(logits, parent, n_rows, tokens,
-                                                                                stream)
+        if mode == "greedy":
+            sharded = ShardedGreedyAcceptor(shard)
+            ver.greedy = lambda logits, parent, n_rows, tokens, stream=None: sharded(logits, parent, n_rows, tokens,
+                                                                                    stream)
+        else:
+            nch = max(sum(1 for q in aug if q == p_) for p_ in set(aug[1:]))
+            ver.stochastic = ShardedStochasticAcceptor(shard, max_children=nch)
     stream = torch.cuda.current_stream()
+    o = ver._buffers(x)
+
+    def part_build():
+        lib = _lib.lib()
+        b_, r_ = x.parent.shape
+        _lib.check(lib.sdb_tree_build(_lib.ptr(x.parent), _lib.ptr(x.n_rows), _lib.ptr(x.ctx_len), b_, r_,
+                                      o["mask"].shape[-1], _lib.ptr(o["mask"]), _lib.ptr(o["pos"]),
+                                      _lib.ptr(o["depth"]), _lib.ptr(o["tree_err"]), _lib.stream_ptr()), "tree_build")
+
+    def part_attn():
+        ver.attn(x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
+                 ver.scale, out=o["out"], lse=o["lse"], max_ctx=ver.max_ctx, num_splits=ver.num_splits,
+                 kernel=ver.kernel)
+
+    acc_box = {}
+
+    def part_accept():
+        if mode == "greedy":
+            acc_box["acc"] = ver.greedy(x.logits, x.parent, x.n_rows, x.tokens)
+        else:
+            acc_box["acc"] = ver.stochastic(x.logits, x.draft_logits, temperature, TOP_P, x.parent, x.n_rows,
+                                            x.tokens, None, seeds=x.seeds, steps=x.steps)
+
+    def part_compact():
+        acc = acc_box["acc"]
+        compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0), x.v_pool.unsqueeze(0),
+                   x.block_table, x.ctx_len, acc.path, acc.path_len)
+
+    if accept_only:
+        def step():
+            part_accept()
+    else:
+        def step():
+            return ver.step(x)
+
     for _ in range(args.warmup):
-        ver.step(x)
+        step()
     torch.cuda.synchronize()
-    # CUDA graph of the whole step (NCCL all-reduce included for N > 1: the
+    # CUDA graph of the whole step (NCCL collectives included for N > 1: the
     # communicator is warm after the eager warm-up steps); gloo cannot be
     # captured and runs eagerly.
     use_graph = world == 1 or backend == "nccl"
+    graph = None
     if use_graph:
         try:
-            ver.capture(x)
+            s_ = torch.cuda.Stream()
+            s_.wait_stream(stream)
+            with torch.cuda.stream(s_):
+                step()
+            stream.wait_stream(s_)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
         except Exception as e:  # noqa: BLE001 - fall back to eager steps, reported in config.graph
             print(f"[bench] rank {rank}: graph capture failed ({e}); timing eager steps", file=sys.stderr)
-            use_graph = False
+            use_graph, graph = False, None
             torch.cuda.synchronize()
         if world > 1:  # every rank times the same mode
             ok = torch.tensor([1 if use_graph else 0], dtype=torch.int32, device=dev)
@@ -337,9 +460,9 @@ def main():
         e0.record(stream)
         for _ in range(args.steps):
             if use_graph:
-                ver.replay()
+                graph.replay()
             else:
-                ver.step(x)
+                step()
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -349,66 +472,54 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
 
-    # ---- per-kernel breakdown (instrumented eager pass, same stream) -----
-    from paper_2508_08192_b200.attention import TreeVerifyAttention
-
-    o = ver._out[1]
-    n_ev = 5
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    # ---- per-kernel breakdown: each part graph-replayed alone ------------
     barrier()
-    torch.cuda.synchronize()
-    for k in range(args.steps):
-        ev = evs[k]
-        ev[0].record(stream)
-        lib = _lib.lib()
-        b_, r_ = x.parent.shape
-        lib.sdb_tree_build(_lib.ptr(x.parent), _lib.ptr(x.n_rows), _lib.ptr(x.ctx_len), b_, r_, o["mask"].shape[-1],
-                           _lib.ptr(o["mask"]), _lib.ptr(o["pos"]), _lib.ptr(o["depth"]), _lib.ptr(o["tree_err"]),
-                           _lib.stream_ptr())
-        ev[1].record(stream)
-        ver.attn(x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
-                 ver.scale, out=o["out"], lse=o["lse"], max_ctx=ver.max_ctx, num_splits=ver.num_splits,
-                 kernel=ver.kernel)
-        ev[2].record(stream)
-        acc = ver.greedy(x.logits, x.parent, x.n_rows, x.tokens)
-        ev[3].record(stream)
-        from paper_2508_08192_b200.kvstore import compact_kv
-
-        compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0), x.v_pool.unsqueeze(0),
-                   x.block_table, x.ctx_len, acc.path, acc.path_len)
-        ev[4].record(stream)
-    torch.cuda.synchronize()
-    parts = np.array([[ev[i].elapsed_time(ev[i + 1]) for i in range(n_ev - 1)] for ev in evs]).mean(axis=0)
-    t_attn_ms = float(parts[1])
+    parts = {}
+    if not accept_only:
+        parts["tree_build"] = graph_time(part_build, args.steps, stream, use_graph)
+        parts["tree_attn"] = graph_time(part_attn, args.steps, stream, use_graph)
+    parts["accept"] = graph_time(part_accept, args.steps, stream, use_graph)
+    if not accept_only:
+        parts["compact"] = graph_time(part_compact, args.steps, stream, use_graph)
+    acc = acc_box["acc"]
     accept_len = float(acc.path_len.float().mean().item())
 
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
     if not args.no_e2e:
-        pinned = {k: getattr(x, k).cpu().pin_memory() for k in ("q", "tree_k", "tree_v", "logits", "parent",
-                                                                   "n_rows", "ctx_len", "tokens")}
+        names = ["logits", "parent", "n_rows", "ctx_len", "tokens"]
+        if not accept_only:
+            names += ["q", "tree_k", "tree_v"]
+        if mode != "greedy":
+            names += ["draft_logits", "seeds", "steps"]
+        pinned = {k: getattr(x, k).cpu().pin_memory() for k in names}
         dev_in = {k: torch.empty_like(getattr(x, k)) for k in pinned}
         h2d = sum(v.numel() * v.element_size() for v in pinned.values())
-        out_h = torch.empty(o["out"].shape, dtype=o["out"].dtype).pin_memory()
-        lse_h = torch.empty(o["lse"].shape, dtype=o["lse"].dtype).pin_memory()
-        path_h = torch.empty(acc.path.shape, dtype=acc.path.dtype).pin_memory()
-        plen_h = torch.empty(acc.path_len.shape, dtype=acc.path_len.dtype).pin_memory()
-        nxt_h = torch.empty(acc.next_token.shape, dtype=acc.next_token.dtype).pin_memory()
-        d2h = sum(t_.numel() * t_.element_size() for t_ in (out_h, lse_h, path_h, plen_h, nxt_h))
+        host_out = {"path": acc.path, "path_len": acc.path_len, "next_token": acc.next_token}
+        if not accept_only:
+            host_out.update(out=o["out"], lse=o["lse"])
+        outs_h = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in host_out.items()}
+        d2h = sum(t_.numel() * t_.element_size() for t_ in outs_h.values())
         from paper_2508_08192_b200.verify import StepInputs
 
-        xe = StepInputs(**{**{k: dev_in[k] for k in pinned}, "k_pool": x.k_pool, "v_pool": x.v_pool,
-                           "block_table": x.block_table})
+        fields = {k: getattr(x, k) for k in StepInputs.__dataclass_fields__}
+        fields.update(dev_in)
+        xe = StepInputs(**fields)
 
         def e2e_step():
             for k_, v_ in pinned.items():
                 dev_in[k_].copy_(v_, non_blocking=True)
-            out_, lse_, acc_, _ = ver.step(xe)
-            out_h.copy_(out_, non_blocking=True)
-            lse_h.copy_(lse_, non_blocking=True)
-            path_h.copy_(acc_.path, non_blocking=True)
-            plen_h.copy_(acc_.path_len, non_blocking=True)
-            nxt_h.copy_(acc_.next_token, non_blocking=True)
+            if accept_only:
+                ver_acc = (ver.greedy(xe.logits, xe.parent, xe.n_rows, xe.tokens) if mode == "greedy" else
+                           ver.stochastic(xe.logits, xe.draft_logits, temperature, TOP_P, xe.parent, xe.n_rows,
+                                          xe.tokens, None, seeds=xe.seeds, steps=xe.steps))
+                res = {"path": ver_acc.path, "path_len": ver_acc.path_len, "next_token": ver_acc.next_token}
+            else:
+                out_, lse_, acc_, _ = ver.step(xe)
+                res = {"path": acc_.path, "path_len": acc_.path_len, "next_token": acc_.next_token, "out": out_,
+                       "lse": lse_}
+            for k_, v_ in res.items():
+                outs_h[k_].copy_(v_, non_blocking=True)
 
         for _ in range(2):
             e2e_step()
@@ -428,50 +539,62 @@ def main():
                "d2h_bytes_per_step": int(d2h)}
 
     attn_bytes, accept_bytes, attn_flops = step_bytes_flops(cfg, shard, R, anc_pairs)
+    if mode != "greedy":
+        # target rows + the draft rows that carry a q (parents), SURVEY 8(d)
+        accept_bytes = cfg["B"] * (R + n_parent_rows) * shard.n_vocab * 4
+    if accept_only:
+        attn_bytes, attn_flops = 0, 0.0
     tot = torch.tensor([attn_bytes + accept_bytes], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot)
     step_bytes_all = float(tot.item())
     hbm_peak, tc_peak, peak_src = _measured_peaks()
-    achieved_tf = attn_flops / (t_attn_ms * 1e-3) / 1e12
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
-            tr = json.load(f)
-        key = f"{args.config}:g{world}"
-        traffic = tr.get(key)
+            traffic = json.load(f).get(f"{args.config}:{mode}:g{world}")
     except Exception:
         pass
     gbs = step_bytes_all / (ms * 1e-3) / 1e9
-    launches_per_step = 1 + (2 if o is not None else 1) + 2 + 1
+    t_acc = parts["accept"]
+    accept_gbs = accept_bytes / (t_acc * 1e-3) / 1e9
+    if accept_only:
+        roof = {"kernel": "accept_" + mode, "bound": "hbm", "achieved": accept_gbs, "peak": hbm_peak,
+                "unit": "GB/s", "frac": accept_gbs / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": accept_bytes}
+    else:
+        t_attn_ms = parts["tree_attn"]
+        achieved_tf = attn_flops / (t_attn_ms * 1e-3) / 1e12
+        roof = {"kernel": "tree_attn", "bound": "tensor", "achieved": achieved_tf, "peak": tc_peak,
+                "unit": "TFLOP/s", "frac": achieved_tf / tc_peak, "traffic": traffic, "peak_source": peak_src,
+                "flops_per_launch": attn_flops, "hbm_gbs": attn_bytes / (t_attn_ms * 1e-3) / 1e9,
+                "accept_hbm_gbs": accept_gbs, "accept_hbm_frac": accept_gbs / hbm_peak}
+    # library kernels per step: tree_build 1, attention 2 (persistent kernel +
+    # LSE fix-up), acceptance 2 (greedy: keys + walk; stochastic: row stats +
+    # walk, + 1 Philox), compaction 1
+    n_launch = (0 if accept_only else 4) + (2 if mode == "greedy" else 3)
     line = {
         "metric": METRIC, "value": ms * 1e3, "unit": "us/step", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "vs_baseline": None, "dtype": "bf16" if not accept_only else "f32", "data": "synthetic",
         "config": {"workload": cfg["workload"], "global_batch": cfg["B"], "seq_len": cfg["ctx"], "tree_rows": R,
                    "heads": f"{cfg['Hq']}q/{cfg['Hkv']}kv d{cfg['d']}", "page": cfg["bs"], "vocab": cfg["V"],
-                   "parallelism": f"kv-head+vocab shard x{world}", "l2": "inputs 2.1 GB/GPU >> 126 MB L2",
-                   "graph": use_graph},
+                   "mode": mode, "parallelism": f"kv-head+vocab shard x{world}",
+                   "l2": f"inputs {(attn_bytes + accept_bytes) / 1e9:.1f} GB/GPU >> 126 MB L2", "graph": use_graph},
         "hbm_gbs": gbs, "pct_of_8tbs": 100.0 * gbs / 8000.0,
-        "kernels_ms": {"tree_build": float(parts[0]), "tree_attn": float(parts[1]), "accept": float(parts[2]),
-                       "compact": float(parts[3])},
+        "kernels_ms": parts,
         "mean_accepted": accept_len,
-        "roofline": {"kernel": "tree_attn", "bound": "tensor", "achieved": achieved_tf, "peak": tc_peak,
-                     "unit": "TFLOP/s", "frac": achieved_tf / tc_peak, "traffic": traffic,
-                     "peak_source": peak_src, "flops_per_launch": attn_flops,
-                     "hbm_gbs": attn_bytes / (t_attn_ms * 1e-3) / 1e9,
-                     "accept_hbm_frac": accept_bytes / (parts[2] * 1e-3) / 1e9 / hbm_peak},
+        "roofline": roof,
         "clocks": sampler.summary(),
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": n_launch * args.steps,
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ta, tacc, fa, facc = cpu_sample(cfg)
-        ta, tacc, fa, facc = cpu_sample(cfg, seed=1)
+        cpu_sample(cfg, mode=mode)
+        ta, tacc, fa, facc = cpu_sample(cfg, seed=1, mode=mode)
         us = (ta * fa + tacc * facc) * 1e6
         line["cpu_baseline"] = {"value": us, "unit": "us/step", "cores": blas_threads(), "kind": "port",
-                                "sample": f"1 seq x 1 KV group attention (x{fa}) + 1 seq greedy acceptance (x{facc}),"
-                                          " numpy float64 oracle port, extrapolated"}
+                                "sample": _sample_desc(cfg, mode, blas_threads())}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

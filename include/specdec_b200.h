@@ -161,6 +161,80 @@ int sdb_accept_stochastic(const float *target_logits, const float *draft_logits,
                           int64_t *next_token, int32_t *uniforms_used, float *residual,
                           int32_t *err, void *stream);
 
+/* ---- K4/K5 (sharded): vocab-sharded stochastic acceptance ----------------
+ * The T > 0 acceptance of sdb_accept_stochastic with the vocabulary split
+ * over `world` ranks; same reference semantics
+ * (sampling.py:87-202, engine.py:266-269, 405-407, 498-503).  The host runs
+ * the phases in order and performs, after the phases marked below, one
+ * collective on the named exchange buffer (identical on every rank):
+ *   SDB_SH_PARTIALS      -> all-gather xchg_partials into gathered [world][...]
+ *   SDB_SH_COMBINE
+ *   SDB_SH_NUCLEUS k=0..3 -> all-reduce SUM hist   (only when top_p < 1)
+ *   SDB_SH_CUT           -> all-reduce SUM tie     (only when top_p < 1)
+ *   SDB_SH_FINISH                                  (only when top_p < 1)
+ *   SDB_SH_TOKEN_PQ      -> all-reduce SUM pq
+ *   SDB_SH_RESIDUAL k=1..max_children -> all-reduce SUM chain_x (each)
+ *   SDB_SH_WALK          -> all-reduce SUM bonus_mass
+ *   SDB_SH_PICK          -> all-reduce MAX bonus_token (= next_token)
+ * path / path_len / uniforms_used are identical on every rank after WALK /
+ * PICK; residual (optional) receives this rank's vocab slice. */
+#define SDB_SH_PARTIALS 0
+#define SDB_SH_COMBINE 1
+#define SDB_SH_NUCLEUS 2
+#define SDB_SH_CUT 3
+#define SDB_SH_FINISH 4
+#define SDB_SH_TOKEN_PQ 5
+#define SDB_SH_RESIDUAL 6
+#define SDB_SH_WALK 7
+#define SDB_SH_PICK 8
+
+/* indices of sdb_sharded_accept_sizes' output (element counts; scratch in bytes) */
+#define SDB_SH_BUF_PARTIALS 0     /* f64 */
+#define SDB_SH_BUF_GATHERED 1     /* f64 */
+#define SDB_SH_BUF_HIST 2         /* f64 */
+#define SDB_SH_BUF_TIE 3          /* int32 */
+#define SDB_SH_BUF_PQ 4           /* f64 */
+#define SDB_SH_BUF_CHAIN_X 5      /* f64 */
+#define SDB_SH_BUF_BONUS_MASS 6   /* f64 */
+#define SDB_SH_BUF_BONUS_TOKEN 7  /* int64 */
+#define SDB_SH_BUF_SCRATCH 8      /* bytes */
+#define SDB_SH_N_BUFS 9
+
+typedef struct sdb_sharded_accept_args {
+  const float *target_logits; /* [B][r_max][vocab_local]: this rank's vocab slice */
+  const float *draft_logits;
+  int batch, r_max, vocab_local;
+  int64_t vocab_offset, vocab; /* slice start, global vocabulary size      */
+  int world, rank;
+  float temperature, top_p;
+  int max_children;            /* >= children of any node (residual levels) */
+  const int32_t *parent, *n_rows, *tokens; /* as sdb_accept_stochastic; tokens global ids */
+  const double *uniforms;      /* [B][n_uniforms], identical on every rank   */
+  int n_uniforms;
+  double *xchg_partials, *gathered, *hist;
+  int32_t *tie;
+  double *pq, *chain_x, *bonus_mass;
+  int64_t *bonus_token;
+  void *scratch;               /* private per-rank state                     */
+  int64_t scratch_bytes;
+  int32_t *path, *path_len, *uniforms_used;
+  float *residual;             /* optional [B][vocab_local]                  */
+  int32_t *err;
+} sdb_sharded_accept_args;
+
+int sdb_sharded_accept_sizes(const sdb_sharded_accept_args *a, int64_t *sizes /* [SDB_SH_N_BUFS] */);
+int sdb_sharded_accept_phase(const sdb_sharded_accept_args *a, int phase, int level, void *stream);
+
+/* ---- uniforms: device Philox4x64-10 ----------------------------------------
+ * Replaces rank_sliced_uniforms (sampling.py:112-124) as the engine consumes
+ * it (engine.py:251-254): out[b][i] = element (row, i) of the (padded_batch,
+ * width) matrix numpy's Generator(Philox(key=(seeds[b], steps[b]))).random()
+ * returns -- bit-identical.  seeds/steps int64 [B] (uint64 bit patterns), out
+ * f64 [B][width].  The engine uses row 0, seed = sampler.seed + seq, step =
+ * 2*round + 2 for acceptance (engine.py:234-235, 499). */
+int sdb_philox_uniforms(const int64_t *seeds, const int64_t *steps, int batch, int64_t row, int width,
+                        double *out, void *stream);
+
 /* ---- drop-in sampling ops (float64, reference precision) ---------------
  * target_dist (sampling.py:87-102): logits f64 [rows][vocab] -> dist f64,
  * allowed uint8 [rows][vocab] or NULL (guided-decoding mask, applied first). */

@@ -46,6 +46,32 @@ class TreeAttnArgs(ctypes.Structure):
     ]
 
 
+class ShardedAcceptArgs(ctypes.Structure):
+    """Mirror of ``sdb_sharded_accept_args``."""
+
+    _fields_ = [
+        ("target_logits", P), ("draft_logits", P),
+        ("batch", I32), ("r_max", I32), ("vocab_local", I32),
+        ("vocab_offset", I64), ("vocab", I64),
+        ("world", I32), ("rank", I32),
+        ("temperature", F32), ("top_p", F32),
+        ("max_children", I32),
+        ("parent", P), ("n_rows", P), ("tokens", P),
+        ("uniforms", P), ("n_uniforms", I32),
+        ("xchg_partials", P), ("gathered", P), ("hist", P),
+        ("tie", P),
+        ("pq", P), ("chain_x", P), ("bonus_mass", P),
+        ("bonus_token", P),
+        ("scratch", P), ("scratch_bytes", I64),
+        ("path", P), ("path_len", P), ("uniforms_used", P),
+        ("residual", P),
+        ("err", P),
+    ]
+
+
+SH_PARTIALS, SH_COMBINE, SH_NUCLEUS, SH_CUT, SH_FINISH, SH_TOKEN_PQ, SH_RESIDUAL, SH_WALK, SH_PICK = range(9)
+SH_N_BUFS = 9
+
 # name -> (restype, argtypes)
 _SIGNATURES = {
     "sdb_version": (I32, []),
@@ -62,6 +88,9 @@ _SIGNATURES = {
     "sdb_accept_stochastic_workspace": (I64, [I32, I32, I32]),
     "sdb_accept_stochastic": (I32, [P, P, I32, I32, I32, F32, F32, P, P, P, P, I32, P, I64, P, P, P, P, P,
                                     P, P]),
+    "sdb_sharded_accept_sizes": (I32, [ctypes.POINTER(ShardedAcceptArgs), ctypes.POINTER(I64)]),
+    "sdb_sharded_accept_phase": (I32, [ctypes.POINTER(ShardedAcceptArgs), I32, I32, P]),
+    "sdb_philox_uniforms": (I32, [P, P, I32, I64, I32, P, P]),
     "sdb_target_dist_f64": (I32, [P, P, I64, I32, F64, F64, P, P, P]),
     "sdb_mss_verify_f64": (I32, [P, P, I32, I32, P, P, P, I32, P, P, P, P, P]),
     "sdb_compact_kv": (I32, [P, P, P, P, I64, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, P]),

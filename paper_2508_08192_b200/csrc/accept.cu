@@ -20,60 +20,10 @@
 #include <float.h>
 #include <math.h>
 
-#include "sdb_common.cuh"
+#include "accept_common.cuh"
 
 namespace sdb {
 
-// ---------------------------------------------------------------------------
-// block reductions
-// ---------------------------------------------------------------------------
-template <int kThreads>
-__device__ __forceinline__ float block_max(float v, float *red) {
-  v = warp_max(v);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    v = lane < kThreads / 32 ? red[lane] : -INFINITY;
-    v = warp_max(v);
-    if (lane == 0) red[0] = v;
-  }
-  __syncthreads();
-  return red[0];
-}
-
-template <int kThreads>
-__device__ __forceinline__ double block_sum(double v, double *red) {
-  v = warp_sum(v);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    v = lane < kThreads / 32 ? red[lane] : 0.0;
-    v = warp_sum(v);
-    if (lane == 0) red[0] = v;
-  }
-  __syncthreads();
-  return red[0];
-}
-
-template <int kThreads>
-__device__ __forceinline__ long long block_max_i64(long long v, long long *red) {
-  v = warp_max_i64(v);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    v = lane < kThreads / 32 ? red[lane] : LLONG_MIN;
-    v = warp_max_i64(v);
-    if (lane == 0) red[0] = v;
-  }
-  __syncthreads();
-  return red[0];
-}
 
 // ---------------------------------------------------------------------------
 // greedy: packed argmax keys
@@ -268,22 +218,6 @@ constexpr float kHistScale = 16.0f;
 constexpr int kHistCopies = 16;        // warp-pair private histograms
 constexpr int kCandCap = 4096;         // exact-sort capacity around the cut
 
-struct RowStats {
-  float m2;        // max of logit * a (a = log2(e) / T)
-  float log2_z;    // log2 of the normaliser of kept mass (S, or Z for nucleus rows)
-  double s;        // sum of exp2(x2 - m2) over the row
-  double z;        // kept mass (== s when the whole row is kept)
-  uint32_t cut_key;
-  int32_t cut_idx;
-  int32_t keep_all;
-  int32_t valid;
-};
-
-__device__ __forceinline__ bool kept(const RowStats &st, float l, int idx) {
-  if (st.keep_all) return true;
-  uint32_t k = orderable_u32(l);
-  return k > st.cut_key || (k == st.cut_key && idx <= st.cut_idx);
-}
 
 __device__ __forceinline__ int hist_bin(float x2, float m2) {
   float d = (m2 - x2) * kHistScale;

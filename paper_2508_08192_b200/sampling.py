@@ -293,6 +293,28 @@ def greedy_walk(keys, parent, n_rows, tokens, stream=None):
     return AcceptResult(path, plen, nxt, used, None)
 
 
+def device_uniforms(seeds, steps, width, row=0, out=None, stream=None):
+    """Per-sequence uniform rows on the device, bit-identical to
+    ``rank_sliced_uniforms(seeds[b], steps[b], padded, width)[row]``
+    (sampling.py:112-124; the engine takes row 0, engine.py:251-254).
+
+    seeds/steps: int64 device tensors [B] (uint64 bit patterns).  Returns
+    float64 [B, width]."""
+    import torch
+
+    if seeds.dtype != torch.int64 or steps.dtype != torch.int64 or seeds.shape != steps.shape or seeds.dim() != 1:
+        raise SamplingError("seeds and steps must be int64 [B] device tensors")
+    if width < 0 or row < 0:
+        raise SamplingError("padded_batch must be >= 1 and row_width >= 0")
+    b = seeds.shape[0]
+    if out is None:
+        out = torch.empty((b, width), dtype=torch.float64, device=seeds.device)
+    rc = _lib.lib().sdb_philox_uniforms(_lib.ptr(seeds), _lib.ptr(steps), b, int(row), int(width), _lib.ptr(out),
+                                        _lib.stream_ptr(stream))
+    _lib.check(rc, "philox_uniforms")
+    return out
+
+
 class StochasticAcceptor:
     """T > 0 acceptance with a cached workspace (graph-capturable)."""
 
@@ -300,8 +322,8 @@ class StochasticAcceptor:
         self._ws = None
         self._bufs = None
 
-    def __call__(self, target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms,
-                 want_residual=False, stream=None):
+    def __call__(self, target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms=None,
+                 want_residual=False, stream=None, seeds=None, steps=None):
         import torch
 
         b, r, v = target_logits.shape
@@ -325,6 +347,14 @@ class StochasticAcceptor:
                 residual=torch.empty((b, v), dtype=torch.float32, device=dev) if want_residual else None))
         o = self._bufs[1]
         o["err"].zero_()
+        if uniforms is None:
+            # (seeds, steps) on the device: the Philox rows are generated in
+            # a launch on the same stream (no host transfer of uniforms)
+            if seeds is None or steps is None:
+                raise SamplingError("pass uniforms, or seeds and steps")
+            if "uni" not in o or o["uni"].shape != (b, r):
+                o["uni"] = torch.empty((b, r), dtype=torch.float64, device=dev)
+            uniforms = device_uniforms(seeds, steps, r, out=o["uni"], stream=stream)
         rc = lib.sdb_accept_stochastic(_lib.ptr(target_logits), _lib.ptr(draft_logits), b, r, v, float(temperature),
                                        float(top_p), _lib.ptr(parent), _lib.ptr(n_rows), _lib.ptr(tokens),
                                        _lib.ptr(uniforms), uniforms.shape[1], _lib.ptr(self._ws), self._ws.numel(),
@@ -335,10 +365,12 @@ class StochasticAcceptor:
         return AcceptResult(o["path"], o["path_len"], o["next_token"], o["used"], o["err"], o["residual"])
 
 
-def accept_stochastic(target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms,
-                      want_residual=False, stream=None):
+def accept_stochastic(target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms=None,
+                      want_residual=False, stream=None, seeds=None, steps=None):
     """Batched T > 0 acceptance (target_dist for every row, draft q per parent
     row, MSS walk).  uniforms float64 [B, n_uniforms] (the reference's
-    rank_sliced_uniforms row per sequence)."""
+    rank_sliced_uniforms row per sequence), or ``uniforms=None`` with int64
+    ``seeds``/``steps`` [B] to draw row 0 of the reference's Philox matrix on
+    the device (engine.py:251-254)."""
     return StochasticAcceptor()(target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms,
-                                want_residual, stream)
+                                want_residual, stream, seeds, steps)

@@ -38,6 +38,8 @@ class StepInputs:
     block_table: "object"  # int32 [B, max_blocks]
     draft_logits: "object" = None  # [B, R, V] for stochastic acceptance
     uniforms: "object" = None      # float64 [B, n_uniforms]
+    seeds: "object" = None         # int64 [B] Philox keys (uniforms=None: drawn on the device)
+    steps: "object" = None         # int64 [B]
 
 
 class TreeVerifier:
@@ -86,7 +88,7 @@ class TreeVerifier:
             acc = self.greedy(x.logits, x.parent, x.n_rows, x.tokens, stream=stream)
         else:
             acc = self.stochastic(x.logits, x.draft_logits, self.temperature, self.top_p, x.parent, x.n_rows,
-                                  x.tokens, x.uniforms, stream=stream)
+                                  x.tokens, x.uniforms, stream=stream, seeds=x.seeds, steps=x.steps)
         if compact:
             compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0), x.v_pool.unsqueeze(0),
                        x.block_table, x.ctx_len, acc.path, acc.path_len, None, stream=stream)

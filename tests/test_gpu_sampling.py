@@ -1,0 +1,260 @@
+"""GPU parity of the sampling side of the path: the device Philox stream vs
+the reference's rank_sliced_uniforms, and stochastic (T > 0) acceptance at the
+full Llama-3 vocabulary vs the CPU oracle (target_dist + mss_verify in
+float64).  Needs a B200."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import specdec_oracle as O  # noqa: E402
+
+TREE64 = [-1, -1, -1, -1, -1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5, 5, 6, 7,
+          8, 8, 8, 8, 9, 9, 9, 10, 10, 10, 11, 11, 12, 13, 14, 15, 32, 32, 32, 33, 33, 34, 34, 35, 36, 37, 48, 48, 49,
+          50, 51]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib_loaded():
+    from paper_2508_08192_b200 import _lib
+
+    _lib.load()
+
+
+def _i64(vals):
+    # uint64 bit patterns as int64
+    return torch.tensor(np.array(vals, dtype=np.uint64).view(np.int64), device="cuda")
+
+
+def test_device_philox_matches_reference_golden(golden):
+    from paper_2508_08192_b200.sampling import device_uniforms
+
+    g = golden("philox")
+    for i in range(int(g["n"])):
+        seed, step, b, w = (int(x) for x in g[f"p{i}_spec"])
+        want = g[f"p{i}_u"]
+        for row in range(b):
+            got = device_uniforms(_i64([seed]), _i64([step]), w, row=row).cpu().numpy()[0]
+            np.testing.assert_array_equal(got, want[row])
+    got = device_uniforms(_i64([0]), _i64([0]), 5).cpu().numpy()
+    assert got[0, 0] == 0.011546754286331562
+
+
+def test_device_philox_batch_of_sessions_vs_oracle():
+    """One launch for a batch of sessions at different (seed, step); large
+    uint64 seeds; widths that are not multiples of 4; rows > 0."""
+    from paper_2508_08192_b200.sampling import device_uniforms
+
+    rng = np.random.default_rng(5)
+    seeds = [int(x) for x in rng.integers(0, 2**63, size=6, dtype=np.int64)] + [2**64 - 1, 0]
+    steps = [2 * int(r) + 2 for r in rng.integers(0, 1000, size=8)]
+    for width, row in ((65, 0), (64, 0), (7, 3), (1, 11), (130, 2)):
+        got = device_uniforms(_i64(seeds), _i64(steps), width, row=row).cpu().numpy()
+        for b in range(len(seeds)):
+            want = O.rank_sliced_uniforms(seeds[b], steps[b], row + 1, width)[row]
+            np.testing.assert_array_equal(got[b], want)
+
+
+def _stochastic_case(B, V, tree, temperature, top_p, seed):
+    """Synthetic inputs of SURVEY 8(d): target N(0, 2^2), draft = target +
+    N(0, 0.5^2), node tokens sampled from the parent's draft q (stochastic
+    drafting, engine.py:393-394), uniforms from the reference Philox."""
+    rng = np.random.default_rng(seed)
+    aug = O.augment(tuple(tree))
+    R = len(aug)
+    tl = (2.0 * rng.normal(size=(B, R, V))).astype(np.float32)
+    dl = (tl + 0.5 * rng.normal(size=(B, R, V))).astype(np.float32)
+    tokens = np.zeros((B, R), dtype=np.int32)
+    for b in range(B):
+        for i in range(1, R):
+            q = O.target_dist(dl[b, aug[i]].astype(np.float64), temperature, 1.0)
+            tokens[b, i] = int(O.sample_from(q, rng.random()))
+    seeds = [1234 + b for b in range(B)]
+    steps = [2 * (b + 3) + 2 for b in range(B)]
+    return aug, tl, dl, tokens, seeds, steps
+
+
+def _oracle_accept(aug, tl, dl, tokens, uniforms, temperature, top_p):
+    parent = tuple(p - 1 if p > 0 else -1 for p in aug[1:])
+    tdists = [O.target_dist(tl[r].astype(np.float64), temperature, top_p) for r in range(len(aug))]
+    qcache = {}
+    ndists = []
+    for i, p in enumerate(aug[1:], 1):
+        if p not in qcache:
+            qcache[p] = O.target_dist(dl[p].astype(np.float64), temperature, 1.0)
+        ndists.append(qcache[p])
+    return O.mss_verify(parent, tokens[1:], ndists, tdists, uniforms)
+
+
+@pytest.mark.parametrize("top_p", [0.9, 1.0])
+def test_accept_stochastic_full_vocab_vs_oracle(top_p):
+    """Llama-3 vocabulary (128,256), the 64-row EAGLE tree, uniforms drawn on
+    the device from (seed, step): path, next token and uniforms_used must
+    equal the float64 oracle's."""
+    from paper_2508_08192_b200.sampling import accept_stochastic
+
+    B, V, T = 3, 128256, 1.0
+    aug, tl, dl, tokens, seeds, steps = _stochastic_case(B, V, TREE64, T, top_p, seed=11)
+    R = len(aug)
+    par = torch.tensor([aug] * B, dtype=torch.int32, device="cuda")
+    res = accept_stochastic(torch.tensor(tl, device="cuda"), torch.tensor(dl, device="cuda"), T, top_p, par,
+                            torch.full((B,), R, dtype=torch.int32, device="cuda"),
+                            torch.tensor(tokens, device="cuda"), seeds=_i64(seeds), steps=_i64(steps))
+    torch.cuda.synchronize()
+    assert int(res.err[0]) == 0
+    for b in range(B):
+        uni = O.rank_sliced_uniforms(seeds[b], steps[b], 1, R)[0]
+        path, nxt, _res, used = _oracle_accept(aug, tl[b], dl[b], tokens[b], uni, T, top_p)
+        plen = int(res.path_len[b])
+        assert res.path[b, :plen].cpu().tolist() == list(path), b
+        assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used, b
+
+
+# ---------------------------------------------------------------------------
+# vocab-sharded stochastic acceptance: every rank's kernels run
+# in this process (VirtualComm); the protocol is the one torch.distributed runs
+# ---------------------------------------------------------------------------
+
+def _dev(x, dt):
+    return torch.as_tensor(np.ascontiguousarray(x)).to(device="cuda", dtype=dt)
+
+
+def test_sharded_stochastic_matches_reference_golden(golden):
+    """Reference golden MSS cases (V = 2048, several temperatures / top-p),
+    vocab split over 2, 3 and 8 ranks: every rank reports the reference's
+    path, bonus token and uniforms_used; residual slices tile the reference
+    residual."""
+    from paper_2508_08192_b200.sharding import run_virtual_sharded_stochastic
+
+    g = golden("accept_stochastic")
+    from test_gpu_parity import _aug_batch
+
+    for world in (2, 3, 8):
+        for k in range(int(g["n_cases"])):
+            p = f"s{k}_"
+            temp, top_p, _seed = g[p + "meta"]
+            logits, dl = g[p + "logits"], g[p + "draft_logits"]
+            n = logits.shape[0]
+            par, tok, nr = _aug_batch([g[p + "parent"]], [g[p + "tokens"]], n)
+            res = run_virtual_sharded_stochastic(_dev(logits[None], torch.float32), _dev(dl[None], torch.float32),
+                                                 float(temp), float(top_p), _dev(par, torch.int32),
+                                                 _dev(nr, torch.int32), _dev(tok, torch.int32),
+                                                 _dev(g[p + "uniforms"][None], torch.float64), world,
+                                                 want_residual=True)
+            torch.cuda.synchronize()
+            want = (list(g[p + "path"]), int(g[p + "next"]), int(g[p + "used"]))
+            for rk, rr in enumerate(res):
+                assert int(rr.err[0]) == 0
+                plen = int(rr.path_len[0])
+                got = (rr.path[0, :plen].cpu().tolist(), int(rr.next_token[0]), int(rr.uniforms_used[0]))
+                assert got == want, (world, k, rk, got, want)
+            resid = np.concatenate([rr.residual[0].cpu().numpy() for rr in res])
+            np.testing.assert_allclose(resid, g[p + "residual"], atol=2e-6)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_stochastic_full_vocab_vs_oracle(world):
+    """128,256-entry vocabulary split over `world` ranks, the 64-row tree,
+    T = 1, top-p 0.9, device Philox uniforms: same path / next / used as the
+    float64 oracle and as the unsharded kernel."""
+    from paper_2508_08192_b200.sampling import accept_stochastic, device_uniforms
+    from paper_2508_08192_b200.sharding import run_virtual_sharded_stochastic
+
+    B, V, T, top_p = 3, 128256, 1.0, 0.9
+    aug, tl, dl, tokens, seeds, steps = _stochastic_case(B, V, TREE64, T, top_p, seed=23)
+    R = len(aug)
+    par = torch.tensor([aug] * B, dtype=torch.int32, device="cuda")
+    nr = torch.full((B,), R, dtype=torch.int32, device="cuda")
+    tl_d, dl_d, tok_d = torch.tensor(tl, device="cuda"), torch.tensor(dl, device="cuda"), torch.tensor(tokens,
+                                                                                                         device="cuda")
+    uni = device_uniforms(_i64(seeds), _i64(steps), R)
+    res = run_virtual_sharded_stochastic(tl_d, dl_d, T, top_p, par, nr, tok_d, uni, world)
+    ref = accept_stochastic(tl_d, dl_d, T, top_p, par, nr, tok_d, uni)
+    torch.cuda.synchronize()
+    for b in range(B):
+        path, nxt, _res, used = _oracle_accept(aug, tl[b], dl[b], tokens[b], uni[b].cpu().numpy(), T, top_p)
+        for rr in res + [ref]:
+            assert int(rr.err[0]) == 0
+            plen = int(rr.path_len[b])
+            assert rr.path[b, :plen].cpu().tolist() == list(path), b
+            assert int(rr.next_token[b]) == nxt and int(rr.uniforms_used[b]) == used, b
+
+
+def test_sharded_stochastic_nan_flags_every_rank():
+    from paper_2508_08192_b200.sharding import run_virtual_sharded_stochastic
+
+    aug = O.augment((-1, -1, 0))
+    R, V = len(aug), 300
+    rng = np.random.default_rng(1)
+    tl = rng.normal(size=(1, R, V)).astype(np.float32)
+    tl[0, 1, 250] = np.nan  # lives on the last of 2 ranks
+    res = run_virtual_sharded_stochastic(_dev(tl, torch.float32), _dev(tl, torch.float32), 1.0, 0.9,
+                                         _dev(np.array([aug]), torch.int32), _dev(np.array([R]), torch.int32),
+                                         _dev(np.array([[0, 1, 2, 3]]), torch.int32),
+                                         _dev(rng.random((1, R)), torch.float64), 2)
+    torch.cuda.synchronize()
+    for rr in res:
+        assert int(rr.err[0]) & 2
+        assert int(rr.path_len[0]) == 0
+
+
+def _gloo_rank(rank, world, port, case, q):
+    import os
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2508_08192_b200 import _lib
+    from paper_2508_08192_b200.sharding import ShardedStochasticAcceptor, shard_for
+
+    _lib.load()
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        aug, tl, dl, tokens, seeds, steps, T, top_p = case
+        B, R, V = tl.shape
+        sh = shard_for(rank, world, world, world, V)
+        acc = ShardedStochasticAcceptor(sh)
+        res = acc(_dev(tl[:, :, sh.v_lo:sh.v_hi], torch.float32), _dev(dl[:, :, sh.v_lo:sh.v_hi], torch.float32), T,
+                  top_p, _dev(np.array([aug] * B), torch.int32), _dev(np.full(B, R), torch.int32),
+                  _dev(tokens, torch.int32), seeds=_i64(seeds), steps=_i64(steps))
+        torch.cuda.synchronize()
+        q.put((rank, int(res.err[0]), res.path.cpu().numpy(), res.path_len.cpu().numpy(),
+               res.next_token.cpu().numpy(), res.uniforms_used.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_stochastic_two_processes_gloo():
+    """The real torch.distributed protocol (two processes sharing cuda:0 over
+    gloo; NCCL runs the same calls on a multi-GPU box) vs the oracle."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    B, V, T, top_p = 2, 4099, 0.8, 0.95
+    case = _stochastic_case(B, V, TREE64, T, top_p, seed=31) + (T, top_p)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_rank, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    aug, tl, dl, tokens, seeds, steps = case[:6]
+    R = len(aug)
+    for rank, err, path, plen, nxt, used in out:
+        assert err == 0
+        for b in range(B):
+            uni = O.rank_sliced_uniforms(seeds[b], steps[b], 1, R)[0]
+            want = _oracle_accept(aug, tl[b], dl[b], tokens[b], uni, T, top_p)
+            assert list(path[b, :plen[b]]) == list(want[0]) and nxt[b] == want[1] and used[b] == want[3], (rank, b)

@@ -20,7 +20,11 @@
 #include <float.h>
 #include <math.h>
 
+#include <cooperative_groups.h>
+
 #include "accept_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sdb {
 
@@ -212,16 +216,29 @@ __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int
 // ---------------------------------------------------------------------------
 // stochastic
 // ---------------------------------------------------------------------------
-constexpr int kStThreads = 1024;
-constexpr int kHistBins = 1024;        // width 1/16 log2 unit below the row max
-constexpr float kHistScale = 16.0f;
-constexpr int kHistCopies = 16;        // warp-pair private histograms
-constexpr int kCandCap = 4096;         // exact-sort capacity around the cut
-
+constexpr int kStThreads = 1024;       // one row per SM: its L2-resident working set (148 x 0.5 MB) fits the 126 MB L2
+constexpr int kHistBins = 4096;        // width 1/64 log2 unit below the row max (64 log2 units)
+constexpr float kHistScale = 64.0f;
+constexpr int kHistCopies = 2;         // fixed-point histograms (warp-parity private copies)
+constexpr int kBinsPerThread = kHistBins / kStThreads;
+constexpr int kRefBins = kStThreads;   // key-space refinement bins (fallback)
+constexpr int kCandCap = 4 * kStThreads;  // exact-sort capacity around the cut
+// Bin b holds weights w in (2^-(b+1)/64, 2^-b/64]; it accumulates r = w *
+// 2^(b/64) in (0.989, 1] as round(r * 2^14) in a native 32-bit shared atomic
+// (float / 64-bit shared atomics are CAS loops).  |rounding| <= 2^-15 per
+// element, i.e. a bin mass is exact to 3.1e-5 relative -- only used to pick
+// the window; the mass above it is summed exactly in f64 afterwards.
+constexpr float kFixScale = 16384.0f;
+constexpr double kBinTol = 1e-4;
 
 __device__ __forceinline__ int hist_bin(float x2, float m2) {
   float d = (m2 - x2) * kHistScale;
   return d >= (float)(kHistBins - 1) ? kHistBins - 1 : (int)d;
+}
+
+__device__ __forceinline__ float key_weight(uint32_t k, float a, float m2) {
+  const uint32_t bits = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return exp2f(__uint_as_float(bits) * a - m2);
 }
 
 // Inclusive block scan of one double per thread (kStThreads threads).
@@ -251,17 +268,119 @@ __device__ double block_inclusive_scan(double v, double *red) {
 }
 
 struct StSmem {
-  float hist[kHistCopies][kHistBins];
-  unsigned long long cand[kCandCap];
+  uint32_t hist[kHistCopies][kHistBins];  // pass-2 masses (fixed point, window selection only)
+  unsigned long long cand[kCandCap];   // (key << 32) | ~index
+  double rh[kRefBins];                 // fallback key-space refinement (f64)
   double red[32];
   float redf[32];
-  double cum[kHistBins];
   int count;
-  int pad[3];
+  int lo, hi, cut;
+  unsigned klo, khi;
+  int idx;
+  double tot;
 };
 
+// Streaming max (+ NaN flag) of a row: 4 independent 16-byte loads in flight
+// per thread.
+__device__ __forceinline__ void row_max_nan(const float *row, int vocab, bool vec, float &mx, bool &nan) {
+  mx = -INFINITY;
+  nan = false;
+  if (vec) {
+    const float4 *r4 = reinterpret_cast<const float4 *>(row);
+    const int n4 = vocab >> 2;
+    int i = threadIdx.x;
+    for (; i + 3 * kStThreads < n4; i += 4 * kStThreads) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(r4 + i + u * kStThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        nan |= (v[u].x != v[u].x) | (v[u].y != v[u].y) | (v[u].z != v[u].z) | (v[u].w != v[u].w);
+        mx = fmaxf(mx, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+      }
+    }
+    for (; i < n4; i += kStThreads) {
+      const float4 v = __ldg(r4 + i);
+      nan |= (v.x != v.x) | (v.y != v.y) | (v.z != v.z) | (v.w != v.w);
+      mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    }
+    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) {
+      const float v = row[j];
+      nan |= v != v;
+      mx = fmaxf(mx, v);
+    }
+  } else {
+    for (int j = threadIdx.x; j < vocab; j += kStThreads) {
+      const float v = row[j];
+      nan |= v != v;
+      mx = fmaxf(mx, v);
+    }
+  }
+}
+
+// Exact cut among `count` (<= kCandCap) candidates in sm.cand whose mass
+// above is mass_above: sort by (key desc, index asc), first position whose
+// cumulative mass reaches tau.  Returns the kept mass; sets cut key / index.
+__device__ double exact_cut(StSmem &sm, int count, double mass_above, double tau, float a, float m2,
+                            uint32_t &cut_key, int &cut_idx) {
+  int np2 = 1;
+  while (np2 < count) np2 <<= 1;
+  for (int i = count + threadIdx.x; i < np2; i += kStThreads) sm.cand[i] = 0ull;
+  __syncthreads();
+  for (int size = 2; size <= np2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < np2; i += kStThreads) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = (i & size) == 0;
+          const unsigned long long x = sm.cand[i], y = sm.cand[j];
+          if (desc ? (x < y) : (x > y)) {
+            sm.cand[i] = y;
+            sm.cand[j] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // per-thread chunk of 4 consecutive sorted candidates
+  constexpr int kPer = kCandCap / kStThreads;
+  double loc[kPer], wv[kPer];
+  double tot = 0.0;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = threadIdx.x * kPer + u;
+    wv[u] = i < count ? (double)key_weight((uint32_t)(sm.cand[i] >> 32), a, m2) : 0.0;
+    tot += wv[u];
+    loc[u] = tot;
+  }
+  const double incl = block_inclusive_scan(tot, sm.red);
+  const double base = mass_above + incl - tot;
+  if (threadIdx.x == 0) sm.cut = count - 1;
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = threadIdx.x * kPer + u;
+    if (i < count && base + loc[u] >= tau) atomicMin(&sm.cut, i);
+  }
+  __syncthreads();
+  const int cpos = sm.cut;
+  double zz = 0.0;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u)
+    if (threadIdx.x * kPer + u <= cpos) zz += wv[u];
+  const double z = mass_above + block_sum<kStThreads>(zz, sm.red);
+  cut_key = (uint32_t)(sm.cand[cpos] >> 32);
+  cut_idx = (int)(0xffffffffu - (uint32_t)(sm.cand[cpos] & 0xffffffffu));
+  return z;
+}
+
 // Phase A.  grid (r_max, batch, 2): z = 0 target rows (nucleus), z = 1 draft
-// rows that have children (full softmax).
+// rows that have children (full softmax).  One HBM pass (max); then, from
+// L2, the normaliser with a 1/64-log2-unit mass histogram (nucleus rows) and
+// one pass that sums the exact (f64) mass above the bins straddling the cut
+// and collects their few elements, which are sorted exactly by (key desc,
+// index asc) -- the reference's top_p_mask order (sampling.py:57-72).
 __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
     float top_p, const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows,
@@ -287,48 +406,56 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   }
   const float *row = (is_draft ? draft : target) + ((int64_t)b * r_max + r) * vocab;
   const bool vec = (vocab & 3) == 0 && ((uintptr_t)row & 15) == 0;
-  // pass 1: max + NaN
-  float mx = -INFINITY;
-  bool nan = false;
-  if (vec) {
-    const float4 *r4 = reinterpret_cast<const float4 *>(row);
-    for (int i = threadIdx.x; i < (vocab >> 2); i += kStThreads) {
-      float4 v = r4[i];
-      nan |= (v.x != v.x) | (v.y != v.y) | (v.z != v.z) | (v.w != v.w);
-      mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-    }
-  } else {
-    for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-      float v = row[i];
-      nan |= v != v;
-      mx = fmaxf(mx, v);
-    }
-  }
-  if (__syncthreads_or(nan)) {
-    if (threadIdx.x == 0) {
-      atomicOr(err, SDB_ERR_NAN);
-      out->valid = 0;
-    }
-    return;
-  }
-  mx = block_max<kStThreads>(mx, sm.redf);
-  const float m2 = mx * a;
   const bool nucleus = !is_draft && top_p < 1.0f;
-  // pass 2: normaliser (+ value histogram for nucleus rows)
-  if (nucleus) {
-    for (int i = threadIdx.x; i < kHistCopies * kHistBins; i += kStThreads) (&sm.hist[0][0])[i] = 0.f;
-    __syncthreads();
+  // the whole row streams into L2 through the TMA engine (deep memory-level
+  // parallelism); the passes below then hit L2
+  if (vec && threadIdx.x == 0) {
+    constexpr uint32_t kChunk = 64u << 10;
+    const uint32_t bytes = (uint32_t)vocab * 4u;
+    for (uint32_t o = 0; o < bytes; o += kChunk) prefetch_l2((const char *)row + o, min(kChunk, bytes - o));
   }
-  float *hist = sm.hist[(threadIdx.x >> 6) % kHistCopies];
-  float s_loc = 0.f;
-  for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-    float x2 = row[i] * a;
-    float w = exp2f(x2 - m2);
-    s_loc += w;
-    if (nucleus) atomicAdd(&hist[hist_bin(x2, m2)], w);
-  }
-  const double s = block_sum<kStThreads>((double)s_loc, sm.red);
+  const int n4 = vec ? vocab >> 2 : 0;
+  const float4 *r4 = reinterpret_cast<const float4 *>(row);
+  constexpr int kU = 4;  // 16-byte loads in flight per thread
   if (!nucleus) {
+    // one pass: online max + normaliser (+ NaN)
+    float m = -INFINITY, sacc = 0.f;
+    bool nan = false;
+    auto one = [&](float x) {
+      nan |= x != x;
+      const float x2 = x * a;
+      if (x2 > m) {
+        sacc *= exp2f(m - x2);
+        m = x2;
+      }
+      sacc += exp2f(x2 - m);
+    };
+    for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kStThreads + threadIdx.x;
+        v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        one(v[u].x);
+        one(v[u].y);
+        one(v[u].z);
+        one(v[u].w);
+      }
+    }
+    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) one(row[j]);
+    if (__syncthreads_or(nan)) {
+      if (threadIdx.x == 0) {
+        atomicOr(err, SDB_ERR_NAN);
+        out->valid = 0;
+      }
+      return;
+    }
+    const float m2 = block_max<kStThreads>(m, sm.redf);
+    const double s = block_sum<kStThreads>(m > -INFINITY ? (double)sacc * exp2((double)m - (double)m2) : 0.0,
+                                           sm.red);
     if (threadIdx.x == 0) {
       RowStats st;
       st.m2 = m2;
@@ -343,214 +470,255 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     }
     return;
   }
-  // cumulative mass by bin (bin 0 = largest values)
-  for (int bb = threadIdx.x; bb < kHistBins; bb += kStThreads) {
-    float t = 0.f;
-#pragma unroll
-    for (int c = 0; c < kHistCopies; ++c) t += sm.hist[c][bb];
-    sm.cum[bb] = t;
-  }
-  __syncthreads();
-  double cv = block_inclusive_scan(threadIdx.x < kHistBins ? sm.cum[threadIdx.x] : 0.0, sm.red);
-  if (threadIdx.x < kHistBins) sm.cum[threadIdx.x] = cv;  // inclusive
-  __syncthreads();
-  const double tau = ((double)top_p - 1e-12) * s;
-  // window of bins whose inclusive cumulative could straddle tau given fp32
-  // bin sums (relative error << 1e-5)
-  int lo = kHistBins - 1, hi = kHistBins - 1;
-  {
-    // first bin with cum >= threshold: parallel min over bins
-    __shared__ int s_lo, s_hi;
+  for (int i = threadIdx.x; i < kHistCopies * kHistBins; i += kStThreads) (&sm.hist[0][0])[i] = 0u;
+  // pass 1: max + NaN
+  float mx;
+  bool nan;
+  row_max_nan(row, vocab, vec, mx, nan);
+  if (__syncthreads_or(nan)) {
     if (threadIdx.x == 0) {
-      s_lo = kHistBins - 1;
-      s_hi = kHistBins - 1;
+      atomicOr(err, SDB_ERR_NAN);
+      out->valid = 0;
     }
-    __syncthreads();
-    for (int bb = threadIdx.x; bb < kHistBins; bb += kStThreads) {
-      if (sm.cum[bb] >= tau * (1.0 - 1e-5)) atomicMin(&s_lo, bb);
-      if (sm.cum[bb] >= tau * (1.0 + 1e-5)) atomicMin(&s_hi, bb);
-    }
-    __syncthreads();
-    lo = s_lo;
-    hi = max(s_hi, lo);
+    return;
   }
-  double mass_above = lo > 0 ? sm.cum[lo - 1] : 0.0;
-  // pass 3+: collect the window [key range]; refine in key space until the
-  // candidates fit the exact-sort buffer or only ties remain.
-  uint32_t klo = 0xffffffffu, khi = 0u;
+  mx = block_max<kStThreads>(mx, sm.redf);
+  const float m2 = mx * a;
+  // pass 2 (L2): normaliser + mass histogram
+  uint32_t *hist = sm.hist[(threadIdx.x >> 5) & (kHistCopies - 1)];
+  float s_loc = 0.f;
+  auto acc2 = [&](float l) {
+    const float x2 = l * a;
+    s_loc += exp2f(x2 - m2);
+    // d = (m2 - x2) * 64: bin = floor(d), r = 2^-(d - bin)/64 by a quadratic
+    // (error < 2e-7), no MUFU
+    const float d = (m2 - x2) * kHistScale;
+    if (d < (float)(kHistBins - 1)) {
+      const int bin = (int)d;
+      const float t = (d - (float)bin) * (0.6931471805599453f / kHistScale);
+      const float rr = fmaf(t, fmaf(t, 0.5f, -1.0f), 1.0f);
+      atomicAdd(&hist[bin], (uint32_t)__float2int_rn(rr * kFixScale));
+    }
+  };
+  for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
+    float4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * kStThreads + threadIdx.x;
+      v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      acc2(v[u].x);
+      acc2(v[u].y);
+      acc2(v[u].z);
+      acc2(v[u].w);
+    }
+  }
+  for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) acc2(row[j]);
+  const double s = block_sum<kStThreads>((double)s_loc, sm.red);
+  const double tau = ((double)top_p - 1e-12) * s;
+  // window [lo, hi] of bins whose cumulative (bin 0 = largest values) may
+  // straddle tau given the f32 bin sums
   {
-    uint32_t kl = 0xffffffffu, kh = 0u;
-    for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-      float l = row[i];
-      int bin = hist_bin(l * a, m2);
-      if (bin >= lo && bin <= hi) {
-        uint32_t k = orderable_u32(l);
+    double loc[kBinsPerThread];
+    double tsum = 0.0;
+#pragma unroll
+    for (int u = 0; u < kBinsPerThread; ++u) {
+      const int bb = threadIdx.x * kBinsPerThread + u;
+      unsigned long long q = 0;
+#pragma unroll
+      for (int c = 0; c < kHistCopies; ++c) q += sm.hist[c][bb];
+      // mass = 2^(-bb/64) * q / 2^14
+      tsum += (double)q * (double)exp2f(-(float)bb * (1.0f / kHistScale)) * (1.0 / kFixScale);
+      loc[u] = tsum;
+    }
+    if (threadIdx.x == 0) {
+      sm.lo = kHistBins - 1;
+      sm.hi = kHistBins - 1;
+      sm.count = 0;
+      sm.klo = 0xffffffffu;
+      sm.khi = 0u;
+    }
+    const double excl = block_inclusive_scan(tsum, sm.red) - tsum;
+    int mlo = kHistBins - 1, mhi = kHistBins - 1;
+#pragma unroll
+    for (int u = kBinsPerThread - 1; u >= 0; --u) {
+      const double cv = excl + loc[u];
+      if (cv >= tau * (1.0 - kBinTol)) mlo = threadIdx.x * kBinsPerThread + u;
+      if (cv >= tau * (1.0 + kBinTol)) mhi = threadIdx.x * kBinsPerThread + u;
+    }
+    atomicMin(&sm.lo, mlo);
+    atomicMin(&sm.hi, mhi);
+    __syncthreads();
+  }
+  const int lo = sm.lo, hi = max(sm.hi, sm.lo);
+  // pass 3 (L2): exact f64 mass above the window; collect the window's
+  // elements (warp-aggregated slots) and their key range
+  double above = 0.0;
+  {
+    unsigned kl = 0xffffffffu, kh = 0u;
+    const int lane = threadIdx.x & 31;
+    auto flush = [&](const float *x, const int *idx, int cnt) {
+      // cnt candidates of this thread among x[0..]: warp prefix -> slots
+      if (!__any_sync(SDB_FULL_MASK, cnt > 0)) return;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(SDB_FULL_MASK, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int base = 0;
+      if (lane == 31) base = atomicAdd(&sm.count, incl);
+      base = __shfl_sync(SDB_FULL_MASK, base, 31) + incl - cnt;
+      for (int q = 0; q < cnt; ++q) {
+        const uint32_t k = orderable_u32(x[q]);
+        if (base + q < kCandCap) sm.cand[base + q] = ((unsigned long long)k << 32) | (0xffffffffu - (uint32_t)idx[q]);
         kl = min(kl, k);
         kh = max(kh, k);
       }
+    };
+    for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kStThreads + threadIdx.x;
+        v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+      float cx[4 * kU];
+      int ci[4 * kU];
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int base_idx = 4 * (i0 + u * kStThreads + threadIdx.x);
+        const float xs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float x2 = xs[e] * a;
+          const int bin = hist_bin(x2, m2);
+          if (bin < lo) above += (double)exp2f(x2 - m2);
+          if (bin >= lo && bin <= hi && base_idx + e < vocab) {
+            cx[cnt] = xs[e];
+            ci[cnt] = base_idx + e;
+            ++cnt;
+          }
+        }
+      }
+      flush(cx, ci, cnt);
     }
-    // block min/max through the float reducer reinterpreted as unsigned
-    __shared__ unsigned s_kl, s_kh;
-    if (threadIdx.x == 0) {
-      s_kl = 0xffffffffu;
-      s_kh = 0u;
+    // scalar tail (and the non-vector path): one element per thread per step
+    const int t0 = n4 << 2;
+    for (int j0 = t0; j0 < vocab; j0 += kStThreads) {
+      const int j = j0 + threadIdx.x;
+      float x = 0.f;
+      int cnt = 0;
+      if (j < vocab) {
+        x = row[j];
+        const float x2 = x * a;
+        const int bin = hist_bin(x2, m2);
+        if (bin < lo) above += (double)exp2f(x2 - m2);
+        cnt = bin >= lo && bin <= hi;
+      }
+      flush(&x, &j, cnt);
     }
-    __syncthreads();
-    atomicMin(&s_kl, kl);
-    atomicMax(&s_kh, kh);
-    __syncthreads();
-    klo = s_kl;
-    khi = s_kh;
+    atomicMin(&sm.klo, kl);
+    atomicMax(&sm.khi, kh);
   }
+  double mass_above = block_sum<kStThreads>(above, sm.red);  // (syncs sm.count / klo / khi too)
+  uint32_t klo = sm.klo, khi = sm.khi;
   uint32_t cut_key = 0;
   int cut_idx = -1;
   double z = 0.0;
+  bool collected = true;
+  if (mass_above >= tau || sm.count == 0) {
+    // the f32 histogram misplaced the window (never expected): refine over
+    // every key from scratch
+    klo = 0u;
+    khi = 0xffffffffu;
+    mass_above = 0.0;
+    collected = false;
+  }
   for (int level = 0; level < 8; ++level) {
-    if (threadIdx.x == 0) sm.count = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-      uint32_t k = orderable_u32(row[i]);
-      if (k >= klo && k <= khi) {
-        int slot = atomicAdd(&sm.count, 1);
-        if (slot < kCandCap) sm.cand[slot] = ((unsigned long long)k << 32) | (0xffffffffu - (uint32_t)i);
+    if (!collected) {
+      if (threadIdx.x == 0) sm.count = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < vocab; i += kStThreads) {
+        const uint32_t k = orderable_u32(row[i]);
+        if (k >= klo && k <= khi) {
+          const int slot = atomicAdd(&sm.count, 1);
+          if (slot < kCandCap) sm.cand[slot] = ((unsigned long long)k << 32) | (0xffffffffu - (uint32_t)i);
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
+    collected = false;
     const int count = sm.count;
+    if (count == 0) {  // empty range (defensive): everything above is kept
+      cut_key = khi;
+      cut_idx = INT_MAX;
+      z = mass_above;
+      break;
+    }
     if (count <= kCandCap) {
-      // exact: sort descending by (key, -index), scan masses from mass_above
-      int np2 = 1;
-      while (np2 < count) np2 <<= 1;
-      for (int i = count + threadIdx.x; i < np2; i += kStThreads) sm.cand[i] = 0ull;
-      __syncthreads();
-      for (int size = 2; size <= np2; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          for (int i = threadIdx.x; i < np2; i += kStThreads) {
-            int j = i ^ stride;
-            if (j > i) {
-              bool desc = (i & size) == 0;
-              unsigned long long x = sm.cand[i], y = sm.cand[j];
-              if (desc ? (x < y) : (x > y)) {
-                sm.cand[i] = y;
-                sm.cand[j] = x;
-              }
-            }
-          }
-          __syncthreads();
-        }
-      }
-      // per-thread chunk of 4 consecutive sorted candidates
-      double loc[4];
-      double tot = 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int i = threadIdx.x * 4 + u;
-        double w = 0.0;
-        if (i < count) {
-          uint32_t k = (uint32_t)(sm.cand[i] >> 32);
-          uint32_t bits = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-          w = (double)exp2f(__uint_as_float(bits) * a - m2);
-        }
-        tot += w;
-        loc[u] = tot;
-      }
-      double incl = block_inclusive_scan(tot, sm.red);
-      double base = mass_above + incl - tot;
-      __shared__ int s_cut;
-      if (threadIdx.x == 0) s_cut = count - 1;
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int i = threadIdx.x * 4 + u;
-        if (i < count && base + loc[u] >= tau) atomicMin(&s_cut, i);
-      }
-      __syncthreads();
-      const int cpos = s_cut;
-      // kept mass = mass_above + candidates[0..cpos]
-      double zz = 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int i = threadIdx.x * 4 + u;
-        if (i <= cpos && i < count) {
-          uint32_t k = (uint32_t)(sm.cand[i] >> 32);
-          uint32_t bits = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-          zz += (double)exp2f(__uint_as_float(bits) * a - m2);
-        }
-      }
-      z = mass_above + block_sum<kStThreads>(zz, sm.red);
-      if (count > 0) {
-        cut_key = (uint32_t)(sm.cand[cpos] >> 32);
-        cut_idx = (int)(0xffffffffu - (uint32_t)(sm.cand[cpos] & 0xffffffffu));
-      } else {
-        // empty window: everything above is kept
-        cut_key = khi;
-        cut_idx = INT_MAX;
-        z = mass_above;
-      }
+      z = exact_cut(sm, count, mass_above, tau, a, m2, cut_key, cut_idx);
       break;
     }
     if (klo == khi) {
       // only ties remain: all candidates share the weight w*; the first j by
       // index are kept, j = ceil((tau - mass_above) / w*)
-      uint32_t bits = (klo & 0x80000000u) ? (klo & 0x7fffffffu) : ~klo;
-      double w = (double)exp2f(__uint_as_float(bits) * a - m2);
+      const double w = (double)key_weight(klo, a, m2);
       long long need = (long long)ceil((tau - mass_above) / w);
       need = need < 1 ? 1 : (need > count ? count : need);
       // index of the need-th tied element in index order: chunked prefix count
-      __shared__ int s_idx;
-      __shared__ double s_tot;
-      if (threadIdx.x == 0) s_idx = vocab - 1;
+      if (threadIdx.x == 0) sm.idx = vocab - 1;
       __syncthreads();
       long long seen = 0;
       for (int c0 = 0; c0 < vocab; c0 += kStThreads) {
-        int i = c0 + threadIdx.x;
-        bool t = i < vocab && orderable_u32(row[i]) == klo;
-        double pre = block_inclusive_scan(t ? 1.0 : 0.0, sm.red);
-        if (t && seen + (long long)pre == need) s_idx = i;
-        if (threadIdx.x == kStThreads - 1) s_tot = pre;
+        const int i = c0 + threadIdx.x;
+        const bool t = i < vocab && orderable_u32(row[i]) == klo;
+        const double pre = block_inclusive_scan(t ? 1.0 : 0.0, sm.red);
+        if (t && seen + (long long)pre == need) sm.idx = i;
+        if (threadIdx.x == kStThreads - 1) sm.tot = pre;
         __syncthreads();
-        seen += (long long)s_tot;
+        seen += (long long)sm.tot;
         __syncthreads();
         if (seen >= need) break;
       }
       __syncthreads();
       cut_key = klo;
-      cut_idx = s_idx;
+      cut_idx = sm.idx;
       z = mass_above + w * (double)need;
       break;
     }
-    // refine: 1024 sub-ranges of [klo, khi] by key (bin 0 = highest keys)
-    for (int i = threadIdx.x; i < kHistBins; i += kStThreads) sm.hist[0][i] = 0.f;
+    // refine: kRefBins sub-ranges of [klo, khi] by key (bin 0 = highest keys)
+    sm.rh[threadIdx.x] = 0.0;
     __syncthreads();
     const unsigned long long span = (unsigned long long)(khi - klo) + 1ull;
     for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-      float l = row[i];
-      uint32_t k = orderable_u32(l);
+      const float l = row[i];
+      const uint32_t k = orderable_u32(l);
       if (k >= klo && k <= khi) {
-        int bin = (int)(((unsigned long long)(khi - k) * kHistBins) / span);
-        atomicAdd(&sm.hist[0][bin], exp2f(l * a - m2));
+        const int bin = (int)(((unsigned long long)(khi - k) * kRefBins) / span);
+        atomicAdd(&sm.rh[bin], (double)exp2f(l * a - m2));
       }
     }
     __syncthreads();
-    double c2 = block_inclusive_scan(threadIdx.x < kHistBins ? (double)sm.hist[0][threadIdx.x] : 0.0, sm.red);
-    if (threadIdx.x < kHistBins) sm.cum[threadIdx.x] = mass_above + c2;
-    __syncthreads();
-    __shared__ int s_lo2, s_hi2;
+    const double rc = mass_above + block_inclusive_scan(sm.rh[threadIdx.x], sm.red);
     if (threadIdx.x == 0) {
-      s_lo2 = kHistBins - 1;
-      s_hi2 = kHistBins - 1;
+      sm.lo = kRefBins - 1;
+      sm.hi = kRefBins - 1;
     }
     __syncthreads();
-    for (int bb = threadIdx.x; bb < kHistBins; bb += kStThreads) {
-      if (sm.cum[bb] >= tau * (1.0 - 1e-5)) atomicMin(&s_lo2, bb);
-      if (sm.cum[bb] >= tau * (1.0 + 1e-5)) atomicMin(&s_hi2, bb);
-    }
+    if (rc >= tau * (1.0 - 1e-9)) atomicMin(&sm.lo, (int)threadIdx.x);
+    if (rc >= tau * (1.0 + 1e-9)) atomicMin(&sm.hi, (int)threadIdx.x);
     __syncthreads();
-    const int blo = s_lo2, bhi = max(s_hi2, s_lo2);
-    mass_above = blo > 0 ? sm.cum[blo - 1] : mass_above;
+    const int blo = sm.lo, bhi = max(sm.hi, sm.lo);
+    if (threadIdx.x == blo - 1) sm.tot = rc;
+    __syncthreads();
+    if (blo > 0) mass_above = sm.tot;
     // key range of bins [blo, bhi]: bin(k) = floor((khi - k) * B / span)
-    const uint32_t nkhi = khi - (uint32_t)(((unsigned long long)blo * span + kHistBins - 1) / kHistBins);
-    const uint32_t nklo_off = (uint32_t)((((unsigned long long)(bhi + 1)) * span + kHistBins - 1) / kHistBins) - 1u;
+    const uint32_t nkhi = khi - (uint32_t)(((unsigned long long)blo * span + kRefBins - 1) / kRefBins);
+    const uint32_t nklo_off = (uint32_t)((((unsigned long long)(bhi + 1)) * span + kRefBins - 1) / kRefBins) - 1u;
     const uint32_t nklo = khi - min((unsigned long long)nklo_off, (unsigned long long)(khi - klo));
     klo = nklo;
     khi = nkhi;
@@ -570,10 +738,18 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   }
 }
 
-// p_k(t) = max(P(t) - c Q(t), 0) / M at row `cur` (Q from draft row cur).
+// Phase B: one thread-block cluster of kCl CTAs per sequence.  Every CTA
+// makes the same walk decisions (sampling.py:173-202) from the same inputs;
+// each owns a contiguous 1/kCl of the vocabulary for the full-row passes (a
+// rejection's residual mass, the bonus inverse CDF), whose block sums are
+// exchanged through distributed shared memory.  A rejection's residual
+// norm(max(p - q, 0)) is kept in closed form max(P - c Q, 0) / M (siblings
+// share the parent's q, engine.py:405-407).
+constexpr int kWThreads = 512;
+
 struct WalkRow {
   const float *tl;  // target logits row
-  const float *dl;  // draft logits row (nullptr when cur has no children)
+  const float *dl;  // draft logits row (nullptr when the row has no children)
   RowStats ts, ds;
 };
 
@@ -585,34 +761,93 @@ __device__ __forceinline__ float q_of(const WalkRow &w, float a, int t) {
   return w.dl ? exp2f(w.dl[t] * a - w.ds.m2 - w.ds.log2_z) : 0.f;
 }
 
-// Phase B: one CTA per sequence.
-__global__ void __launch_bounds__(kStThreads, 1) stochastic_walk_kernel(
+// sum over [v0, v1) of max(P - c Q, 0) / M (per thread), with the values
+// optionally stored (residual); 16-byte loads, 4 iterations in flight.
+template <bool kStore>
+__device__ __forceinline__ double residual_part(const WalkRow &w, float a, double c, double M, int v0, int v1,
+                                                bool vec, float *__restrict__ store) {
+  double part = 0.0;
+  const float *__restrict__ tl = w.tl;
+  const float *__restrict__ dl = w.dl;
+  auto one = [&](float l, float d, int i) {
+    const float p = kept(w.ts, l, i) ? exp2f(l * a - w.ts.m2 - w.ts.log2_z) : 0.f;
+    const float q = dl ? exp2f(d * a - w.ds.m2 - w.ds.log2_z) : 0.f;
+    double v = (double)p - c * (double)q;
+    v = (v > 0.0 ? v : 0.0) / M;
+    if (kStore) store[i] = (float)v;
+    part += v;
+  };
+  if (vec) {
+    const float4 *__restrict__ t4 = reinterpret_cast<const float4 *>(tl + v0);
+    const float4 *__restrict__ d4 = dl ? reinterpret_cast<const float4 *>(dl + v0) : nullptr;
+    const int n4 = (v1 - v0) >> 2;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n4; i += kWThreads) {
+      const float4 t = __ldg(t4 + i);
+      const float4 d = d4 ? __ldg(d4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int base = v0 + 4 * i;
+      one(t.x, d.x, base);
+      one(t.y, d.y, base + 1);
+      one(t.z, d.z, base + 2);
+      one(t.w, d.w, base + 3);
+    }
+    for (int i = v0 + (n4 << 2) + threadIdx.x; i < v1; i += kWThreads) one(tl[i], dl ? dl[i] : 0.f, i);
+  } else {
+    for (int i = v0 + threadIdx.x; i < v1; i += kWThreads) one(tl[i], dl ? dl[i] : 0.f, i);
+  }
+  return part;
+}
+
+// Cluster-wide exchange of one double per CTA: returns all kCl values in
+// CTA-rank order (identical on every CTA).  Two alternating slots make one
+// cluster barrier per exchange sufficient.
+template <int kCl>
+__device__ __forceinline__ void cluster_exchange(double v, double *slots, int &phase, double *out) {
+  cg::cluster_group cl = cg::this_cluster();
+  if (threadIdx.x == 0) slots[phase & 1] = v;
+  cl.sync();
+#pragma unroll
+  for (int q = 0; q < kCl; ++q) out[q] = *cl.map_shared_rank(&slots[phase & 1], q);
+  ++phase;
+}
+
+template <int kCl>
+__global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
     const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, const int32_t *__restrict__ tokens,
     const double *__restrict__ uniforms, int n_uniforms, const RowStats *__restrict__ stats,
     int32_t *__restrict__ path, int32_t *__restrict__ path_len, int64_t *__restrict__ next_token,
     int32_t *__restrict__ uniforms_used, float *__restrict__ residual, int32_t *__restrict__ err) {
   __shared__ double red[32];
+  __shared__ double slots[2];
   __shared__ int s_flag;
-  const int b = blockIdx.x;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank();
+  const int b = blockIdx.x / kCl;
   const int n = min(n_rows[b], r_max);
   const int32_t *par = parent + (int64_t)b * r_max;
   const int32_t *tok = tokens + (int64_t)b * r_max;
   const double *uni = uniforms + (int64_t)b * n_uniforms;
   const RowStats *st = stats + (int64_t)b * r_max * 2;
+  // this CTA's vocabulary slice (multiple of 4 wide, so 16-byte aligned rows stay aligned)
+  const int per = ((vocab + kCl - 1) / kCl + 3) & ~3;
+  const int v0 = min(vocab, crank * per), v1 = min(vocab, v0 + per);
+  const bool vec = (vocab & 3) == 0 && ((uintptr_t)target & 15) == 0 && ((uintptr_t)draft & 15) == 0;
+  int phase = 0;
+  double vals[kCl];
   if (threadIdx.x == 0) s_flag = 0;
   __syncthreads();
   // any invalid (NaN) row in this sequence aborts it
-  for (int r = threadIdx.x; r < n; r += kStThreads)
+  for (int r = threadIdx.x; r < n; r += kWThreads)
     if (!st[2 * r].valid) atomicOr(&s_flag, 1);
   __syncthreads();
   if (s_flag) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && crank == 0) {
       path_len[b] = 0;
       next_token[b] = 0;
       uniforms_used[b] = 0;
     }
-    return;
+    return;  // uniform across the cluster: no exchange follows
   }
   int cur = 0, used = 0, len = 0;
   double c = 0.0, M = 1.0;
@@ -623,6 +858,12 @@ __global__ void __launch_bounds__(kStThreads, 1) stochastic_walk_kernel(
     w.ts = st[2 * r];
     w.ds = st[2 * r + 1];
     w.dl = w.ds.valid ? draft + ((int64_t)b * r_max + r) * vocab : nullptr;
+    // this CTA's slices of the node's rows stream into L2 while the
+    // (latency-bound) sibling decisions run
+    if (vec && threadIdx.x == 0 && v1 > v0) {
+      prefetch_l2(w.tl + v0, (uint32_t)(v1 - v0) * 4u);
+      if (w.dl) prefetch_l2(w.dl + v0, (uint32_t)(v1 - v0) * 4u);
+    }
     return w;
   };
   WalkRow w = make_row(cur);
@@ -641,7 +882,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stochastic_walk_kernel(
       const double pt = fmax(pt_full - c * qt, 0.0) / M;
       const bool acc = qt <= 0.0 ? pt > 0.0 : u < fmin(1.0, pt / qt);
       if (acc) {
-        if (threadIdx.x == 0) path[(int64_t)b * r_max + len] = j - 1;
+        if (threadIdx.x == 0 && crank == 0) path[(int64_t)b * r_max + len] = j - 1;
         ++len;
         cur = j;
         c = 0.0;
@@ -652,12 +893,11 @@ __global__ void __launch_bounds__(kStThreads, 1) stochastic_walk_kernel(
       }
       // rejection: residual norm(max(p - q, 0)) == max(P - c' Q, 0) / M'
       const double cn = c + M;
-      double part = 0.0;
-      for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-        double v = (double)p_of(w, a, i) - cn * (double)q_of(w, a, i);
-        part += v > 0.0 ? v : 0.0;
-      }
-      const double Mn = block_sum<kStThreads>(part, red);
+      const double part = block_sum<kWThreads>(residual_part<false>(w, a, cn, 1.0, v0, v1, vec, nullptr), red);
+      cluster_exchange<kCl>(part, slots, phase, vals);
+      double Mn = 0.0;
+#pragma unroll
+      for (int q = 0; q < kCl; ++q) Mn += vals[q];
       if (Mn / M <= 1e-12) {
         c = 0.0;  // anchor fallback (sampling.py:193-195)
         M = 1.0;
@@ -670,78 +910,97 @@ __global__ void __launch_bounds__(kStThreads, 1) stochastic_walk_kernel(
   }
   if (!failed && used >= n_uniforms) failed = true;
   if (failed) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && crank == 0) {
       atomicOr(err, SDB_ERR_UNIFORMS);
       path_len[b] = len;
       next_token[b] = -1;
       uniforms_used[b] = used;
     }
+    cl.sync();
     return;
   }
   const double u = uni[used++];
   // bonus: inverse CDF of p = max(P - c Q, 0) / M over the vocab in index
-  // order (sample_from, sampling.py:105-109).  Warps own contiguous segments.
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = kStThreads / 32;
-  const int seg = (vocab + nw - 1) / nw;
-  const int s0 = warp * seg, s1 = min(vocab, s0 + seg);
-  auto pval = [&](int i) {
-    double v = (double)p_of(w, a, i) - c * (double)q_of(w, a, i);
-    return (v > 0.0 ? v : 0.0) / M;
-  };
-  double wsum = 0.0;
-  for (int i = s0 + lane; i < s1; i += 32) {
-    double v = pval(i);
-    wsum += v;
-    if (residual) residual[(int64_t)b * vocab + i] = (float)v;
-  }
-  wsum = warp_sum(wsum);
-  __shared__ double segsum[32];
-  __shared__ double s_prefix;
-  if (lane == 0) segsum[warp] = wsum;
-  __syncthreads();
-  __shared__ int s_tok;
-  if (threadIdx.x == 0) {
-    // searchsorted(cumsum, u, 'right'): first index with cumsum > u
-    double cum = 0.0;
-    int ws = nw - 1;
-    for (int k = 0; k < nw; ++k) {
-      if (cum + segsum[k] > u) {
-        ws = k;
-        break;
-      }
-      cum += segsum[k];
-    }
-    s_prefix = cum;  // mass before the chosen segment
-    s_tok = ws;
-  }
-  __syncthreads();
-  const int ws = s_tok;
-  if (warp == ws) {
-    double cum = s_prefix;
-    const int a0 = ws * seg, a1 = min(vocab, a0 + seg);
-    int found = -1;
-    for (int i0 = a0; i0 < a1 && found < 0; i0 += 32) {
-      int i = i0 + lane;
-      double v = i < a1 ? pval(i) : 0.0;
-      double incl = v;
+  // order (sample_from, sampling.py:105-109): slice masses -> owning CTA.
+  float *res_row = residual ? residual + (int64_t)b * vocab : nullptr;
+  const double mine = block_sum<kWThreads>(
+      res_row ? residual_part<true>(w, a, c, M, v0, v1, vec, res_row) : residual_part<false>(w, a, c, M, v0, v1, vec,
+                                                                                           nullptr),
+      red);
+  cluster_exchange<kCl>(mine, slots, phase, vals);
+  double base = 0.0, total = 0.0;
+  int owner = -1;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        double t = __shfl_up_sync(SDB_FULL_MASK, incl, o);
-        if (lane >= o) incl += t;
-      }
-      unsigned hit = __ballot_sync(SDB_FULL_MASK, i < a1 && cum + incl > u);
-      if (hit) found = i0 + __ffs(hit) - 1;
-      cum += __shfl_sync(SDB_FULL_MASK, incl, 31);
+  for (int q = 0; q < kCl; ++q) {
+    if (owner < 0 && total + vals[q] > u) {
+      owner = q;
+      base = total;
     }
-    if (lane == 0) s_tok = found < 0 ? vocab - 1 : found;
+    total += vals[q];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (owner < 0 && crank == kCl - 1) {
+    if (threadIdx.x == 0) next_token[b] = vocab - 1;
+  } else if (owner == crank) {
+    // warps own contiguous segments of the slice
+    __shared__ double segsum[kWThreads / 32];
+    __shared__ double s_prefix;
+    __shared__ int s_seg, s_tok;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int nw = kWThreads / 32;
+    const int seg = (v1 - v0 + nw - 1) / nw;
+    const int s0 = v0 + warp * seg, s1 = min(v1, s0 + seg);
+    auto pval = [&](int i) {
+      double v = (double)p_of(w, a, i) - c * (double)q_of(w, a, i);
+      return (v > 0.0 ? v : 0.0) / M;
+    };
+    double wsum = 0.0;
+    for (int i = s0 + lane; i < s1; i += 32) wsum += pval(i);
+    wsum = warp_sum(wsum);
+    if (lane == 0) segsum[warp] = wsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // searchsorted(cumsum, u, 'right'): first index with cumsum > u
+      double cum = base;
+      int ws = nw - 1;
+      for (int k = 0; k < nw; ++k) {
+        if (cum + segsum[k] > u) {
+          ws = k;
+          break;
+        }
+        cum += segsum[k];
+      }
+      s_prefix = cum;  // mass before the chosen segment
+      s_seg = ws;
+    }
+    __syncthreads();
+    const int ws = s_seg;
+    if (warp == ws) {
+      double cum = s_prefix;
+      const int a0 = v0 + ws * seg, a1 = min(v1, a0 + seg);
+      int found = -1;
+      for (int i0 = a0; i0 < a1 && found < 0; i0 += 32) {
+        int i = i0 + lane;
+        double v = i < a1 ? pval(i) : 0.0;
+        double incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          double t = __shfl_up_sync(SDB_FULL_MASK, incl, o);
+          if (lane >= o) incl += t;
+        }
+        unsigned hit = __ballot_sync(SDB_FULL_MASK, i < a1 && cum + incl > u);
+        if (hit) found = i0 + __ffs(hit) - 1;
+        cum += __shfl_sync(SDB_FULL_MASK, incl, 31);
+      }
+      if (lane == 0) s_tok = found < 0 ? v1 - 1 : found;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) next_token[b] = min(s_tok, vocab - 1);
+  }
+  if (threadIdx.x == 0 && crank == 0) {
     path_len[b] = len;
-    next_token[b] = min(s_tok, vocab - 1);
     uniforms_used[b] = used;
   }
+  cl.sync();  // peers may still read this CTA's exchange slots
 }
 
 }  // namespace sdb
@@ -845,10 +1104,29 @@ extern "C" int sdb_accept_stochastic(const float *target_logits, const float *dr
   sdb::row_stats_kernel<<<dim3(r_max, batch, 2), sdb::kStThreads, smem, s>>>(
       target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err);
   SDB_CHECK_LAUNCH();
-  sdb::stochastic_walk_kernel<<<batch, sdb::kStThreads, 0, s>>>(target_logits, draft_logits, r_max, vocab, a,
-                                                                 parent, n_rows, tokens, uniforms, n_uniforms,
-                                                                 stats, path, path_len, next_token, uniforms_used,
-                                                                 residual, err);
+  // cluster size: enough CTAs to cover the SMs (8 = portable maximum)
+  const int ncl = batch >= 64 ? 4 : (batch >= 32 ? 8 : 8);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(batch * ncl);
+  cfg.blockDim = dim3(sdb::kWThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = ncl;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  cudaError_t le;
+  if (ncl == 4)
+    le = cudaLaunchKernelEx(&cfg, sdb::stochastic_walk_kernel<4>, target_logits, draft_logits, r_max, vocab, a,
+                            parent, n_rows, tokens, uniforms, n_uniforms, (const sdb::RowStats *)stats, path,
+                            path_len, next_token, uniforms_used, residual, err);
+  else
+    le = cudaLaunchKernelEx(&cfg, sdb::stochastic_walk_kernel<8>, target_logits, draft_logits, r_max, vocab, a,
+                            parent, n_rows, tokens, uniforms, n_uniforms, (const sdb::RowStats *)stats, path,
+                            path_len, next_token, uniforms_used, residual, err);
+  if (le != cudaSuccess) return sdb::record_cuda_error(le);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

@@ -81,4 +81,9 @@ __device__ __forceinline__ bool kept(const RowStats &st, float l, int idx) {
   return k > st.cut_key || (k == st.cut_key && idx <= st.cut_idx);
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (TMA engine; one thread issues it).
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 }  // namespace sdb

@@ -1,0 +1,11 @@
+#!/bin/bash
+O=gpurun_out; T=${1:-st2}; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_sampling.py tests/test_gpu_parity.py -q -m gpu -x > $O/${T}_pytest.txt 2>&1; tail -15 $O/${T}_pytest.txt
+for c in "--config c5" "--config c3 --mode stochastic"; do
+  timeout 600 python bench.py $c --no-cpu-baseline --no-e2e 2>>$O/${T}_bench.err | tee -a $O/${T}_bench.json | cut -c 1-200
+  grep -o '"kernels_ms": {[^}]*}' $O/${T}_bench.json | tail -1
+done
+tail -5 $O/${T}_bench.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"row_stats|stochastic_walk" -s 2 -c 2 -o $O/${T}_c5 \
+  python bench.py --config c5 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/${T}_ncu.log 2>&1; tail -1 $O/${T}_ncu.log
+exit 0

@@ -471,11 +471,20 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     return;
   }
   for (int i = threadIdx.x; i < kHistCopies * kHistBins; i += kStThreads) (&sm.hist[0][0])[i] = 0u;
-  // pass 1: max + NaN
-  float mx;
-  bool nan;
-  row_max_nan(row, vocab, vec, mx, nan);
-  if (__syncthreads_or(nan)) {
+  // pass 1: max + NaN (3-input max.NaN: NaN propagates into the maximum)
+  float mx = -INFINITY;
+  for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
+    float4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * kStThreads + threadIdx.x;
+      v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) mx = max3_nan(mx, max3_nan(v[u].x, v[u].y, v[u].z), v[u].w);
+  }
+  for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) mx = max3_nan(mx, row[j], row[j]);
+  if (__syncthreads_or(mx != mx)) {
     if (threadIdx.x == 0) {
       atomicOr(err, SDB_ERR_NAN);
       out->valid = 0;
@@ -484,21 +493,31 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   }
   mx = block_max<kStThreads>(mx, sm.redf);
   const float m2 = mx * a;
-  // pass 2 (L2): normaliser + mass histogram
+  // pass 2 (L2): normaliser + mass histogram, two elements per packed op.
+  // d = (m2 - x a) * 64 >= 0; bin = round(d) by the 1.5 * 2^23 magic add;
+  // r = 2^-(d - bin)/64 = e^-t by a quadratic (|error| < 3e-8); the bin
+  // accumulates round(r * 2^14) in a native 32-bit shared atomic.
+  constexpr float kMagic = 12582912.0f;
+  const uint32_t kMagicBits = __float_as_uint(kMagic);
   uint32_t *hist = sm.hist[(threadIdx.x >> 5) & (kHistCopies - 1)];
-  float s_loc = 0.f;
-  auto acc2 = [&](float l) {
-    const float x2 = l * a;
-    s_loc += exp2f(x2 - m2);
-    // d = (m2 - x2) * 64: bin = floor(d), r = 2^-(d - bin)/64 by a quadratic
-    // (error < 2e-7), no MUFU
-    const float d = (m2 - x2) * kHistScale;
-    if (d < (float)(kHistBins - 1)) {
-      const int bin = (int)d;
-      const float t = (d - (float)bin) * (0.6931471805599453f / kHistScale);
-      const float rr = fmaf(t, fmaf(t, 0.5f, -1.0f), 1.0f);
-      atomicAdd(&hist[bin], (uint32_t)__float2int_rn(rr * kFixScale));
-    }
+  const uint64_t A2 = f2splat(a), NM2 = f2splat(-m2), DA2 = f2splat(-kHistScale * a),
+                 DM2 = f2splat(kHistScale * m2), MAG2 = f2splat(kMagic), NMAG2 = f2splat(-kMagic),
+                 TC2 = f2splat(0.6931471805599453f / kHistScale), HALF2 = f2splat(0.5f), NEG1 = f2splat(-1.0f),
+                 ONE2 = f2splat(1.0f), FIX2 = f2splat(kFixScale);
+  uint64_t s2 = 0;  // packed (0.f, 0.f)
+  auto acc2 = [&](uint64_t l2) {
+    float e0, e1;
+    f2unpack(ffma2(l2, A2, NM2), e0, e1);
+    s2 = fadd2(s2, f2pack(ex2(e0), ex2(e1)));
+    const uint64_t d = ffma2(l2, DA2, DM2);
+    const uint64_t g = fadd2(d, MAG2);
+    const uint64_t t = fmul2(fsub2(d, fadd2(g, NMAG2)), TC2);
+    const uint64_t rr = ffma2(t, ffma2(t, HALF2, NEG1), ONE2);
+    const uint64_t fx = ffma2(rr, FIX2, MAG2);
+    const uint32_t b0 = (uint32_t)g - kMagicBits, b1 = (uint32_t)(g >> 32) - kMagicBits;
+    const uint32_t f0 = (uint32_t)fx - kMagicBits, f1 = (uint32_t)(fx >> 32) - kMagicBits;
+    if (b0 < (uint32_t)(kHistBins - 1)) atomicAdd(&hist[b0], f0);
+    if (b1 < (uint32_t)(kHistBins - 1)) atomicAdd(&hist[b1], f1);
   };
   for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
     float4 v[kU];
@@ -509,17 +528,25 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      acc2(v[u].x);
-      acc2(v[u].y);
-      acc2(v[u].z);
-      acc2(v[u].w);
+      acc2(f2pack(v[u].x, v[u].y));
+      acc2(f2pack(v[u].z, v[u].w));
     }
   }
-  for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) acc2(row[j]);
+  float s_lo, s_hi;
+  f2unpack(s2, s_lo, s_hi);
+  float s_loc = s_lo + s_hi;
+  for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) {
+    const float x = row[j];
+    const uint64_t l2 = f2pack(x, -INFINITY);
+    s2 = 0;
+    acc2(l2);
+    f2unpack(s2, s_lo, s_hi);
+    s_loc += s_lo;
+  }
   const double s = block_sum<kStThreads>((double)s_loc, sm.red);
   const double tau = ((double)top_p - 1e-12) * s;
   // window [lo, hi] of bins whose cumulative (bin 0 = largest values) may
-  // straddle tau given the f32 bin sums
+  // straddle tau given the fixed-point bin sums
   {
     double loc[kBinsPerThread];
     double tsum = 0.0;
@@ -553,15 +580,17 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     __syncthreads();
   }
   const int lo = sm.lo, hi = max(sm.hi, sm.lo);
-  // pass 3 (L2): exact f64 mass above the window; collect the window's
-  // elements (warp-aggregated slots) and their key range
-  double above = 0.0;
+  // pass 3 (L2): the same d splits the keys monotonically into above (d <
+  // lo - 1/2), the window and below; exact mass above, window elements
+  // collected with warp-aggregated slots.  Keys with equal logits share d,
+  // so ties are never split.
+  const float dlo = (float)lo - 0.5f, dhi = (float)hi + 0.5f;
+  float above = 0.f;
   {
     unsigned kl = 0xffffffffu, kh = 0u;
     const int lane = threadIdx.x & 31;
-    auto flush = [&](const float *x, const int *idx, int cnt) {
-      // cnt candidates of this thread among x[0..]: warp prefix -> slots
-      if (!__any_sync(SDB_FULL_MASK, cnt > 0)) return;
+    // append this thread's `cnt` window elements (warp prefix -> slots)
+    auto append_slots = [&](int cnt) {
       int incl = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -570,14 +599,15 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
       }
       int base = 0;
       if (lane == 31) base = atomicAdd(&sm.count, incl);
-      base = __shfl_sync(SDB_FULL_MASK, base, 31) + incl - cnt;
-      for (int q = 0; q < cnt; ++q) {
-        const uint32_t k = orderable_u32(x[q]);
-        if (base + q < kCandCap) sm.cand[base + q] = ((unsigned long long)k << 32) | (0xffffffffu - (uint32_t)idx[q]);
-        kl = min(kl, k);
-        kh = max(kh, k);
-      }
+      return __shfl_sync(SDB_FULL_MASK, base, 31) + incl - cnt;
     };
+    auto put = [&](int slot, float x, int idx) {
+      const uint32_t k = prob_key(x);
+      if (slot < kCandCap) sm.cand[slot] = ((unsigned long long)k << 32) | (0xffffffffu - (uint32_t)idx);
+      kl = min(kl, k);
+      kh = max(kh, k);
+    };
+    uint64_t ab2 = 0;
     for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
       float4 v[kU];
 #pragma unroll
@@ -585,27 +615,35 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
         const int i = i0 + u * kStThreads + threadIdx.x;
         v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       }
-      float cx[4 * kU];
-      int ci[4 * kU];
-      int cnt = 0;
+      uint32_t mask = 0;  // bit 4u+e: element e of v[u] lies in the window
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int base_idx = 4 * (i0 + u * kStThreads + threadIdx.x);
-        const float xs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float x2 = xs[e] * a;
-          const int bin = hist_bin(x2, m2);
-          if (bin < lo) above += (double)exp2f(x2 - m2);
-          if (bin >= lo && bin <= hi && base_idx + e < vocab) {
-            cx[cnt] = xs[e];
-            ci[cnt] = base_idx + e;
-            ++cnt;
-          }
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t l2 = h ? f2pack(v[u].z, v[u].w) : f2pack(v[u].x, v[u].y);
+          float d0, d1, e0, e1;
+          f2unpack(ffma2(l2, DA2, DM2), d0, d1);
+          f2unpack(ffma2(l2, A2, NM2), e0, e1);
+          ab2 = fadd2(ab2, f2pack(d0 < dlo ? ex2(e0) : 0.f, d1 < dlo ? ex2(e1) : 0.f));
+          mask |= (uint32_t)(d0 >= dlo && d0 < dhi) << (4 * u + 2 * h);
+          mask |= (uint32_t)(d1 >= dlo && d1 < dhi) << (4 * u + 2 * h + 1);
         }
       }
-      flush(cx, ci, cnt);
+      if (__any_sync(SDB_FULL_MASK, mask != 0)) {
+        int slot = append_slots(__popc(mask));
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int bi = 4 * (i0 + u * kStThreads + threadIdx.x);
+          if (mask & (1u << (4 * u))) put(slot++, v[u].x, bi);
+          if (mask & (2u << (4 * u))) put(slot++, v[u].y, bi + 1);
+          if (mask & (4u << (4 * u))) put(slot++, v[u].z, bi + 2);
+          if (mask & (8u << (4 * u))) put(slot++, v[u].w, bi + 3);
+        }
+      }
     }
+    float a_lo, a_hi;
+    f2unpack(ab2, a_lo, a_hi);
+    above = a_lo + a_hi;
     // scalar tail (and the non-vector path): one element per thread per step
     const int t0 = n4 << 2;
     for (int j0 = t0; j0 < vocab; j0 += kStThreads) {
@@ -614,17 +652,22 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
       int cnt = 0;
       if (j < vocab) {
         x = row[j];
-        const float x2 = x * a;
-        const int bin = hist_bin(x2, m2);
-        if (bin < lo) above += (double)exp2f(x2 - m2);
-        cnt = bin >= lo && bin <= hi;
+        float d0, d1, e0, e1;
+        const uint64_t l2 = f2pack(x, x);
+        f2unpack(ffma2(l2, DA2, DM2), d0, d1);
+        f2unpack(ffma2(l2, A2, NM2), e0, e1);
+        if (d0 < dlo) above += ex2(e0);
+        cnt = d0 >= dlo && d0 < dhi;
       }
-      flush(&x, &j, cnt);
+      if (__any_sync(SDB_FULL_MASK, cnt != 0)) {
+        const int slot = append_slots(cnt);
+        if (cnt) put(slot, x, j);
+      }
     }
     atomicMin(&sm.klo, kl);
     atomicMax(&sm.khi, kh);
   }
-  double mass_above = block_sum<kStThreads>(above, sm.red);  // (syncs sm.count / klo / khi too)
+  double mass_above = block_sum<kStThreads>((double)above, sm.red);  // (syncs sm.count / klo / khi too)
   uint32_t klo = sm.klo, khi = sm.khi;
   uint32_t cut_key = 0;
   int cut_idx = -1;
@@ -643,7 +686,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
       if (threadIdx.x == 0) sm.count = 0;
       __syncthreads();
       for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-        const uint32_t k = orderable_u32(row[i]);
+        const uint32_t k = prob_key(row[i]);
         if (k >= klo && k <= khi) {
           const int slot = atomicAdd(&sm.count, 1);
           if (slot < kCandCap) sm.cand[slot] = ((unsigned long long)k << 32) | (0xffffffffu - (uint32_t)i);
@@ -675,7 +718,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
       long long seen = 0;
       for (int c0 = 0; c0 < vocab; c0 += kStThreads) {
         const int i = c0 + threadIdx.x;
-        const bool t = i < vocab && orderable_u32(row[i]) == klo;
+        const bool t = i < vocab && prob_key(row[i]) == klo;
         const double pre = block_inclusive_scan(t ? 1.0 : 0.0, sm.red);
         if (t && seen + (long long)pre == need) sm.idx = i;
         if (threadIdx.x == kStThreads - 1) sm.tot = pre;
@@ -696,7 +739,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const unsigned long long span = (unsigned long long)(khi - klo) + 1ull;
     for (int i = threadIdx.x; i < vocab; i += kStThreads) {
       const float l = row[i];
-      const uint32_t k = orderable_u32(l);
+      const uint32_t k = prob_key(l);
       if (k >= klo && k <= khi) {
         const int bin = (int)(((unsigned long long)(khi - k) * kRefBins) / span);
         atomicAdd(&sm.rh[bin], (double)exp2f(l * a - m2));
@@ -750,32 +793,40 @@ constexpr int kWThreads = 512;
 struct WalkRow {
   const float *tl;  // target logits row
   const float *dl;  // draft logits row (nullptr when the row has no children)
-  RowStats ts, ds;
+  float p_off, q_off;  // -(m2 + log2 Z) of the target / draft softmax
+  float cut_l;         // nucleus cut logit (keys above are kept; ties by index)
+  int cut_idx, keep_all;
 };
 
-__device__ __forceinline__ float p_of(const WalkRow &w, float a, int t) {
-  float l = w.tl[t];
-  return kept(w.ts, l, t) ? exp2f(l * a - w.ts.m2 - w.ts.log2_z) : 0.f;
-}
-__device__ __forceinline__ float q_of(const WalkRow &w, float a, int t) {
-  return w.dl ? exp2f(w.dl[t] * a - w.ds.m2 - w.ds.log2_z) : 0.f;
+__device__ __forceinline__ float key_to_logit(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-// sum over [v0, v1) of max(P - c Q, 0) / M (per thread), with the values
-// optionally stored (residual); 16-byte loads, 4 iterations in flight.
+// target p of logit l at vocab index i (target_dist, sampling.py:87-102)
+__device__ __forceinline__ float p_val(const WalkRow &w, float a, float l, int i) {
+  const bool keep = w.keep_all || l > w.cut_l || (l == w.cut_l && i <= w.cut_idx);
+  return keep ? ex2(fmaf(l, a, w.p_off)) : 0.f;
+}
+__device__ __forceinline__ float q_val(const WalkRow &w, float a, float d) { return ex2(fmaf(d, a, w.q_off)); }
+__device__ __forceinline__ float p_of(const WalkRow &w, float a, int t) { return p_val(w, a, w.tl[t], t); }
+__device__ __forceinline__ float q_of(const WalkRow &w, float a, int t) { return w.dl ? q_val(w, a, w.dl[t]) : 0.f; }
+
+// sum over [v0, v1) of max(P - c Q, 0) / M (per-element fp32, f64
+// accumulation), with the values optionally stored (residual); 16-byte
+// loads, 4 iterations in flight.
 template <bool kStore>
 __device__ __forceinline__ double residual_part(const WalkRow &w, float a, double c, double M, int v0, int v1,
                                                 bool vec, float *__restrict__ store) {
   double part = 0.0;
   const float *__restrict__ tl = w.tl;
   const float *__restrict__ dl = w.dl;
+  const float cf = (float)c, inv_m = (float)(1.0 / M);
   auto one = [&](float l, float d, int i) {
-    const float p = kept(w.ts, l, i) ? exp2f(l * a - w.ts.m2 - w.ts.log2_z) : 0.f;
-    const float q = dl ? exp2f(d * a - w.ds.m2 - w.ds.log2_z) : 0.f;
-    double v = (double)p - c * (double)q;
-    v = (v > 0.0 ? v : 0.0) / M;
-    if (kStore) store[i] = (float)v;
-    part += v;
+    const float p = p_val(w, a, l, i);
+    const float q = dl ? q_val(w, a, d) : 0.f;
+    const float v = fmaxf(fmaf(-cf, q, p), 0.f) * inv_m;
+    if (kStore) store[i] = v;
+    part += (double)v;
   };
   if (vec) {
     const float4 *__restrict__ t4 = reinterpret_cast<const float4 *>(tl + v0);
@@ -854,10 +905,14 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
   bool failed = false;
   auto make_row = [&](int r) {
     WalkRow w;
+    const RowStats ts = st[2 * r], ds = st[2 * r + 1];
     w.tl = target + ((int64_t)b * r_max + r) * vocab;
-    w.ts = st[2 * r];
-    w.ds = st[2 * r + 1];
-    w.dl = w.ds.valid ? draft + ((int64_t)b * r_max + r) * vocab : nullptr;
+    w.dl = ds.valid ? draft + ((int64_t)b * r_max + r) * vocab : nullptr;
+    w.p_off = -(ts.m2 + ts.log2_z);
+    w.q_off = ds.valid ? -(ds.m2 + ds.log2_z) : 0.f;
+    w.keep_all = ts.keep_all;
+    w.cut_l = key_to_logit(ts.cut_key);
+    w.cut_idx = ts.cut_idx;
     // this CTA's slices of the node's rows stream into L2 while the
     // (latency-bound) sibling decisions run
     if (vec && threadIdx.x == 0 && v1 > v0) {
@@ -949,10 +1004,8 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     constexpr int nw = kWThreads / 32;
     const int seg = (v1 - v0 + nw - 1) / nw;
     const int s0 = v0 + warp * seg, s1 = min(v1, s0 + seg);
-    auto pval = [&](int i) {
-      double v = (double)p_of(w, a, i) - c * (double)q_of(w, a, i);
-      return (v > 0.0 ? v : 0.0) / M;
-    };
+    const float cf = (float)c, inv_m = (float)(1.0 / M);
+    auto pval = [&](int i) { return (double)(fmaxf(fmaf(-cf, q_of(w, a, i), p_of(w, a, i)), 0.f) * inv_m); };
     double wsum = 0.0;
     for (int i = s0 + lane; i < s1; i += 32) wsum += pval(i);
     wsum = warp_sum(wsum);
@@ -1105,7 +1158,7 @@ extern "C" int sdb_accept_stochastic(const float *target_logits, const float *dr
       target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err);
   SDB_CHECK_LAUNCH();
   // cluster size: enough CTAs to cover the SMs (8 = portable maximum)
-  const int ncl = batch >= 64 ? 4 : (batch >= 32 ? 8 : 8);
+  const int ncl = batch * 8 <= 4 * sdb::num_sms() ? 8 : 4;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(batch * ncl);
   cfg.blockDim = dim3(sdb::kWThreads);

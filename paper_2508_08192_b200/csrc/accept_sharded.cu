@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kShThreads) sh_nucleus_kernel(ShParams p, int 
     const int hi_shift = 32 - 8 * k, shift = 24 - 8 * k;
     for (int i = threadIdx.x; i < p.vl; i += kShThreads) {
       const float l = row[i];
-      const uint32_t key = orderable_u32(l);
+      const uint32_t key = prob_key(l);
       if (k > 0 && (key >> hi_shift) != nu.prefix) continue;
       const int bin = (key >> shift) & 0xff;
       atomicAdd(&hist[bin], (double)exp2f(l * p.a - st.m2));
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kShThreads) sh_finish_kernel(ShParams p) {
     __syncthreads();
     for (int c0 = 0; c0 < p.vl; c0 += kShThreads) {
       const int i = c0 + threadIdx.x;
-      const bool t = i < p.vl && orderable_u32(row[i]) == nu0.cut_key;
+      const bool t = i < p.vl && prob_key(row[i]) == nu0.cut_key;
       const unsigned bal = __ballot_sync(SDB_FULL_MASK, t);
       // block-wide exclusive prefix of tied flags (warp ballots)
       __shared__ int wcnt[kShThreads / 32];

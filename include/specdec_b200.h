@@ -109,6 +109,11 @@ typedef struct sdb_tree_attn_args {
   int dtype;                  /* SDB_DTYPE_BF16 (tcgen05 path) or SDB_DTYPE_F32 */
   int num_splits;             /* 0 = auto                                     */
   int kernel;                 /* 0 = auto, 1 = tcgen05 (sm_100a), 2 = SIMT    */
+  const int32_t *q_row0;      /* [B] or NULL: only rows [q_row0, n_rows) query
+                                 (written); keys stay all tree rows [0, n_rows).
+                                 The draft stage's depth step: new nodes attend
+                                 the carried + new suffix under a rectangular
+                                 mask (engine.py:424-432, model.py:265-270) */
 } sdb_tree_attn_args;
 
 int64_t sdb_tree_attn_workspace(const sdb_tree_attn_args *a);

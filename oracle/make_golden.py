@@ -424,13 +424,71 @@ def gen_compact():
     np.savez_compressed(os.path.join(OUT, "compact.npz"), **out)
 
 
+def gen_draft_attention():
+    """Draft stage depth steps (engine.py:424-432 -> model.py:257-270): the
+    new nodes of each depth attend the draft-cache prefix (CausalPrefix) and
+    the carried ++ new suffix under the engine's vis-row mask (built here
+    exactly like draft_stage, engine.py:409-421), merged with the
+    reference's merge_attentions."""
+    rng = np.random.default_rng(909)
+    store = {}
+    k = 0
+    for spec, hq, hkv, d, ctx in ((TREE64, 8, 2, 16, 40), (N8, 4, 1, 8, 0), ("chain:4", 4, 2, 8, 17)):
+        tree = R_tree.parse_tree(spec)
+        parent = tree.parent
+        n = len(parent)
+        depth = [0] * n
+        vis = []
+        for i, p in enumerate(parent):
+            depth[i] = 1 if p == R_tree.ROOT else depth[p] + 1
+            row = np.zeros(i + 1, dtype=bool)
+            if p != R_tree.ROOT:
+                row[:p + 1] = vis[p]
+            row[i] = True
+            vis.append(row)
+        g = hq // hkv
+
+        def rep(x):
+            return np.repeat(x.reshape(x.shape[0], hkv, d), g, axis=1).reshape(x.shape[0], hq * d)
+
+        ck = bf16_round(rng.normal(size=(ctx, hkv * d)))
+        cv = bf16_round(rng.normal(size=(ctx, hkv * d)))
+        sk = bf16_round(rng.normal(size=(n, hkv * d)))
+        sv = bf16_round(rng.normal(size=(n, hkv * d)))
+        q = bf16_round(rng.normal(size=(n, hq * d)))
+        scale = d ** -0.5
+        for dep in range(1, max(depth) + 1):
+            new = [i for i in range(n) if depth[i] == dep]
+            total = new[-1] + 1
+            mask = np.zeros((len(new), total), dtype=bool)
+            for j, real in enumerate(new):
+                mask[j, :real + 1] = vis[real]
+            parts = []
+            if ctx > 0:
+                parts.append(R_att.attend(q[new], rep(ck), rep(cv), R_att.CausalPrefix(ctx), scale, hq))
+            parts.append(R_att.attend(q[new], rep(sk[:total]), rep(sv[:total]), R_att.TreeSuffix(mask), scale, hq))
+            m = R_att.merge_partials(parts, hq)  # merge_attentions == merge_partials(...).out
+            pre = f"d{k}_"
+            store.update({pre + "meta": np.array([hq, hkv, d, ctx, new[0], total]), pre + "parent": np.array(parent),
+                          pre + "q": q[new], pre + "ck": ck, pre + "cv": cv, pre + "sk": sk[:total],
+                          pre + "sv": sv[:total], pre + "mask": mask, pre + "out": m.out, pre + "lse": m.lse})
+            k += 1
+    store["n_cases"] = np.array(k)
+    np.savez_compressed(os.path.join(OUT, "draft_attention.npz"), **store)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1:  # e.g. `make_golden.py gen_draft_attention`
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     gen_trees()
     gen_attention_f64()
     gen_attention_gqa()
     gen_accept()
     gen_philox()
     gen_compact()
+    gen_draft_attention()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -253,6 +253,53 @@ def tree_verify_attention_batch(q, k_pool, v_pool, block_table, ctx_len, tree_k,
     return out, lse
 
 
+def draft_depth_attention(q_new, committed_k, committed_v, suffix_k, suffix_v, mask_new, scale, n_heads,
+                          n_kv_heads=None):
+    """One depth step of the draft stage's tree attention (engine.py:424-432
+    -> model.py:257-270 with ``suffix_mask_new`` and ``carry_kv``): the new
+    nodes' queries attend the draft cache prefix (CausalPrefix: every
+    committed key) plus the suffix = carried K/V of the earlier nodes ++ the
+    new nodes' K/V under the rectangular visibility ``mask_new`` (n_new,
+    total), merged by LSE.  q_new (n_new, Hq*d); suffix_k/v (total, Hkv*d).
+    Returns (out (n_new, Hq*d), lse (Hq, n_new))."""
+    n_kv = n_heads if n_kv_heads is None else n_kv_heads
+    g = n_heads // n_kv
+    ck, cv = gqa_repeat(committed_k, n_kv, g), gqa_repeat(committed_v, n_kv, g)
+    sk, sv = gqa_repeat(suffix_k, n_kv, g), gqa_repeat(suffix_v, n_kv, g)
+    parts = []
+    if ck.shape[0] > 0:
+        parts.append(attend(q_new, ck, cv, None, scale, n_heads))
+    parts.append(attend(q_new, sk, sv, np.asarray(mask_new, dtype=bool), scale, n_heads))
+    return merge_partials(parts, n_heads)
+
+
+def draft_depth_attention_batch(q, k_pool, v_pool, block_table, ctx_len, suffix_k, suffix_v, parents, q_row0,
+                                scale):
+    """Batched oracle of the rectangular device call (``q_row0``): rows
+    [q_row0[b], len(parents[b])) of q (B, R, Hq, d) attend; suffix keys are
+    all realized nodes [0, len(parents[b])) with the ancestor-or-self mask of
+    the realized draft tree (engine.py:409-421 vis_rows).  Returns out / lse
+    arrays with only those rows filled (others NaN)."""
+    bsz, r_max, hq, d = q.shape
+    hkv = k_pool.shape[1]
+    out = np.full((bsz, r_max, hq, d), np.nan)
+    lse = np.full((bsz, hq, r_max), np.nan)
+    for b in range(bsz):
+        n, q0 = len(parents[b]), int(q_row0[b])
+        if q0 >= n:
+            continue
+        c = int(ctx_len[b])
+        ck = paged_gather(k_pool, block_table[b], c)
+        cv = paged_gather(v_pool, block_table[b], c)
+        mask = suffix_mask(parents[b])[q0:n]
+        o, l = draft_depth_attention(q[b, q0:n].reshape(n - q0, hq * d), ck, cv,
+                                     suffix_k[b, :n].reshape(n, hkv * d), suffix_v[b, :n].reshape(n, hkv * d),
+                                     mask, scale, hq, hkv)
+        out[b, q0:n] = o.reshape(n - q0, hq, d)
+        lse[b, :, q0:n] = l
+    return out, lse
+
+
 # ---------------------------------------------------------------------------
 # K4-K6: target distribution, acceptance, uniforms (numcore.py / sampling.py)
 # ---------------------------------------------------------------------------

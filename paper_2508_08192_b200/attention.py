@@ -245,7 +245,7 @@ class TreeVerifyAttention:
         self._ws = None
 
     def __call__(self, q, k_cache, v_cache, block_table, ctx_len, tree_k, tree_v, mask_words, n_rows, scale,
-                 out=None, lse=None, max_ctx=None, num_splits=0, kernel=KERNEL_AUTO, stream=None):
+                 out=None, lse=None, max_ctx=None, num_splits=0, kernel=KERNEL_AUTO, stream=None, q_row0=None):
         import torch
 
         b, r, hq, d = q.shape
@@ -275,6 +275,10 @@ class TreeVerifyAttention:
         a.block_size, a.num_blocks, a.max_blocks = bs, nb, block_table.shape[1]
         a.max_ctx = int(max_ctx) if max_ctx is not None else block_table.shape[1] * bs
         a.scale, a.dtype, a.num_splits, a.kernel = float(scale), dt, int(num_splits), int(kernel)
+        if q_row0 is not None:
+            if q_row0.dtype != torch.int32 or q_row0.shape != (b,):
+                raise AttentionError("q_row0 must be int32 [B]")
+            a.q_row0 = q_row0.data_ptr()
         lib = _lib.lib()
         need = lib.sdb_tree_attn_workspace(a)
         if need < 0:
@@ -299,3 +303,17 @@ def tree_verify_attention(*args, **kwargs):
     [B, R, Hkv, d]; mask_words int32 [B, R, W] (from drafttree.tree_build);
     n_rows int32 [B].  Returns (out [B, R, Hq, d], lse fp32 [B, Hq, R])."""
     return _default_launcher(*args, **kwargs)
+
+
+def draft_tree_attention(q, k_cache, v_cache, block_table, ctx_len, suffix_k, suffix_v, mask_words, n_rows, q_row0,
+                         scale, out=None, lse=None, **kw):
+    """One depth step of the draft stage's tree attention (engine.py:424-432,
+    model.py:257-270 with ``suffix_mask_new`` / ``carry_kv``), batched.
+
+    The realized draft nodes are rows [0, n_rows[b]) of ``suffix_k/v``
+    [B, R, Hkv, d] (carried K/V of earlier depths followed by this depth's new
+    nodes); the new nodes are rows [q_row0[b], n_rows[b]) of ``q`` [B, R, Hq,
+    d].  ``mask_words`` is ``tree_build`` of the realized parent array (the
+    engine's vis_rows).  Only rows >= q_row0 of out / lse are written."""
+    return _default_launcher(q, k_cache, v_cache, block_table, ctx_len, suffix_k, suffix_v, mask_words, n_rows,
+                             scale, out=out, lse=lse, q_row0=q_row0, **kw)

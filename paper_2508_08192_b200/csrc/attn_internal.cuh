@@ -8,6 +8,7 @@ namespace sdb {
 struct TreeAttnParams {
   const void *q, *k_cache, *v_cache, *tree_k, *tree_v;
   const int32_t *block_table, *ctx_len, *n_rows;
+  const int32_t *q_row0;  // [B] first query row (draft-side rectangular attention) or nullptr = 0
   const uint32_t *mask_words;
   void *out;
   float *lse;
@@ -17,6 +18,12 @@ struct TreeAttnParams {
   float scale;
   int num_splits;
 };
+
+// First query row of sequence b: rows [q0, n_rows) attend, keys are all the
+// tree rows [0, n_rows) (the draft stage's depth step, engine.py:424-432).
+__device__ __forceinline__ int q_first(const TreeAttnParams &p, int b, int n_nodes) {
+  return p.q_row0 ? min(max(p.q_row0[b], 0), n_nodes) : 0;
+}
 
 // Write one row's attention result: the final output when the KV range is
 // not split, otherwise the fp32 partial for the combine kernel.

@@ -123,15 +123,16 @@ __global__ void __launch_bounds__(kSimtWarps * 32) tree_attn_simt_kernel(TreeAtt
   const int b = blockIdx.z / p.hkv, kvh = blockIdx.z % p.hkv;
   const int g = p.hq / p.hkv;
   const int n_nodes = min(p.n_rows[b], p.r_max);
-  const int rows_total = n_nodes * g;
+  const int q0 = q_first(p, b, n_nodes);  // query rows: nodes [q0, n_nodes)
+  const int rows_total = (n_nodes - q0) * g;
   const int row0 = row_tile * kSimtRows;
   if (row0 >= rows_total) {
     // padding rows of an unsplit launch still get zeros / -inf
     if (p.num_splits == 1) {
       for (int r = warp; r < kSimtRows; r += kSimtWarps) {
         int rho = row0 + r;
-        if (rho < p.r_max * g)
-          store_partial<T>(p, 0, b, rho / g, kvh * g + rho % g, -INFINITY, [&](int) { return 0.f; }, lane);
+        if (q0 * g + rho < p.r_max * g)
+          store_partial<T>(p, 0, b, q0 + rho / g, kvh * g + rho % g, -INFINITY, [&](int) { return 0.f; }, lane);
       }
     }
     return;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) tree_attn_simt_kernel(TreeAtt
     int rho = row0 + r;
     float val = 0.f;
     if (rho < rows_total) {
-      int node = rho / g, j = rho % g;
+      int node = q0 + rho / g, j = rho % g;
       val = to_f32<T>(q[(((int64_t)b * p.r_max + node) * p.hq + kvh * g + j) * D + c]);
     }
     sQ[idx] = val;
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) tree_attn_simt_kernel(TreeAtt
       int rho = row0 + wrow0 + r;
       bool vis = key < T_keys && rho < rows_total;
       if (vis && key >= C) {
-        int node = rho / g, j = key - C;
+        int node = q0 + rho / g, j = key - C;
         uint32_t w = p.mask_words[((int64_t)b * p.r_max + node) * p.n_words + (j >> 5)];
         vis = (w >> (j & 31)) & 1u;
       }
@@ -245,11 +246,11 @@ __global__ void __launch_bounds__(kSimtWarps * 32) tree_attn_simt_kernel(TreeAtt
   for (int r = 0; r < kSimtRowsPerWarp; ++r) {
     int rho = row0 + wrow0 + r;
     if (rho >= rows_total) {
-      if (p.num_splits == 1 && rho < p.r_max * g)
-        store_partial<T>(p, 0, b, rho / g, kvh * g + rho % g, -INFINITY, [&](int) { return 0.f; }, lane);
+      if (p.num_splits == 1 && q0 * g + rho < p.r_max * g)
+        store_partial<T>(p, 0, b, q0 + rho / g, kvh * g + rho % g, -INFINITY, [&](int) { return 0.f; }, lane);
       continue;
     }
-    int node = rho / g, hq_idx = kvh * g + rho % g;
+    int node = q0 + rho / g, hq_idx = kvh * g + rho % g;
     float inv = l_r[r] > 0.f ? 1.f / l_r[r] : 0.f;
     float lse2 = l_r[r] > 0.f ? m_r[r] + log2f(l_r[r]) : -INFINITY;
     float lse_n = lse2 * 0.6931471805599453f;
@@ -271,6 +272,7 @@ __global__ void tree_attn_combine_kernel(TreeAttnParams p) {
   const int D = p.head_dim;
   T *out = reinterpret_cast<T *>(p.out) + (((int64_t)b * p.r_max + node) * p.hq + hq_idx) * D;
   const int n_nodes = min(p.n_rows[b], p.r_max);
+  if (node < q_first(p, b, n_nodes)) return;  // not a query row of this call
   if (node >= n_nodes) {
     for (int c = lane; c < D; c += 32) out[c] = from_f32<T>(0.f);
     if (p.lse && lane == 0) p.lse[((int64_t)b * p.hq + hq_idx) * p.r_max + node] = -INFINITY;

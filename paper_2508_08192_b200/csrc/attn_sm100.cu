@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
         mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
         mbar_expect_tx(&sm.q_full, NT * kTileBytes);
         for (int t = 0; t < NT; ++t) {
-          const int node0 = (geo.row0 + t * kTileM) / g;
+          const int node0 = geo.q0 + (geo.row0 + t * kTileM) / g;
           for (int c = 0; c < 2; ++c)
             tma_load_4d(sm.q[t] + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, 0, geo.kvh,
                         geo.b * p.r_max + node0);
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
       }
       const int rho = geo.row0 + local;
       const bool row_ok = rho < geo.rows_total;
-      const int node = min(rho / g, max(geo.n_nodes - 1, 0));
+      const int node = min(geo.q0 + rho / g, max(geo.n_nodes - 1, 0));
       const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
       float m = -INFINITY, l = 0.f;
       for (int it = 0; it < geo.n_tiles; ++it) {
@@ -294,12 +294,13 @@ __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params 
   const int bh = p.batch * p.hkv;
   const int b = (unit % bh) / p.hkv, kvh = unit % p.hkv;
   const int rho = (unit / bh) * sp.rows_unit + local;
-  if (rho >= p.r_max * g) return;
   const int n_nodes = min(p.n_rows[b], p.r_max);
-  const int node = rho / g, hq_idx = kvh * g + rho % g;
+  const int q0 = q_first(p, b, n_nodes);
+  if (q0 * g + rho >= p.r_max * g) return;
+  const int node = q0 + rho / g, hq_idx = kvh * g + rho % g;
   __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + (((int64_t)b * p.r_max + node) * p.hq + hq_idx) * kHeadDim;
   float *lse_out = p.lse ? p.lse + ((int64_t)b * p.hq + hq_idx) * p.r_max + node : nullptr;
-  if (rho >= n_nodes * g) {
+  if (rho >= (n_nodes - q0) * g) {
     *reinterpret_cast<uint2 *>(out + lane * 4) = make_uint2(0, 0);
     if (lse_out && lane == 0) *lse_out = -INFINITY;
     return;

@@ -202,8 +202,8 @@ __device__ __forceinline__ void epilogue_chunk(const Sm100Params &sp, const Item
   const TreeAttnParams &p = sp.p;
   const int rho = geo.row0 + local;
   const bool row_ok = rho < geo.rows_total;
-  const bool in_range = rho < p.r_max * g;
-  const int node_o = rho / g;
+  const bool in_range = geo.q0 * g + rho < p.r_max * g;
+  const int node_o = geo.q0 + rho / g;
   const int hq_idx = geo.kvh * g + (rho % g);
   const float inv = l_full > 0.f ? 1.f / l_full : 0.f;
   const float lse_n = l_full > 0.f ? (m + __log2f(l_full)) * 0.6931471805599453f : -INFINITY;
@@ -324,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         if (kprod) {
           mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
           if (rank == 0) mbar_expect_tx(&sm.q_full, 2 * kTileBytes);
-          const int node0 = (geo.row0 + (int)rank * kTileM) / g;
+          const int node0 = geo.q0 + (geo.row0 + (int)rank * kTileM) / g;
           for (int c = 0; c < 2; ++c)
             tma2_4d(sm.q + c * kChunkBytes, &tm_q, l_qfull, c * 64, 0, geo.kvh, geo.b * p.r_max + node0);
         }
@@ -471,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
       const int rho = geo.row0 + local;
       const bool row_ok = rho < geo.rows_total;
-      const int node = min(rho / g, max(geo.n_nodes - 1, 0));
+      const int node = min(geo.q0 + rho / g, max(geo.n_nodes - 1, 0));
       const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
       const int N = geo.n_tiles;
       float m_w = -INFINITY, l_w = 0.f;

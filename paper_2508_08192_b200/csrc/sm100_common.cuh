@@ -288,6 +288,7 @@ struct ItemIter {
 // Per-item geometry: which (b, kvh, rows) and which actual KV tiles.
 struct ItemGeo {
   int b, kvh, row0, n_nodes, rows_total, C;
+  int q0;  // first query node; query row rho is node q0 + rho / g
   int pa, n_pref, sa, n_suf, n_tiles;
   bool active;
 };
@@ -303,7 +304,8 @@ __device__ __forceinline__ ItemGeo item_geo(const Sm100Params &sp, const Item &i
   o.kvh = it.unit % p.hkv;
   o.row0 = (it.unit / bh) * sp.rows_unit;
   o.n_nodes = min(p.n_rows[o.b], p.r_max);
-  o.rows_total = o.n_nodes * g;
+  o.q0 = q_first(p, o.b, o.n_nodes);
+  o.rows_total = (o.n_nodes - o.q0) * g;
   o.C = p.ctx_len[o.b];
   const int pb = (o.C + kTileN - 1) / kTileN;
   const int sb = (o.n_nodes + kTileN - 1) / kTileN;
@@ -522,8 +524,8 @@ __device__ __forceinline__ void epilogue_half_row(const Sm100Params &sp, const I
   const TreeAttnParams &p = sp.p;
   const int rho = geo.row0 + local;
   const bool row_ok = rho < geo.rows_total;
-  const bool in_range = rho < p.r_max * g;
-  const int node_o = rho / g;
+  const bool in_range = geo.q0 * g + rho < p.r_max * g;
+  const int node_o = geo.q0 + rho / g;
   const int hq_idx = geo.kvh * g + (rho % g);
   const float inv = l_full > 0.f ? 1.f / l_full : 0.f;
   const float lse_n = l_full > 0.f ? (m + __log2f(l_full)) * 0.6931471805599453f : -INFINITY;
@@ -576,8 +578,8 @@ __device__ __forceinline__ void epilogue_row(const Sm100Params &sp, const Item &
   const TreeAttnParams &p = sp.p;
   const int rho = geo.row0 + local;
   const bool row_ok = rho < geo.rows_total;
-  const bool in_range = rho < p.r_max * g;
-  const int node_o = rho / g;
+  const bool in_range = geo.q0 * g + rho < p.r_max * g;
+  const int node_o = geo.q0 + rho / g;
   const int hq_idx = geo.kvh * g + (rho % g);
   const float inv = l > 0.f ? 1.f / l : 0.f;
   const float lse_n = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
@@ -630,8 +632,8 @@ __device__ __forceinline__ void inactive_row(const Sm100Params &sp, const Item &
     float *o = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim;
     for (int c = 0; c < kHeadDim; c += 4) *reinterpret_cast<float4 *>(o + c) = make_float4(0, 0, 0, 0);
     sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = -INFINITY;
-  } else if (rho < p.r_max * g) {
-    const int node_o = rho / g, hq_idx = geo.kvh * g + (rho % g);
+  } else if (geo.q0 * g + rho < p.r_max * g) {
+    const int node_o = geo.q0 + rho / g, hq_idx = geo.kvh * g + (rho % g);
     __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
                        (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim;
     for (int c = 0; c < kHeadDim; c += 8) *reinterpret_cast<uint4 *>(o + c) = make_uint4(0, 0, 0, 0);

@@ -26,6 +26,7 @@ static bool fill_params(const sdb_tree_attn_args *a, TreeAttnParams &p) {
   p.block_table = a->block_table;
   p.ctx_len = a->ctx_len;
   p.n_rows = a->n_rows;
+  p.q_row0 = a->q_row0;
   p.mask_words = a->mask_words;
   p.out = a->out;
   p.lse = a->lse;

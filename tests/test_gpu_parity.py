@@ -572,3 +572,70 @@ def test_tcgen05_single_cta_and_pair_kernels_agree(group, monkeypatch):
     err = np.abs(out.float().cpu().numpy() - want_o)
     assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
     assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
+
+
+# ---------------------------------------------------------------------------
+# Draft-side tree attention: the draft stage's depth step
+# -- new nodes attend prefix + carried/new suffix under a rectangular mask
+# ---------------------------------------------------------------------------
+
+def _depths(parent):
+    d = []
+    for p in parent:
+        d.append(1 if p < 0 else d[p] + 1)
+    return d
+
+
+@pytest.mark.parametrize("kernel,dtype,hq,hkv,d", [(1, torch.bfloat16, 64, 8, 128), (2, torch.bfloat16, 32, 8, 128),
+                                                    (2, torch.float32, 8, 2, 64)])
+def test_draft_depth_attention_vs_oracle(kernel, dtype, hq, hkv, d):
+    """Every depth of a realized draft tree (the 63-node EAGLE shape without
+    the root, plus a ragged chain) as one rectangular call per depth:
+    rows [q0, total) vs the float64 oracle of model.py:257-270; rows < q0
+    are left untouched."""
+    from paper_2508_08192_b200.attention import draft_tree_attention
+    from paper_2508_08192_b200.drafttree import tree_build
+
+    trees = [tuple(TREE64), (-1, 0, 1, 2, 3)]
+    B, bs = len(trees), 32
+    R = max(len(t) for t in trees)
+    rng = np.random.default_rng(7)
+    ctx = np.array([1500, 777], dtype=np.int32)
+    pages = -(-(int(ctx.max()) + 1) // bs)
+    nb = B * pages + 3
+    table = rng.permutation(nb)[:B * pages].reshape(B, pages).astype(np.int32)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    kp = torch.randn((nb, hkv, bs, d), generator=gen, device="cuda").to(dtype)
+    vp = torch.randn((nb, hkv, bs, d), generator=gen, device="cuda").to(dtype)
+    q = torch.randn((B, R, hq, d), generator=gen, device="cuda").to(dtype)
+    sk = torch.randn((B, R, hkv, d), generator=gen, device="cuda").to(dtype)
+    sv = torch.randn((B, R, hkv, d), generator=gen, device="cuda").to(dtype)
+    par = np.full((B, R), -1, dtype=np.int32)
+    for b, t in enumerate(trees):
+        par[b, :len(t)] = t
+    par_t = torch.tensor(par, device="cuda")
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    depths = [_depths(t) for t in trees]
+    tol_max, tol_mean, tol_lse = (2e-2, 2e-3, 2e-3) if dtype == torch.bfloat16 else (1e-4, 1e-5, 1e-5)
+    for depth in range(1, max(max(x) for x in depths) + 1):
+        # realized nodes so far and the first node of this depth, per sequence
+        total = [sum(1 for x in dp if x <= depth) for dp in depths]
+        q0 = [sum(1 for x in dp if x < depth) for dp in depths]
+        nr = torch.tensor(total, dtype=torch.int32, device="cuda")
+        q0_t = torch.tensor(q0, dtype=torch.int32, device="cuda")
+        mask, _, _, _ = tree_build(par_t, nr, torch.tensor(ctx, device="cuda"))
+        out = torch.full_like(q, 7.0)
+        lse = torch.full((B, hq, R), 7.0, device="cuda")
+        draft_tree_attention(q, kp, vp, torch.tensor(table, device="cuda"), torch.tensor(ctx, device="cuda"), sk, sv,
+                             mask, nr, q0_t, d ** -0.5, out=out, lse=lse, kernel=kernel)
+        torch.cuda.synchronize()
+        want_o, want_l = O.draft_depth_attention_batch(f64(q), f64(kp), f64(vp), table, ctx, f64(sk), f64(sv),
+                                                       [t[:total[b]] for b, t in enumerate(trees)], q0, d ** -0.5)
+        got_o, got_l = out.float().cpu().numpy(), lse.cpu().numpy()
+        for b in range(B):
+            assert (got_o[b, :q0[b]] == 7.0).all() and (got_l[b, :, :q0[b]] == 7.0).all(), (depth, b)
+            if q0[b] >= total[b]:
+                continue
+            e = np.abs(got_o[b, q0[b]:total[b]] - want_o[b, q0[b]:total[b]])
+            assert e.max() < tol_max and e.mean() < tol_mean, (depth, b, e.max(), e.mean())
+            assert np.abs(got_l[b, :, q0[b]:total[b]] - want_l[b, :, q0[b]:total[b]]).max() < tol_lse, (depth, b)

@@ -178,3 +178,20 @@ def test_compaction_matches_reference_cache(golden):
             n = L + kept - 1
             np.testing.assert_array_equal(O.paged_gather(kp, table, n), g[p + f"gk{li}"])
             np.testing.assert_array_equal(O.paged_gather(vp, table, n), g[p + f"gv{li}"])
+
+
+def test_draft_depth_attention_matches_reference(golden):
+    """Oracle of the draft stage's depth step (rectangular suffix mask over
+    carried ++ new K/V, engine.py:424-432) vs the reference's attend /
+    merge on the engine's own vis-row masks."""
+    g = golden("draft_attention")
+    for k in range(int(g["n_cases"])):
+        p = f"d{k}_"
+        hq, hkv, d, ctx, q0, total = (int(x) for x in g[p + "meta"])
+        # the vis rows the engine builds equal the realized tree's ancestor closure
+        parent = tuple(int(x) for x in g[p + "parent"])[:total]
+        np.testing.assert_array_equal(g[p + "mask"], O.suffix_mask(parent)[q0:total])
+        out, lse = O.draft_depth_attention(g[p + "q"], g[p + "ck"], g[p + "cv"], g[p + "sk"], g[p + "sv"],
+                                           g[p + "mask"], d ** -0.5, hq, hkv)
+        np.testing.assert_allclose(out, g[p + "out"], atol=1e-12)
+        np.testing.assert_allclose(lse, g[p + "lse"], atol=1e-12)

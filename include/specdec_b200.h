@@ -114,6 +114,8 @@ typedef struct sdb_tree_attn_args {
                                  The draft stage's depth step: new nodes attend
                                  the carried + new suffix under a rectangular
                                  mask (engine.py:424-432, model.py:265-270) */
+  int max_q_nodes;            /* host bound of n_rows - q_row0 over the batch
+                                 (sizes the work plan); 0 = r_max            */
 } sdb_tree_attn_args;
 
 int64_t sdb_tree_attn_workspace(const sdb_tree_attn_args *a);

@@ -43,7 +43,7 @@ class TreeAttnArgs(ctypes.Structure):
         ("batch", I32), ("r_max", I32), ("n_words", I32), ("hq", I32), ("hkv", I32), ("head_dim", I32),
         ("block_size", I32), ("num_blocks", I32), ("max_blocks", I32), ("max_ctx", I32),
         ("scale", F32), ("dtype", I32), ("num_splits", I32), ("kernel", I32),
-        ("q_row0", P),
+        ("q_row0", P), ("max_q_nodes", I32),
     ]
 
 

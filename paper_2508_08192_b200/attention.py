@@ -245,7 +245,8 @@ class TreeVerifyAttention:
         self._ws = None
 
     def __call__(self, q, k_cache, v_cache, block_table, ctx_len, tree_k, tree_v, mask_words, n_rows, scale,
-                 out=None, lse=None, max_ctx=None, num_splits=0, kernel=KERNEL_AUTO, stream=None, q_row0=None):
+                 out=None, lse=None, max_ctx=None, num_splits=0, kernel=KERNEL_AUTO, stream=None, q_row0=None,
+                 max_q_nodes=None):
         import torch
 
         b, r, hq, d = q.shape
@@ -279,6 +280,8 @@ class TreeVerifyAttention:
             if q_row0.dtype != torch.int32 or q_row0.shape != (b,):
                 raise AttentionError("q_row0 must be int32 [B]")
             a.q_row0 = q_row0.data_ptr()
+        if max_q_nodes is not None:
+            a.max_q_nodes = int(max_q_nodes)
         lib = _lib.lib()
         need = lib.sdb_tree_attn_workspace(a)
         if need < 0:
@@ -314,6 +317,9 @@ def draft_tree_attention(q, k_cache, v_cache, block_table, ctx_len, suffix_k, su
     [B, R, Hkv, d] (carried K/V of earlier depths followed by this depth's new
     nodes); the new nodes are rows [q_row0[b], n_rows[b]) of ``q`` [B, R, Hq,
     d].  ``mask_words`` is ``tree_build`` of the realized parent array (the
-    engine's vis_rows).  Only rows >= q_row0 of out / lse are written."""
+    engine's vis_rows).  Only rows >= q_row0 of out / lse are written.
+    ``max_q_nodes`` (host int, >= max over b of n_rows - q_row0, e.g. the
+    depth's node count of the tree shape) sizes the work plan to the new
+    rows instead of R."""
     return _default_launcher(q, k_cache, v_cache, block_table, ctx_len, suffix_k, suffix_v, mask_words, n_rows,
                              scale, out=out, lse=lse, q_row0=q_row0, **kw)

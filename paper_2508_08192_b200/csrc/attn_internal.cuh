@@ -15,6 +15,7 @@ struct TreeAttnParams {
   float *ws_out;  // [splits][B][r_max][hq][D]
   float *ws_lse;  // [splits][B][hq][r_max]
   int batch, r_max, n_words, hq, hkv, head_dim, block_size, num_blocks, max_blocks, max_ctx;
+  int max_q_nodes;  // query nodes per sequence (<= r_max); plans the row blocks
   float scale;
   int num_splits;
 };

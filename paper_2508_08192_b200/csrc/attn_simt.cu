@@ -307,7 +307,7 @@ template <typename T>
 int launch_tree_attn_simt(const TreeAttnParams &p, cudaStream_t stream) {
   if (p.head_dim % 4 != 0 || p.head_dim > 256) return SDB_E_UNSUPPORTED;
   const int g = p.hq / p.hkv;
-  const int row_tiles = cdiv(p.r_max * g, kSimtRows);
+  const int row_tiles = cdiv(p.max_q_nodes * g, kSimtRows);
   dim3 grid(p.num_splits, row_tiles, p.batch * p.hkv);
   const int D = p.head_dim;
   size_t smem = sizeof(float) * ((size_t)kSimtRows * D + (size_t)kSimtKeys * (D + 4) + (size_t)kSimtKeys * D +

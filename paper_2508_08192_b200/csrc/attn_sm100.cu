@@ -390,7 +390,7 @@ bool tree_attn_sm100_supported(const TreeAttnParams &p) {
 static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100Params &sp) {
   using namespace sm100;
   const int g = p.hq / p.hkv;
-  const int rows = p.r_max * g;
+  const int rows = p.max_q_nodes * g;  // query rows per (sequence, KV head)
   const char *fg = getenv("SDB_ATTN_CTA_GROUP");  // testing knob: force 1-CTA or pair kernels
   const int force_group = fg ? atoi(fg) : 0;
   sp.p = p;

@@ -7,7 +7,8 @@ namespace sdb {
 
 static int auto_splits(const sdb_tree_attn_args *a, int rows_per_cta) {
   const int g = a->hq / a->hkv;
-  const int row_tiles = cdiv(a->r_max * g, rows_per_cta);
+  const int qn = (a->max_q_nodes > 0 && a->max_q_nodes < a->r_max) ? a->max_q_nodes : a->r_max;
+  const int row_tiles = cdiv(qn * g, rows_per_cta);
   const int64_t units = (int64_t)a->batch * a->hkv * row_tiles;
   const int max_ctx = a->max_ctx > 0 ? a->max_ctx : a->max_blocks * a->block_size;
   const int target = 2 * num_sms();
@@ -27,6 +28,7 @@ static bool fill_params(const sdb_tree_attn_args *a, TreeAttnParams &p) {
   p.ctx_len = a->ctx_len;
   p.n_rows = a->n_rows;
   p.q_row0 = a->q_row0;
+  p.max_q_nodes = (a->max_q_nodes > 0 && a->max_q_nodes < a->r_max) ? a->max_q_nodes : a->r_max;
   p.mask_words = a->mask_words;
   p.out = a->out;
   p.lse = a->lse;

@@ -627,7 +627,8 @@ def test_draft_depth_attention_vs_oracle(kernel, dtype, hq, hkv, d):
         out = torch.full_like(q, 7.0)
         lse = torch.full((B, hq, R), 7.0, device="cuda")
         draft_tree_attention(q, kp, vp, torch.tensor(table, device="cuda"), torch.tensor(ctx, device="cuda"), sk, sv,
-                             mask, nr, q0_t, d ** -0.5, out=out, lse=lse, kernel=kernel)
+                             mask, nr, q0_t, d ** -0.5, out=out, lse=lse, kernel=kernel,
+                             max_q_nodes=max(t - z for t, z in zip(total, q0)) if depth % 2 else None)
         torch.cuda.synchronize()
         want_o, want_l = O.draft_depth_attention_batch(f64(q), f64(kp), f64(vp), table, ctx, f64(sk), f64(sv),
                                                        [t[:total[b]] for b, t in enumerate(trees)], q0, d ** -0.5)

@@ -101,3 +101,100 @@ def test_vocab_sharded_greedy_acceptance_gloo_world2():
         assert got == want, (rank, got, want)
     # every rank walks to the same result without a broadcast
     assert len({(tuple(r[3]), r[4], r[5]) for r in res}) == 1
+
+
+# ---------------------------------------------------------------------------
+# vocab-sharded stochastic acceptance: the phase/collective decomposition of
+# csrc/accept_sharded.cu, restated in numpy (oracle/sharded_accept.py), run
+# over real gloo collectives on CPU -- every rank must reproduce the unsharded
+# reference acceptance (target_dist + mss_verify).
+# ---------------------------------------------------------------------------
+
+class _GlooNumpyComm:
+    def __init__(self, rank, world):
+        self.rank, self.world = rank, world
+
+    def all_gather(self, a):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t)
+        return np.stack([o.numpy() for o in out])
+
+    def all_reduce_sum(self, a):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        dist.all_reduce(t)
+        return t.numpy()
+
+    def all_reduce_max(self, a):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.numpy()
+
+
+def _stoch_cases():
+    rng = np.random.default_rng(12)
+    cases = []
+    trees = [(-1, -1, 0, 0, 1, 2, 2, 5), (-1, 0, 1, 2), (-1, -1, -1, 0, 0, 0, 3)]
+    for ci in range(9):
+        parent = O.augment(trees[ci % 3])
+        R, V = len(parent), (203, 1000, 64)[ci % 3]
+        T, top_p = ((1.0, 0.9), (0.7, 0.95), (1.3, 1.0))[ci % 3]
+        if ci >= 6:  # integer logits: ties everywhere, also across the shard boundary
+            tl = rng.integers(-3, 4, size=(R, V)).astype(np.float32)
+            dl = np.where(rng.random((R, V)) < 0.7, tl, rng.integers(-3, 4, size=(R, V))).astype(np.float32)
+        else:
+            tl = (2.0 * rng.normal(size=(R, V))).astype(np.float32)
+            dl = (tl + 0.5 * rng.normal(size=(R, V))).astype(np.float32)
+        tokens = np.zeros(R, dtype=np.int64)
+        for i in range(1, R):
+            q = O.target_dist(dl[parent[i]].astype(np.float64), T, 1.0)
+            tokens[i] = O.sample_from(q, rng.random())
+        uni = O.rank_sliced_uniforms(77 + ci, 2 * ci + 2, 1, R)[0]
+        cases.append((parent, tl, dl, tokens, uni, T, top_p))
+    return cases
+
+
+def _want(case):
+    parent, tl, dl, tokens, uni, T, top_p = case
+    R = len(parent)
+    tdists = [O.target_dist(tl[r].astype(np.float64), T, top_p) for r in range(R)]
+    nd = [O.target_dist(dl[parent[i]].astype(np.float64), T, 1.0) for i in range(1, R)]
+    path, tok, _res, used = O.mss_verify(tuple(p - 1 if p > 0 else -1 for p in parent[1:]), tokens[1:], nd, tdists,
+                                         uni)
+    return list(path), int(tok), int(used)
+
+
+def _stoch_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.sharded_accept import sharded_accept
+
+        comm = _GlooNumpyComm(rank, world)
+        res = []
+        for parent, tl, dl, tokens, uni, T, top_p in _stoch_cases():
+            sh = shard_for(rank, world, world, world, tl.shape[1])
+            res.append(sharded_accept(comm, tl[:, sh.v_lo:sh.v_hi], dl[:, sh.v_lo:sh.v_hi], sh.v_lo, tl.shape[1],
+                                      parent, tokens, uni, T, top_p))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_vocab_sharded_stochastic_protocol_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stoch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [_want(c) for c in _stoch_cases()]
+    for rank, got in res:
+        for ci, (g, w) in enumerate(zip(got, want)):
+            assert (list(g[0]), g[1], g[2]) == w, (world, rank, ci, g, w)

@@ -144,7 +144,10 @@ int sdb_greedy_walk(const int64_t *keys, const int32_t *parent, const int32_t *n
                     int32_t *path_len, int64_t *next_token, int32_t *uniforms_used,
                     void *stream);
 
-/* Steps 1+2 fused in one launch (single GPU, unsharded vocab). */
+/* Steps 1+2 (single GPU, unsharded vocab).  keys is scratch of
+ * batch * r_max * SDB_GREEDY_KEY_SLOTS int64 (small batches split each
+ * row's vocabulary over several CTAs, one partial key each). */
+#define SDB_GREEDY_KEY_SLOTS 8
 int sdb_accept_greedy(const void *logits, int dtype, int batch, int r_max, int vocab,
                       int64_t row_stride, const int32_t *parent, const int32_t *n_rows,
                       const int32_t *tokens, int64_t *keys, int32_t *path, int32_t *path_len,

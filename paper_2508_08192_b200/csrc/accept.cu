@@ -18,6 +18,8 @@
 // engine.py:405-407), so each rejection costs one block-wide pass over the
 // vocab and the bonus draw one inverse-CDF pass.
 #include <float.h>
+
+#include <algorithm>
 #include <math.h>
 
 #include <cooperative_groups.h>
@@ -145,28 +147,36 @@ __device__ __forceinline__ void argmax_row(const T *__restrict__ row, int vocab,
   nan |= nacc != nacc;
 }
 
-// grid.x = rows (flat) or (r_max, batch) with n_rows gating.
+// grid.x = rows (flat) or (r_max * split, batch) with n_rows gating; with
+// split > 1 each row's vocabulary is cut into `split` segments (multiples of
+// 8 elements) scanned by separate CTAs, keys[row * split + s] (small batches:
+// enough CTAs to stream at HBM speed); the walk takes the max over segments.
 template <typename T>
 __global__ void __launch_bounds__(kArgmaxThreads, 2) argmax_keys_kernel(const T *__restrict__ logits, int vocab,
                                                                      int64_t row_stride, int64_t vocab_offset,
                                                                      const int32_t *__restrict__ n_rows,
                                                                      int r_max, long long *__restrict__ keys,
-                                                                     int32_t *__restrict__ err, bool vec_ok) {
+                                                                     int32_t *__restrict__ err, bool vec_ok,
+                                                                     int split) {
   __shared__ long long red[kArgmaxThreads / 32];
   int64_t row;
+  int seg = 0;
   if (n_rows) {
-    const int r = blockIdx.x, b = blockIdx.y;
+    const int r = blockIdx.x / split, b = blockIdx.y;
+    seg = blockIdx.x % split;
     if (r >= n_rows[b]) return;
     row = (int64_t)b * r_max + r;
   } else {
     row = blockIdx.x + (int64_t)blockIdx.y * gridDim.x;
   }
+  const int seg_len = split > 1 ? ((vocab + split - 1) / split + 7) & ~7 : vocab;
+  const int v0 = min(vocab, seg * seg_len), v1 = min(vocab, v0 + seg_len);
   long long best = LLONG_MIN;
   bool nan = false;
-  argmax_row<T>(logits + row * row_stride, vocab, vocab_offset, vec_ok, best, nan);
+  argmax_row<T>(logits + row * row_stride + v0, v1 - v0, vocab_offset + v0, vec_ok, best, nan);
   best = block_max_i64<kArgmaxThreads>(best, red);
   if (__syncthreads_or(nan) && threadIdx.x == 0 && err) atomicOr(err, SDB_ERR_NAN);
-  if (threadIdx.x == 0) keys[row] = best;
+  if (threadIdx.x == 0) keys[row * split + seg] = best;
 }
 
 // One warp per sequence: the argmax walk in the augmented frame (row 0 =
@@ -174,17 +184,23 @@ __global__ void __launch_bounds__(kArgmaxThreads, 2) argmax_keys_kernel(const T 
 __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int32_t *__restrict__ parent,
                                    const int32_t *__restrict__ n_rows, const int32_t *__restrict__ tokens,
                                    int batch, int r_max, int32_t *__restrict__ path, int32_t *__restrict__ path_len,
-                                   int64_t *__restrict__ next_token, int32_t *__restrict__ uniforms_used) {
+                                   int64_t *__restrict__ next_token, int32_t *__restrict__ uniforms_used,
+                                   int split) {
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= batch) return;
   const int n = min(n_rows[b], r_max);
   const int32_t *par = parent + (int64_t)b * r_max;
   const int32_t *tok = tokens + (int64_t)b * r_max;
-  const long long *key = keys + (int64_t)b * r_max;
+  const long long *key = keys + (int64_t)b * r_max * split;
+  auto row_key = [&](int r) {  // max over the row's vocabulary segments
+    long long k = key[(int64_t)r * split];
+    for (int s = 1; s < split; ++s) k = max(k, key[(int64_t)r * split + s]);
+    return k;
+  };
   int cur = 0, used = 0, len = 0;
   while (true) {
-    const int want = (int)key_index(key[cur]);
+    const int want = (int)key_index(row_key(cur));
     int accepted = -1, examined = 0;
     for (int j0 = cur + 1; j0 < n; j0 += 32) {
       const int j = j0 + lane;
@@ -208,7 +224,7 @@ __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int
   }
   if (lane == 0) {
     path_len[b] = len;
-    next_token[b] = (int64_t)key_index(key[cur]);
+    next_token[b] = (int64_t)key_index(row_key(cur));
     uniforms_used[b] = used + 1;
   }
 }
@@ -1082,11 +1098,11 @@ extern "C" int sdb_argmax_keys(const void *logits, int dtype, int64_t rows, int 
   if (dtype == SDB_DTYPE_F32)
     sdb::argmax_keys_kernel<float><<<grid, sdb::kArgmaxThreads, 0, s>>>(
         (const float *)logits, vocab, row_stride, vocab_offset, nullptr, 0, (long long *)keys, err,
-        vec_aligned(logits, row_stride, 4, vocab));
+        vec_aligned(logits, row_stride, 4, vocab), 1);
   else if (dtype == SDB_DTYPE_BF16)
     sdb::argmax_keys_kernel<__nv_bfloat16><<<grid, sdb::kArgmaxThreads, 0, s>>>(
         (const __nv_bfloat16 *)logits, vocab, row_stride, vocab_offset, nullptr, 0, (long long *)keys, err,
-        vec_aligned(logits, row_stride, 2, vocab));
+        vec_aligned(logits, row_stride, 2, vocab), 1);
   else
     return SDB_E_UNSUPPORTED;
   SDB_CHECK_LAUNCH();
@@ -1101,7 +1117,7 @@ extern "C" int sdb_greedy_walk(const int64_t *keys, const int32_t *parent, const
     return SDB_E_INVALID;
   if (batch == 0) return SDB_OK;
   sdb::greedy_walk_kernel<<<sdb::cdiv(batch * 32, 128), 128, 0, sdb::as_stream(stream)>>>(
-      (const long long *)keys, parent, n_rows, tokens, batch, r_max, path, path_len, next_token, uniforms_used);
+      (const long long *)keys, parent, n_rows, tokens, batch, r_max, path, path_len, next_token, uniforms_used, 1);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
@@ -1114,21 +1130,28 @@ extern "C" int sdb_accept_greedy(const void *logits, int dtype, int batch, int r
       row_stride < vocab)
     return SDB_E_INVALID;
   if (batch == 0) return SDB_OK;
-  dim3 grid(r_max, batch);
+  // small batches: cut each row's vocabulary over several CTAs (>= 4096
+  // elements each) so that ~4 CTAs per SM stream the logits
+  const int64_t rows = (int64_t)batch * r_max;
+  int split = (int)std::min<int64_t>(SDB_GREEDY_KEY_SLOTS, std::max<int64_t>(1, (sdb::num_sms() + rows - 1) / rows));
+  split = std::max(1, std::min(split, vocab / 16384));
+  dim3 grid(r_max * split, batch);
   cudaStream_t s = sdb::as_stream(stream);
   if (dtype == SDB_DTYPE_F32)
     sdb::argmax_keys_kernel<float><<<grid, sdb::kArgmaxThreads, 0, s>>>(
         (const float *)logits, vocab, row_stride, 0, n_rows, r_max, (long long *)keys, err,
-        vec_aligned(logits, row_stride, 4, vocab));
+        vec_aligned(logits, row_stride, 4, vocab), split);
   else if (dtype == SDB_DTYPE_BF16)
     sdb::argmax_keys_kernel<__nv_bfloat16><<<grid, sdb::kArgmaxThreads, 0, s>>>(
         (const __nv_bfloat16 *)logits, vocab, row_stride, 0, n_rows, r_max, (long long *)keys, err,
-        vec_aligned(logits, row_stride, 2, vocab));
+        vec_aligned(logits, row_stride, 2, vocab), split);
   else
     return SDB_E_UNSUPPORTED;
   SDB_CHECK_LAUNCH();
-  return sdb_greedy_walk(keys, parent, n_rows, tokens, batch, r_max, path, path_len, next_token, uniforms_used,
-                         stream);
+  sdb::greedy_walk_kernel<<<sdb::cdiv(batch * 32, 128), 128, 0, s>>>(
+      (const long long *)keys, parent, n_rows, tokens, batch, r_max, path, path_len, next_token, uniforms_used, split);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
 }
 
 extern "C" int64_t sdb_accept_stochastic_workspace(int batch, int r_max, int vocab) {

@@ -405,8 +405,10 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   sp.w_unit = sp.w_pref + cdiv(p.r_max, kTileN);
   sp.total = (int64_t)sp.units * sp.w_unit;
   int n = ctas_override > 0 ? ctas_override : num_sms() / sp.cta_group;
-  // at least ~2 tiles per worker
-  n = (int)std::max<int64_t>(1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : sp.total / 2));
+  // at least ~16 tiles per worker: small batches (bs 1) then leave SMs free
+  // for the acceptance branch running concurrently (verify.TreeVerifier.step)
+  // at no cost -- their time is set by the per-unit pipeline latency
+  n = (int)std::max<int64_t>(1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : sp.total / 16));
   sp.n_workers = n;
   sp.part_out = nullptr;
   sp.part_lse = nullptr;

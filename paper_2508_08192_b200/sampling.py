@@ -217,7 +217,7 @@ class GreedyAcceptor:
         key = (b, r, str(dev))
         if self._bufs is None or self._bufs[0] != key:
             self._bufs = (key, dict(
-                keys=torch.empty((b, r), dtype=torch.int64, device=dev),
+                keys=torch.empty((b, r, 8), dtype=torch.int64, device=dev),  # SDB_GREEDY_KEY_SLOTS
                 path=torch.zeros((b, r), dtype=torch.int32, device=dev),
                 path_len=torch.empty((b,), dtype=torch.int32, device=dev),
                 next_token=torch.empty((b,), dtype=torch.int64, device=dev),

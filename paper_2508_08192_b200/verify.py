@@ -54,6 +54,7 @@ class TreeVerifier:
         self.greedy = GreedyAcceptor()
         self.stochastic = StochasticAcceptor()
         self._out = None
+        self._side = None
         self.graph = None
 
     def _buffers(self, x: StepInputs):
@@ -73,25 +74,46 @@ class TreeVerifier:
                 lse=torch.empty((b, hq, r), dtype=torch.float32, device=dev)))
         return self._out[1]
 
-    def step(self, x: StepInputs, stream=None, compact=True):
+    def step(self, x: StepInputs, stream=None, compact=True, overlap=True):
+        """One verification step.  Attention (tree_build -> attention) and
+        acceptance (-> compaction) do not depend on each other, so with
+        ``overlap`` they run as two branches (side stream forked from and
+        joined back into ``stream``; captured as parallel graph branches):
+        at small batches the attention leaves SMs idle that the acceptance
+        kernels use."""
+        import torch
+
         o = self._buffers(x)
         b, r = x.parent.shape
         lib = _lib.lib()
+        main = stream if stream is not None else torch.cuda.current_stream()
+        side = main
+        if overlap:
+            if self._side is None or self._side.device != main.device:
+                self._side = torch.cuda.Stream(device=main.device)
+            side = self._side
+            side.wait_stream(main)
         rc = lib.sdb_tree_build(_lib.ptr(x.parent), _lib.ptr(x.n_rows), _lib.ptr(x.ctx_len), b, r,
                                 o["mask"].shape[-1], _lib.ptr(o["mask"]), _lib.ptr(o["pos"]), _lib.ptr(o["depth"]),
-                                _lib.ptr(o["tree_err"]), _lib.stream_ptr(stream))
+                                _lib.ptr(o["tree_err"]), _lib.stream_ptr(main))
         _lib.check(rc, "tree_build")
         self.attn(x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
                   self.scale, out=o["out"], lse=o["lse"], max_ctx=self.max_ctx, num_splits=self.num_splits,
-                  kernel=self.kernel, stream=stream)
-        if self.temperature == 0:
-            acc = self.greedy(x.logits, x.parent, x.n_rows, x.tokens, stream=stream)
-        else:
-            acc = self.stochastic(x.logits, x.draft_logits, self.temperature, self.top_p, x.parent, x.n_rows,
-                                  x.tokens, x.uniforms, stream=stream, seeds=x.seeds, steps=x.steps)
-        if compact:
-            compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0), x.v_pool.unsqueeze(0),
-                       x.block_table, x.ctx_len, acc.path, acc.path_len, None, stream=stream)
+                  kernel=self.kernel, stream=main)
+        with torch.cuda.stream(side):
+            if self.temperature == 0:
+                acc = self.greedy(x.logits, x.parent, x.n_rows, x.tokens, stream=side)
+            else:
+                acc = self.stochastic(x.logits, x.draft_logits, self.temperature, self.top_p, x.parent, x.n_rows,
+                                      x.tokens, x.uniforms, stream=side, seeds=x.seeds, steps=x.steps)
+            if compact:
+                # writes cache rows >= ctx_len only: disjoint from what the
+                # attention reads (prefix keys < ctx_len are the only unmasked ones)
+                compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0),
+                           x.v_pool.unsqueeze(0), x.block_table, x.ctx_len, acc.path, acc.path_len, None,
+                           stream=side)
+        if side is not main:
+            main.wait_stream(side)
         return o["out"], o["lse"], acc, o["tree_err"]
 
     # kernel launches per step (for the bench's gpu_launches claim)

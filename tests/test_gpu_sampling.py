@@ -258,3 +258,34 @@ def test_sharded_stochastic_two_processes_gloo():
             uni = O.rank_sliced_uniforms(seeds[b], steps[b], 1, R)[0]
             want = _oracle_accept(aug, tl[b], dl[b], tokens[b], uni, T, top_p)
             assert list(path[b, :plen[b]]) == list(want[0]) and nxt[b] == want[1] and used[b] == want[3], (rank, b)
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_accept_greedy_small_batch_split_rows_vs_oracle(B):
+    """bs 1-3 at V = 128,256: each row's vocabulary is scanned by several CTAs
+    (partial keys); ties planted across segment boundaries must resolve to
+    the lowest index, NaN-free rows bit-exact vs the oracle walk."""
+    from paper_2508_08192_b200.sampling import accept_greedy
+
+    V = 128256
+    rng = np.random.default_rng(41 + B)
+    aug = O.augment(tuple(TREE64))
+    R = len(aug)
+    lg = (2.0 * rng.normal(size=(B, R, V))).astype(np.float32)
+    for b in range(B):
+        for r in range(0, R, 3):  # tie of the row max in two far-apart segments
+            i, j = sorted(rng.choice(V, size=2, replace=False))
+            lg[b, r, i] = lg[b, r, j] = 50.0
+    am = lg.argmax(axis=-1)
+    tokens = np.zeros((B, R), dtype=np.int32)
+    for b in range(B):
+        for i in range(1, R):
+            tokens[b, i] = am[b, aug[i]] if rng.random() < 0.7 else rng.integers(V)
+    res = accept_greedy(torch.tensor(lg, device="cuda"), torch.tensor([aug] * B, dtype=torch.int32, device="cuda"),
+                        torch.full((B,), R, dtype=torch.int32, device="cuda"), torch.tensor(tokens, device="cuda"))
+    torch.cuda.synchronize()
+    for b in range(B):
+        path, nxt, used = O.greedy_walk(tuple(p - 1 if p > 0 else -1 for p in aug[1:]), tokens[b, 1:], am[b])
+        plen = int(res.path_len[b])
+        assert res.path[b, :plen].cpu().tolist() == list(path)
+        assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used

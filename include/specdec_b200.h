@@ -116,9 +116,19 @@ typedef struct sdb_tree_attn_args {
                                  mask (engine.py:424-432, model.py:265-270) */
   int max_q_nodes;            /* host bound of n_rows - q_row0 over the batch
                                  (sizes the work plan); 0 = r_max            */
+  int flags;                  /* SDB_ATTN_FLAG_*                              */
 } sdb_tree_attn_args;
 
+/* The kernel launched just before on the stream is sdb_tree_build (the only
+ * producer of mask_words this call must wait for): launch the tcgen05 kernel
+ * as its programmatic dependent, so its prologue and K/V streaming overlap
+ * tree_build (sm_100 PDL; captured as a programmatic graph edge). */
+#define SDB_ATTN_FLAG_PDL 1
+
 int64_t sdb_tree_attn_workspace(const sdb_tree_attn_args *a);
+/* SMs the launch plan of these arguments occupies (the persistent grid);
+ * callers that run independent work concurrently (acceptance) use the rest. */
+int sdb_tree_attn_sms(const sdb_tree_attn_args *a);
 int sdb_tree_attn(const sdb_tree_attn_args *a, void *stream);
 
 /* ---- K4/K5: greedy (T = 0) acceptance ----------------------------------

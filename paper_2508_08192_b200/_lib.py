@@ -22,6 +22,8 @@ SDB_ERR_UNIFORMS = 8
 SDB_ERR_ALL_MASKED = 16
 SDB_ERR_NO_ALLOWED = 32
 
+ATTN_FLAG_PDL = 1
+
 DTYPE_BF16 = 0
 DTYPE_F32 = 1
 DTYPE_F64 = 2
@@ -43,7 +45,7 @@ class TreeAttnArgs(ctypes.Structure):
         ("batch", I32), ("r_max", I32), ("n_words", I32), ("hq", I32), ("hkv", I32), ("head_dim", I32),
         ("block_size", I32), ("num_blocks", I32), ("max_blocks", I32), ("max_ctx", I32),
         ("scale", F32), ("dtype", I32), ("num_splits", I32), ("kernel", I32),
-        ("q_row0", P), ("max_q_nodes", I32),
+        ("q_row0", P), ("max_q_nodes", I32), ("flags", I32),
     ]
 
 
@@ -83,6 +85,7 @@ _SIGNATURES = {
     "sdb_merge_partials_f64": (I32, [P, P, I32, I32, I32, I32, P, P, P, P]),
     "sdb_tree_attn_workspace": (I64, [ctypes.POINTER(TreeAttnArgs)]),
     "sdb_tree_attn": (I32, [ctypes.POINTER(TreeAttnArgs), P]),
+    "sdb_tree_attn_sms": (I32, [ctypes.POINTER(TreeAttnArgs)]),
     "sdb_argmax_keys": (I32, [P, I32, I64, I32, I64, I64, P, P, P]),
     "sdb_greedy_walk": (I32, [P, P, P, P, I32, I32, P, P, P, P, P]),
     "sdb_accept_greedy": (I32, [P, I32, I32, I32, I32, I64, P, P, P, P, P, P, P, P, P, P]),

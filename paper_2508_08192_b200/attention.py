@@ -243,10 +243,11 @@ class TreeVerifyAttention:
 
     def __init__(self):
         self._ws = None
+        self.last_sms = None
 
     def __call__(self, q, k_cache, v_cache, block_table, ctx_len, tree_k, tree_v, mask_words, n_rows, scale,
                  out=None, lse=None, max_ctx=None, num_splits=0, kernel=KERNEL_AUTO, stream=None, q_row0=None,
-                 max_q_nodes=None):
+                 max_q_nodes=None, after_tree_build=False):
         import torch
 
         b, r, hq, d = q.shape
@@ -282,7 +283,10 @@ class TreeVerifyAttention:
             a.q_row0 = q_row0.data_ptr()
         if max_q_nodes is not None:
             a.max_q_nodes = int(max_q_nodes)
+        if after_tree_build:  # the previous kernel on `stream` is tree_build: PDL launch
+            a.flags |= _lib.ATTN_FLAG_PDL
         lib = _lib.lib()
+        self.last_sms = lib.sdb_tree_attn_sms(a)  # SMs this launch occupies (verify.TreeVerifier overlap)
         need = lib.sdb_tree_attn_workspace(a)
         if need < 0:
             _lib.check(int(need), "tree_verify_attention(workspace)")

@@ -16,6 +16,7 @@ struct TreeAttnParams {
   float *ws_lse;  // [splits][B][hq][r_max]
   int batch, r_max, n_words, hq, hkv, head_dim, block_size, num_blocks, max_blocks, max_ctx;
   int max_q_nodes;  // query nodes per sequence (<= r_max); plans the row blocks
+  int pdl;          // launch the tcgen05 kernel as a programmatic dependent of the previous kernel
   float scale;
   int num_splits;
 };
@@ -54,6 +55,7 @@ int launch_tree_attn_simt(const TreeAttnParams &p, cudaStream_t stream);
 int launch_tree_attn_combine_bf16(const TreeAttnParams &p, cudaStream_t stream);
 int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *workspace, cudaStream_t stream);
 int64_t tree_attn_sm100_workspace(const TreeAttnParams &p, int ctas_override);
+int tree_attn_sm100_sms(const TreeAttnParams &p, int ctas_override);
 bool tree_attn_sm100_supported(const TreeAttnParams &p);
 
 }  // namespace sdb

@@ -227,6 +227,10 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
     }
   } else if (warp >= 4) {
     // ===================== softmax warpgroups =====================
+    // programmatic dependent launch: the mask words come from the kernel
+    // launched just before (tree_build); everything else in flight above
+    // (TMEM alloc, TMA of Q/K/V, first QK^T) already overlaps its tail
+    griddep_wait();
     const int t = (warp - 4) >> 2;          // query tile
     const int i = ((warp & 3) << 5) + lane;  // row within tile == TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -422,6 +426,12 @@ int64_t tree_attn_sm100_workspace(const TreeAttnParams &p, int ctas_override) {
          (int64_t)(sp.n_workers + 1) * 8 + 256;
 }
 
+int tree_attn_sm100_sms(const TreeAttnParams &p, int ctas_override) {
+  sm100::Sm100Params sp;
+  sm100_plan(p, ctas_override, sp);
+  return sp.n_workers * sp.cta_group;
+}
+
 int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *workspace, cudaStream_t stream) {
   using namespace sm100;
   const int g = p.hq / p.hkv;
@@ -473,11 +483,21 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *wor
     if (rc != SDB_OK) return rc;
   } else {
     dim3 grid(sp.n_workers);
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
 #define SDB_LAUNCH_TC(NT, EMU)                                                                               \
   do {                                                                                                       \
     const size_t smem = sizeof(Smem<NT>) + 1024;                                                             \
     cudaFuncSetAttribute(tree_attn_tcgen05_kernel<NT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    tree_attn_tcgen05_kernel<NT, EMU><<<grid, 128 + NT * 128, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);   \
+    cudaLaunchConfig_t cfg = {};                                                                             \
+    cfg.gridDim = grid;                                                                                      \
+    cfg.blockDim = dim3(128 + NT * 128);                                                                     \
+    cfg.dynamicSmemBytes = smem;                                                                             \
+    cfg.stream = stream;                                                                                     \
+    cfg.attrs = &attr;                                                                                       \
+    cfg.numAttrs = sp.p.pdl ? 1 : 0;                                                                         \
+    cudaLaunchKernelEx(&cfg, tree_attn_tcgen05_kernel<NT, EMU>, mq, mk, mv, mtk, mtv, sp);                   \
   } while (0)
     if (sp.nt == 2) {
       if (emu == 0) SDB_LAUNCH_TC(2, 0); else if (emu == 2) SDB_LAUNCH_TC(2, 2); else SDB_LAUNCH_TC(2, 1);

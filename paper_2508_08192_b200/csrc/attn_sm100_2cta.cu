@@ -451,6 +451,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
     }
   } else if (warp >= 4) {
+    // programmatic dependent launch: the mask words come from the kernel
+    // launched just before (tree_build); everything else in flight above
+    // (TMEM alloc, TMA of Q/K/V, first QK^T) already overlaps its tail
+    griddep_wait();
     // ===================== softmax: 3 warpgroups, one row per thread ===========
     const int wg = (warp - 4) >> 2;
     const int lg = warp & 3;         // TMEM lane group (warp % 4 by hardware rule)
@@ -623,11 +627,21 @@ int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap 
                 const CUtensorMap &mtv, const Sm100Params &sp, int emu, cudaStream_t stream) {
   dim3 grid(sp.n_workers * 2);
   const size_t smem = sizeof(Smem2) + 1024;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kPairThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = sp.p.pdl ? 1 : 0;
 #define SDB_LAUNCH_PAIR(EMU8)                                                                                      \
   do {                                                                                                             \
     cudaFuncSetAttribute(tree_attn_tcgen05_pair_kernel<EMU8>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                          (int)smem);                                                                               \
-    tree_attn_tcgen05_pair_kernel<EMU8><<<grid, kPairThreads, smem, stream>>>(mq, mk, mv, mtk, mtv, sp);         \
+    cudaLaunchKernelEx(&cfg, tree_attn_tcgen05_pair_kernel<EMU8>, mq, mk, mv, mtk, mtv, sp);                      \
   } while (0)
   // emu: pairs of every 8 whose exp2 runs on the FMA pipe
   switch (emu) {

@@ -162,6 +162,16 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return r;
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// wait for the upstream kernel's completion + memory flush (no-op when the
+// kernel was launched without the programmatic-serialization attribute)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the downstream PDL kernel start launching (its CTAs run their
+// prologue until their own griddep_wait)
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- packed fp32x2 math (FFMA2 / FADD2) and 3-input max (FMNMX3), sm_100 ----
 __device__ __forceinline__ uint64_t f2pack(float a, float b) {
   uint64_t r;

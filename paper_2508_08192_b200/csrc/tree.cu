@@ -20,6 +20,8 @@ __global__ void __launch_bounds__(128) tree_build_kernel(
     uint32_t *__restrict__ mask_words, int32_t *__restrict__ positions,
     int32_t *__restrict__ depth_out, int32_t *__restrict__ err) {
   extern __shared__ int32_t smem_par[];  // [warps][r_max]
+  // a programmatic-dependent attention launch may start its prologue now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + warp;
   if (b >= batch) return;

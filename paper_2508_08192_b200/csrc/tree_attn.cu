@@ -29,6 +29,7 @@ static bool fill_params(const sdb_tree_attn_args *a, TreeAttnParams &p) {
   p.n_rows = a->n_rows;
   p.q_row0 = a->q_row0;
   p.max_q_nodes = (a->max_q_nodes > 0 && a->max_q_nodes < a->r_max) ? a->max_q_nodes : a->r_max;
+  p.pdl = (a->flags & SDB_ATTN_FLAG_PDL) != 0;
   p.mask_words = a->mask_words;
   p.out = a->out;
   p.lse = a->lse;
@@ -84,6 +85,15 @@ extern "C" int64_t sdb_tree_attn_workspace(const sdb_tree_attn_args *a) {
   int rc = sdb::resolve(a, p, sm100);
   if (rc != SDB_OK) return rc;
   return sdb::workspace_for(p, sm100, a->num_splits);
+}
+
+extern "C" int sdb_tree_attn_sms(const sdb_tree_attn_args *a) {
+  sdb::TreeAttnParams p;
+  bool sm100 = false;
+  int rc = sdb::resolve(a, p, sm100);
+  if (rc != SDB_OK) return rc;
+  if (sm100) return sdb::tree_attn_sm100_sms(p, a->num_splits);
+  return sdb::num_sms();  // SIMT: a full-device grid
 }
 
 extern "C" int sdb_tree_attn(const sdb_tree_attn_args *a, void *stream) {

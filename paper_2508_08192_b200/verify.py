@@ -42,6 +42,17 @@ class StepInputs:
     steps: "object" = None         # int64 [B]
 
 
+_SMS = {}
+
+
+def _num_sms(device):
+    import torch
+
+    if device not in _SMS:
+        _SMS[device] = torch.cuda.get_device_properties(device).multi_processor_count
+    return _SMS[device]
+
+
 class TreeVerifier:
     def __init__(self, scale, temperature=0.0, top_p=1.0, max_ctx=None, num_splits=0, kernel=0):
         self.scale = scale
@@ -87,19 +98,24 @@ class TreeVerifier:
         b, r = x.parent.shape
         lib = _lib.lib()
         main = stream if stream is not None else torch.cuda.current_stream()
-        side = main
-        if overlap:
-            if self._side is None or self._side.device != main.device:
-                self._side = torch.cuda.Stream(device=main.device)
-            side = self._side
-            side.wait_stream(main)
+        fork = torch.cuda.Event()
+        fork.record(main)
         rc = lib.sdb_tree_build(_lib.ptr(x.parent), _lib.ptr(x.n_rows), _lib.ptr(x.ctx_len), b, r,
                                 o["mask"].shape[-1], _lib.ptr(o["mask"]), _lib.ptr(o["pos"]), _lib.ptr(o["depth"]),
                                 _lib.ptr(o["tree_err"]), _lib.stream_ptr(main))
         _lib.check(rc, "tree_build")
         self.attn(x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
                   self.scale, out=o["out"], lse=o["lse"], max_ctx=self.max_ctx, num_splits=self.num_splits,
-                  kernel=self.kernel, stream=main)
+                  kernel=self.kernel, stream=main, after_tree_build=True)
+        # overlap only when the attention's persistent grid leaves SMs free
+        # (small batches); at full occupancy the acceptance CTAs would delay
+        # the attention's workers instead
+        side = main
+        if overlap and self.attn.last_sms is not None and self.attn.last_sms + 16 <= _num_sms(main.device):
+            if self._side is None or self._side.device != main.device:
+                self._side = torch.cuda.Stream(device=main.device)
+            side = self._side
+            side.wait_event(fork)
         with torch.cuda.stream(side):
             if self.temperature == 0:
                 acc = self.greedy(x.logits, x.parent, x.n_rows, x.tokens, stream=side)

@@ -117,6 +117,17 @@ typedef struct sdb_tree_attn_args {
   int max_q_nodes;            /* host bound of n_rows - q_row0 over the batch
                                  (sizes the work plan); 0 = r_max            */
   int flags;                  /* SDB_ATTN_FLAG_*                              */
+  /* optional fused greedy-acceptance scan (sdb_argmax_keys semantics over the
+   * flat rows [batch * r_max] of fp32 logits): when fused_keys is set, the
+   * call also produces keys[b * r_max + r] -- inside the CTA-pair attention
+   * kernel (an otherwise idle warp streams the logits through TMA while the
+   * tensor pipe works), else by a separate launch after it.  Feed the keys
+   * to sdb_greedy_walk (replaces argmax_keys_kernel of sdb_accept_greedy). */
+  const float *fused_logits;  /* [batch][r_max][row_stride], this rank's vocab slice */
+  int64_t fused_row_stride, fused_vocab_offset;
+  int fused_vocab;
+  int64_t *fused_keys;        /* [batch * r_max]                              */
+  int32_t *fused_err;         /* NaN -> SDB_ERR_NAN                           */
 } sdb_tree_attn_args;
 
 /* The kernel launched just before on the stream is sdb_tree_build (the only

@@ -46,6 +46,8 @@ class TreeAttnArgs(ctypes.Structure):
         ("block_size", I32), ("num_blocks", I32), ("max_blocks", I32), ("max_ctx", I32),
         ("scale", F32), ("dtype", I32), ("num_splits", I32), ("kernel", I32),
         ("q_row0", P), ("max_q_nodes", I32), ("flags", I32),
+        ("fused_logits", P), ("fused_row_stride", I64), ("fused_vocab_offset", I64), ("fused_vocab", I32),
+        ("fused_keys", P), ("fused_err", P),
     ]
 
 

@@ -245,9 +245,9 @@ class TreeVerifyAttention:
         self._ws = None
         self.last_sms = None
 
-    def __call__(self, q, k_cache, v_cache, block_table, ctx_len, tree_k, tree_v, mask_words, n_rows, scale,
+    def _args(self, q, k_cache, v_cache, block_table, ctx_len, tree_k, tree_v, mask_words, n_rows, scale,
                  out=None, lse=None, max_ctx=None, num_splits=0, kernel=KERNEL_AUTO, stream=None, q_row0=None,
-                 max_q_nodes=None, after_tree_build=False):
+                 max_q_nodes=None, after_tree_build=False, fused_argmax=None):
         import torch
 
         b, r, hq, d = q.shape
@@ -285,6 +285,26 @@ class TreeVerifyAttention:
             a.max_q_nodes = int(max_q_nodes)
         if after_tree_build:  # the previous kernel on `stream` is tree_build: PDL launch
             a.flags |= _lib.ATTN_FLAG_PDL
+        if fused_argmax is not None:
+            # (logits fp32 [B, R, V_local] (unit vocab stride), keys int64 [B*R], err int32 [1], vocab_offset)
+            lg, keys, err, voff = fused_argmax
+            if lg.dtype != torch.float32 or lg.stride(2) != 1 or lg.shape[:2] != (b, r):
+                raise AttentionError("fused argmax: logits must be fp32 [B, R, V] with unit vocab stride")
+            a.fused_logits, a.fused_row_stride, a.fused_vocab = lg.data_ptr(), lg.stride(1), lg.shape[2]
+            a.fused_vocab_offset, a.fused_keys, a.fused_err = int(voff), keys.data_ptr(), err.data_ptr()
+        return a, out, lse
+
+    def sms(self, *args, **kw):
+        """SMs the launch plan of this call would occupy (no launch)."""
+        a, _, _ = self._args(*args, **kw)
+        return _lib.lib().sdb_tree_attn_sms(a)
+
+    def __call__(self, *args, **kw):
+        import torch
+
+        a, out, lse = self._args(*args, **kw)
+        q = args[0]
+        stream = kw.get("stream")
         lib = _lib.lib()
         self.last_sms = lib.sdb_tree_attn_sms(a)  # SMs this launch occupies (verify.TreeVerifier overlap)
         need = lib.sdb_tree_attn_workspace(a)

@@ -17,6 +17,13 @@ struct TreeAttnParams {
   int batch, r_max, n_words, hq, hkv, head_dim, block_size, num_blocks, max_blocks, max_ctx;
   int max_q_nodes;  // query nodes per sequence (<= r_max); plans the row blocks
   int pdl;          // launch the tcgen05 kernel as a programmatic dependent of the previous kernel
+  // fused greedy-acceptance scan (idle warp of the pair kernel): packed
+  // argmax keys of the fp32 logits rows [B][r_max][vocab] (n_rows gated)
+  const float *fa_logits;
+  int64_t fa_row_stride, fa_vocab_offset;
+  int fa_vocab;
+  long long *fa_keys;
+  int32_t *fa_err;
   float scale;
   int num_splits;
 };
@@ -56,6 +63,7 @@ int launch_tree_attn_combine_bf16(const TreeAttnParams &p, cudaStream_t stream);
 int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *workspace, cudaStream_t stream);
 int64_t tree_attn_sm100_workspace(const TreeAttnParams &p, int ctas_override);
 int tree_attn_sm100_sms(const TreeAttnParams &p, int ctas_override);
+int tree_attn_sm100_group(const TreeAttnParams &p, int ctas_override);
 bool tree_attn_sm100_supported(const TreeAttnParams &p);
 
 }  // namespace sdb

@@ -426,6 +426,12 @@ int64_t tree_attn_sm100_workspace(const TreeAttnParams &p, int ctas_override) {
          (int64_t)(sp.n_workers + 1) * 8 + 256;
 }
 
+int tree_attn_sm100_group(const TreeAttnParams &p, int ctas_override) {
+  sm100::Sm100Params sp;
+  sm100_plan(p, ctas_override, sp);
+  return sp.cta_group;
+}
+
 int tree_attn_sm100_sms(const TreeAttnParams &p, int ctas_override) {
   sm100::Sm100Params sp;
   sm100_plan(p, ctas_override, sp);

@@ -20,7 +20,7 @@ namespace sdb {
 namespace sm100 {
 
 constexpr int kStagesK = 6;  // K ring: S(n) is issued ~3 items before its PV, so K needs the deeper ring
-constexpr int kStagesV = 4;
+constexpr int kStagesV = 3;  // (3 suffice: V(n) is consumed by PV(n), ~3 items after its load is issued)
 
 #ifdef SDB_TRACE
 // [event][iteration] clock64 stamps of worker 0 (debug builds only)
@@ -122,6 +122,9 @@ __host__ __device__ constexpr uint32_t make_idesc2(bool b_mn_major) {
          ((uint32_t)(256 >> 4) << 24);
 }
 
+constexpr int kLgStages = 5;     // fused argmax: 5 x 8 KB bulk-copy ring
+constexpr int kLgChunk = 2048;   // floats per chunk
+
 struct alignas(1024) Smem2 {
   uint8_t q[kTileBytes];  // this CTA's 128 query rows
   uint8_t k[kStagesK][kHalfBytes];
@@ -134,6 +137,8 @@ struct alignas(1024) Smem2 {
   float mref[3][128];  // running reference max after each item (log2 units), by slot
   float lsum[3][128];  // per-warpgroup partial row sums at the end of a unit
   float msum[3][128];  // ... and the reference max they are relative to
+  alignas(128) float lg[kLgStages][kLgChunk];  // fused greedy scan: logits chunk ring (warp 3; 16-B aligned for TMA)
+  uint64_t lg_full[kLgStages];
 };
 
 constexpr int kSoftmaxWG = 3;                       // softmax warpgroups (one per S slot)
@@ -286,6 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       mbar_init(&sm.o_done[s], 1);
     }
     mbar_init(&sm.o_free, 2 * 4 * kSoftmaxWG);
+    for (int s = 0; s < kLgStages; ++s) mbar_init(&sm.lg_full[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -448,6 +454,97 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         g_tile += N;
         g_item += N;
         ++g_q;
+      }
+    }
+  } else if (warp == 3) {
+    // ============ fused greedy-acceptance scan (otherwise idle warp) ============
+    // Packed argmax keys (orderable max, lowest index on ties; argmax_keys_kernel
+    // semantics, numcore.py:51-55) of logits rows r = cta, cta + grid, ...:
+    // the TMA engine streams each row through a 3 x 8 KB shared ring while
+    // the tensor pipe runs the attention, so the HBM-bound acceptance scan
+    // uses the attention's spare memory bandwidth instead of its own launch.
+    if (p.fa_logits) {
+      griddep_wait();  // logits may come from the kernel launched just before
+      const int nrows = p.batch * p.r_max;
+      const int cta = blockIdx.x, ncta = gridDim.x;
+      const int nchunk = (p.fa_vocab + kLgChunk - 1) / kLgChunk;
+      // this CTA's rows cta, cta + ncta, ... (n_rows gated), streamed as one
+      // continuous chunk sequence so the ring never drains at row boundaries
+      auto valid_from = [&](int row) {
+        for (; row < nrows; row += ncta) {
+          const int b = row / p.r_max, r = row % p.r_max;
+          if (r < min(p.n_rows[b], p.r_max)) return row;
+        }
+        return nrows;
+      };
+      int prow = valid_from(cta), pchunk = 0;  // producer cursor (lane 0)
+      uint32_t pg = 0;
+      auto issue_next = [&]() {
+        if (prow >= nrows) return;
+        const int st = pg % kLgStages;
+        const int n = min(kLgChunk, p.fa_vocab - pchunk * kLgChunk);
+        mbar_expect_tx(&sm.lg_full[st], (uint32_t)n * 4u);
+        bulk_g2s(sm.lg[st], p.fa_logits + (int64_t)prow * p.fa_row_stride + (int64_t)pchunk * kLgChunk,
+                 (uint32_t)n * 4u, &sm.lg_full[st]);
+        ++pg;
+        if (++pchunk == nchunk) {
+          pchunk = 0;
+          prow = valid_from(prow + ncta);
+        }
+      };
+      if (lane == 0)
+        for (int c = 0; c < kLgStages; ++c) issue_next();
+      uint32_t g = 0;  // consumer chunk count (ring slot / parity)
+      for (int row = valid_from(cta); row < nrows; row = valid_from(row + ncta)) {
+        // hot loop: 3 instructions per 16 bytes (LDS.128 + two 3-input
+        // max.NaN); the lane remembers only the chunk where its max first
+        // appeared, and the element index is recovered once per row
+        float bv = -INFINITY;
+        int bc = 0;  // (an all -inf row still resolves to its first index)
+        bool nan = false;
+        for (int c = 0; c < nchunk; ++c, ++g) {
+          const int st = g % kLgStages;
+          mbar_wait(&sm.lg_full[st], (g / kLgStages) & 1);
+          const int n4 = min(kLgChunk, p.fa_vocab - c * kLgChunk) >> 2;
+          const float4 *v4 = reinterpret_cast<const float4 *>(sm.lg[st]);
+          float cm = -INFINITY;
+#pragma unroll 4
+          for (int i = lane; i < n4; i += 32) {
+            const float4 v = v4[i];
+            cm = max_nan3(cm, max_nan3(v.x, v.y, v.z), v.w);
+          }
+          nan |= cm != cm;
+          if (cm > bv) {  // strict: the earliest chunk wins ties
+            bv = cm;
+            bc = c;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            fence_proxy_async_smem();  // the slot's generic reads precede the async-proxy refill
+            issue_next();
+          }
+        }
+        // row max, then the lowest index holding it (numpy argmax tie rule)
+        float m = bv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        int idx = 0x7fffffff;
+        if (bv == m) {
+          const float *ch = p.fa_logits + (int64_t)row * p.fa_row_stride + (int64_t)bc * kLgChunk;
+          const int n4 = min(kLgChunk, p.fa_vocab - bc * kLgChunk) >> 2;
+          for (int i = lane; i < n4 && idx == 0x7fffffff; i += 32) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(ch) + i);
+            const int e = v.x == m ? 0 : (v.y == m ? 1 : (v.z == m ? 2 : (v.w == m ? 3 : -1)));
+            if (e >= 0) idx = bc * kLgChunk + 4 * i + e;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) idx = min(idx, __shfl_xor_sync(0xffffffffu, idx, o));
+        const bool any_nan = __any_sync(0xffffffffu, nan);
+        if (lane == 0) {
+          p.fa_keys[row] = idx != 0x7fffffff ? argmax_key(m, (uint32_t)(p.fa_vocab_offset + idx)) : LLONG_MIN;
+          if (any_nan && p.fa_err) atomicOr(p.fa_err, SDB_ERR_NAN);
+        }
       }
     }
   } else if (warp >= 4) {

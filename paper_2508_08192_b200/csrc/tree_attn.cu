@@ -30,6 +30,9 @@ static bool fill_params(const sdb_tree_attn_args *a, TreeAttnParams &p) {
   p.q_row0 = a->q_row0;
   p.max_q_nodes = (a->max_q_nodes > 0 && a->max_q_nodes < a->r_max) ? a->max_q_nodes : a->r_max;
   p.pdl = (a->flags & SDB_ATTN_FLAG_PDL) != 0;
+  p.fa_logits = nullptr;
+  p.fa_keys = nullptr;
+  p.fa_err = nullptr;
   p.mask_words = a->mask_words;
   p.out = a->out;
   p.lse = a->lse;
@@ -107,7 +110,32 @@ extern "C" int sdb_tree_attn(const sdb_tree_attn_args *a, void *stream) {
     if (!a->workspace || a->workspace_bytes < need) return SDB_E_WORKSPACE;
   }
   cudaStream_t s = sdb::as_stream(stream);
-  if (sm100) return sdb::launch_tree_attn_sm100(p, a->num_splits, a->workspace, s);
+  // fused greedy acceptance scan: inside the pair kernel when it runs,
+  // otherwise a separate argmax launch right after the attention
+  bool fa_separate = false;
+  if (a->fused_keys) {
+    const bool ok = a->fused_logits && a->fused_vocab > 0 && a->fused_row_stride >= a->fused_vocab &&
+                    a->fused_vocab_offset >= 0 && a->fused_vocab_offset + a->fused_vocab <= 0xFFFFFFFFll;
+    if (!ok) return SDB_E_INVALID;
+    const bool vec = (a->fused_vocab % 4) == 0 && (a->fused_row_stride % 4) == 0 &&
+                     ((uintptr_t)a->fused_logits % 16) == 0;
+    if (sm100 && vec && sdb::tree_attn_sm100_group(p, a->num_splits) == 2) {
+      p.fa_logits = reinterpret_cast<const float *>(a->fused_logits);
+      p.fa_row_stride = a->fused_row_stride;
+      p.fa_vocab = a->fused_vocab;
+      p.fa_vocab_offset = a->fused_vocab_offset;
+      p.fa_keys = reinterpret_cast<long long *>(a->fused_keys);
+      p.fa_err = a->fused_err;
+    } else {
+      fa_separate = true;
+    }
+  }
+  if (sm100) {
+    rc = sdb::launch_tree_attn_sm100(p, a->num_splits, a->workspace, s);
+    if (rc != SDB_OK || !fa_separate) return rc;
+    return sdb_argmax_keys(a->fused_logits, SDB_DTYPE_F32, (int64_t)a->batch * a->r_max, a->fused_vocab,
+                           a->fused_row_stride, a->fused_vocab_offset, a->fused_keys, a->fused_err, stream);
+  }
   if (need > 0) {
     const int64_t rows = (int64_t)p.batch * p.r_max * p.hq;
     p.ws_out = reinterpret_cast<float *>(a->workspace);
@@ -116,6 +144,9 @@ extern "C" int sdb_tree_attn(const sdb_tree_attn_args *a, void *stream) {
     p.ws_out = nullptr;
     p.ws_lse = nullptr;
   }
-  if (a->dtype == SDB_DTYPE_BF16) return sdb::launch_tree_attn_simt<__nv_bfloat16>(p, s);
-  return sdb::launch_tree_attn_simt<float>(p, s);
+  rc = a->dtype == SDB_DTYPE_BF16 ? sdb::launch_tree_attn_simt<__nv_bfloat16>(p, s)
+                                  : sdb::launch_tree_attn_simt<float>(p, s);
+  if (rc != SDB_OK || !fa_separate) return rc;
+  return sdb_argmax_keys(a->fused_logits, SDB_DTYPE_F32, (int64_t)a->batch * a->r_max, a->fused_vocab,
+                         a->fused_row_stride, a->fused_vocab_offset, a->fused_keys, a->fused_err, stream);
 }

@@ -251,6 +251,23 @@ class GreedyAcceptor:
         return AcceptResult(o["path"], o["path_len"], o["next_token"], o["used"], o["err"])
 
 
+    def fused_keys(self, b, r, dev):
+        """Key buffer + error word for the attention-fused argmax scan."""
+        o = self._alloc(b, r, dev)
+        return o["keys"], o["err"]
+
+    def walk(self, parent, n_rows, tokens, stream=None):
+        """The greedy walk on keys produced by the attention-fused scan
+        (sdb_tree_attn fused_keys); err was zeroed by the caller."""
+        b, r = parent.shape
+        o = self._alloc(b, r, parent.device)
+        rc = _lib.lib().sdb_greedy_walk(_lib.ptr(o["keys"]), _lib.ptr(parent), _lib.ptr(n_rows), _lib.ptr(tokens),
+                                        b, r, _lib.ptr(o["path"]), _lib.ptr(o["path_len"]),
+                                        _lib.ptr(o["next_token"]), _lib.ptr(o["used"]), _lib.stream_ptr(stream))
+        _lib.check(rc, "greedy_walk")
+        return AcceptResult(o["path"], o["path_len"], o["next_token"], o["used"], o["err"])
+
+
 def accept_greedy(logits, parent, n_rows, tokens, stream=None):
     """Batched temperature-0 acceptance.
 

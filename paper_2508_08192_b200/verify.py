@@ -54,13 +54,14 @@ def _num_sms(device):
 
 
 class TreeVerifier:
-    def __init__(self, scale, temperature=0.0, top_p=1.0, max_ctx=None, num_splits=0, kernel=0):
+    def __init__(self, scale, temperature=0.0, top_p=1.0, max_ctx=None, num_splits=0, kernel=0, fuse_greedy=True):
         self.scale = scale
         self.temperature = temperature
         self.top_p = top_p
         self.max_ctx = max_ctx
         self.num_splits = num_splits
         self.kernel = kernel
+        self.fuse_greedy = fuse_greedy  # greedy scan inside the attention kernel: True (when it hides), "always", False
         self.attn = TreeVerifyAttention()
         self.greedy = GreedyAcceptor()
         self.stochastic = StochasticAcceptor()
@@ -98,20 +99,42 @@ class TreeVerifier:
         b, r = x.parent.shape
         lib = _lib.lib()
         main = stream if stream is not None else torch.cuda.current_stream()
+        attn_args = (x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
+                     self.scale)
+        attn_kw = dict(out=o["out"], lse=o["lse"], max_ctx=self.max_ctx, num_splits=self.num_splits,
+                       kernel=self.kernel)
+        # small batches: the attention's persistent grid leaves SMs free ->
+        # run acceptance beside it; full occupancy -> fold the greedy scan
+        # into the attention kernel (its otherwise idle warp + TMA ring)
+        can_overlap = overlap and self.attn.sms(*attn_args, **attn_kw) + 16 <= _num_sms(main.device)
+        fused = None
+        if (not can_overlap and self.fuse_greedy and self.temperature == 0 and isinstance(self.greedy, GreedyAcceptor)
+                and x.logits.dtype == torch.float32 and x.logits.stride(2) == 1
+                and (self.fuse_greedy == "always" or self._scan_hides(x, b, r, main.device))):
+            keys, err = self.greedy.fused_keys(b, r, x.logits.device)
+            with torch.cuda.stream(main):
+                err.zero_()  # before tree_build: the attention is tree_build's programmatic dependent
+            fused = (x.logits, keys, err, 0)
         fork = torch.cuda.Event()
         fork.record(main)
         rc = lib.sdb_tree_build(_lib.ptr(x.parent), _lib.ptr(x.n_rows), _lib.ptr(x.ctx_len), b, r,
                                 o["mask"].shape[-1], _lib.ptr(o["mask"]), _lib.ptr(o["pos"]), _lib.ptr(o["depth"]),
                                 _lib.ptr(o["tree_err"]), _lib.stream_ptr(main))
         _lib.check(rc, "tree_build")
-        self.attn(x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
-                  self.scale, out=o["out"], lse=o["lse"], max_ctx=self.max_ctx, num_splits=self.num_splits,
-                  kernel=self.kernel, stream=main, after_tree_build=True)
+        self.attn(*attn_args, **attn_kw, stream=main, after_tree_build=True, fused_argmax=fused)
+        if fused is not None:
+            # the attention kernel streamed the logits and left the argmax keys
+            acc = self.greedy.walk(x.parent, x.n_rows, x.tokens, stream=main)
+            if compact:
+                compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0),
+                           x.v_pool.unsqueeze(0), x.block_table, x.ctx_len, acc.path, acc.path_len, None,
+                           stream=main)
+            return o["out"], o["lse"], acc, o["tree_err"]
         # overlap only when the attention's persistent grid leaves SMs free
         # (small batches); at full occupancy the acceptance CTAs would delay
         # the attention's workers instead
         side = main
-        if overlap and self.attn.last_sms is not None and self.attn.last_sms + 16 <= _num_sms(main.device):
+        if can_overlap:
             if self._side is None or self._side.device != main.device:
                 self._side = torch.cuda.Stream(device=main.device)
             side = self._side
@@ -131,6 +154,17 @@ class TreeVerifier:
         if side is not main:
             main.wait_stream(side)
         return o["out"], o["lse"], acc, o["tree_err"]
+
+    def _scan_hides(self, x, b, r, device):
+        """Fold the greedy scan into the attention kernel only when one warp
+        per CTA streaming its share of the logits (~10 GB/s per SM through
+        the 40 KB TMA ring, measured) finishes well inside the attention
+        (~1 PFLOP/s achieved): e.g. 405B shapes (C4) yes, 70B bs32 (C3) no."""
+        hq, d = x.q.shape[2], x.q.shape[3]
+        ctx = self.max_ctx if self.max_ctx else x.block_table.shape[1] * x.k_pool.shape[2]
+        attn_s = 4.0 * d * hq * b * r * ctx / 1.0e15
+        scan_s = (b * r / _num_sms(device)) * x.logits.shape[2] * 4 / 10.0e9
+        return scan_s < 0.8 * attn_s
 
     # kernel launches per step (for the bench's gpu_launches claim)
     def launches_per_step(self, x: StepInputs):

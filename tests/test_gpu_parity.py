@@ -640,3 +640,40 @@ def test_draft_depth_attention_vs_oracle(kernel, dtype, hq, hkv, d):
             e = np.abs(got_o[b, q0[b]:total[b]] - want_o[b, q0[b]:total[b]])
             assert e.max() < tol_max and e.mean() < tol_mean, (depth, b, e.max(), e.mean())
             assert np.abs(got_l[b, :, q0[b]:total[b]] - want_l[b, :, q0[b]:total[b]]).max() < tol_lse, (depth, b)
+
+
+@pytest.mark.parametrize("B,V,tree", [(4, 128256, "t64"), (1, 4096, "t64"), (3, 1000, "n8"), (2, 4101, "t64")])
+def test_attention_fused_greedy_scan(B, V, tree):
+    """The greedy argmax scan fused into the attention call (pair kernel's
+    idle warp when it runs, else a separate launch) gives the same keys /
+    walk as accept_greedy; NaN rows raise the error bit."""
+    from paper_2508_08192_b200.sampling import accept_greedy
+    from paper_2508_08192_b200.verify import StepInputs, TreeVerifier
+
+    t = TREE64 if tree == "t64" else [-1, -1, 0, 0, 1, 2, 2, 5]
+    c = _rand_paged_case(B, 64, 8, 128, 1000, 32, t, seed=B + V)
+    R = c["R"]
+    rng = np.random.default_rng(V)
+    lg = (2.0 * rng.normal(size=(B, R, V))).astype(np.float32)
+    lg[:, ::5, 7] = lg[:, ::5, -3] = 40.0  # ties spanning chunks
+    am = lg.argmax(-1)
+    tok = np.where(rng.random((B, R)) < 0.7, am[:, np.array(c["aug"]).clip(min=0)], rng.integers(V, size=(B, R)))
+    tok = torch.tensor(tok.astype(np.int32), device="cuda")
+    x = StepInputs(parent=torch.tensor([list(c["aug"])] * B, dtype=torch.int32, device="cuda"), n_rows=c["nr"],
+                   ctx_len=c["ctx"], tokens=tok, q=c["q"], tree_k=c["tk"], tree_v=c["tv"],
+                   logits=torch.tensor(lg, device="cuda"), k_pool=c["kp"], v_pool=c["vp"], block_table=c["table"])
+    for fuse in ("always", False):
+        ver = TreeVerifier(scale=128 ** -0.5, fuse_greedy=fuse)
+        out, lse, acc, _ = ver.step(x, compact=False)
+        ref = accept_greedy(x.logits, x.parent, x.n_rows, x.tokens)
+        torch.cuda.synchronize()
+        assert int(acc.err[0]) == 0
+        assert torch.equal(acc.path_len, ref.path_len) and torch.equal(acc.next_token, ref.next_token)
+        for b in range(B):
+            n = int(ref.path_len[b])
+            assert torch.equal(acc.path[b, :n], ref.path[b, :n])
+    x.logits[0, 1, 5] = float("nan")
+    ver = TreeVerifier(scale=128 ** -0.5, fuse_greedy="always")
+    _, _, acc, _ = ver.step(x, compact=False)
+    torch.cuda.synchronize()
+    assert int(acc.err[0]) & 2

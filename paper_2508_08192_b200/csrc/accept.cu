@@ -433,60 +433,8 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   const int n4 = vec ? vocab >> 2 : 0;
   const float4 *r4 = reinterpret_cast<const float4 *>(row);
   constexpr int kU = 4;  // 16-byte loads in flight per thread
-  if (!nucleus) {
-    // one pass: online max + normaliser (+ NaN)
-    float m = -INFINITY, sacc = 0.f;
-    bool nan = false;
-    auto one = [&](float x) {
-      nan |= x != x;
-      const float x2 = x * a;
-      if (x2 > m) {
-        sacc *= exp2f(m - x2);
-        m = x2;
-      }
-      sacc += exp2f(x2 - m);
-    };
-    for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
-      float4 v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * kStThreads + threadIdx.x;
-        v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        one(v[u].x);
-        one(v[u].y);
-        one(v[u].z);
-        one(v[u].w);
-      }
-    }
-    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) one(row[j]);
-    if (__syncthreads_or(nan)) {
-      if (threadIdx.x == 0) {
-        atomicOr(err, SDB_ERR_NAN);
-        out->valid = 0;
-      }
-      return;
-    }
-    const float m2 = block_max<kStThreads>(m, sm.redf);
-    const double s = block_sum<kStThreads>(m > -INFINITY ? (double)sacc * exp2((double)m - (double)m2) : 0.0,
-                                           sm.red);
-    if (threadIdx.x == 0) {
-      RowStats st;
-      st.m2 = m2;
-      st.s = s;
-      st.z = s;
-      st.log2_z = (float)log2(s);
-      st.cut_key = 0;
-      st.cut_idx = 0;
-      st.keep_all = 1;
-      st.valid = 1;
-      *out = st;
-    }
-    return;
-  }
-  for (int i = threadIdx.x; i < kHistCopies * kHistBins; i += kStThreads) (&sm.hist[0][0])[i] = 0u;
+  if (nucleus)
+    for (int i = threadIdx.x; i < kHistCopies * kHistBins; i += kStThreads) (&sm.hist[0][0])[i] = 0u;
   // pass 1: max + NaN (3-input max.NaN: NaN propagates into the maximum)
   float mx = -INFINITY;
   for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
@@ -509,6 +457,44 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   }
   mx = block_max<kStThreads>(mx, sm.redf);
   const float m2 = mx * a;
+  if (!nucleus) {
+    // draft rows (and top_p = 1): the normaliser, two elements per packed op
+    const uint64_t A2 = f2splat(a), NM2 = f2splat(-m2);
+    uint64_t s2 = 0;
+    for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kStThreads + threadIdx.x;
+        v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        float e0, e1, e2, e3;
+        f2unpack(ffma2(f2pack(v[u].x, v[u].y), A2, NM2), e0, e1);
+        f2unpack(ffma2(f2pack(v[u].z, v[u].w), A2, NM2), e2, e3);
+        s2 = fadd2(s2, fadd2(f2pack(ex2(e0), ex2(e1)), f2pack(ex2(e2), ex2(e3))));
+      }
+    }
+    float s_lo, s_hi;
+    f2unpack(s2, s_lo, s_hi);
+    float s_loc = s_lo + s_hi;
+    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) s_loc += ex2(fmaf(row[j], a, -m2));
+    const double s = block_sum<kStThreads>((double)s_loc, sm.red);
+    if (threadIdx.x == 0) {
+      RowStats st;
+      st.m2 = m2;
+      st.s = s;
+      st.z = s;
+      st.log2_z = (float)log2(s);
+      st.cut_key = 0;
+      st.cut_idx = 0;
+      st.keep_all = 1;
+      st.valid = 1;
+      *out = st;
+    }
+    return;
+  }
   // pass 2 (L2): normaliser + mass histogram, two elements per packed op.
   // d = (m2 - x a) * 64 >= 0; bin = round(d) by the 1.5 * 2^23 magic add;
   // r = 2^-(d - bin)/64 = e^-t by a quadratic (|error| < 3e-8); the bin
@@ -530,10 +516,13 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const uint64_t t = fmul2(fsub2(d, fadd2(g, NMAG2)), TC2);
     const uint64_t rr = ffma2(t, ffma2(t, HALF2, NEG1), ONE2);
     const uint64_t fx = ffma2(rr, FIX2, MAG2);
+    // branch-free: out-of-range bins (d >= 4095, or -inf padding) add 0 to
+    // some bin (spread, so masked/-inf rows do not serialise on one address)
     const uint32_t b0 = (uint32_t)g - kMagicBits, b1 = (uint32_t)(g >> 32) - kMagicBits;
-    const uint32_t f0 = (uint32_t)fx - kMagicBits, f1 = (uint32_t)(fx >> 32) - kMagicBits;
-    if (b0 < (uint32_t)(kHistBins - 1)) atomicAdd(&hist[b0], f0);
-    if (b1 < (uint32_t)(kHistBins - 1)) atomicAdd(&hist[b1], f1);
+    const uint32_t f0 = b0 < (uint32_t)(kHistBins - 1) ? (uint32_t)fx - kMagicBits : 0u;
+    const uint32_t f1 = b1 < (uint32_t)(kHistBins - 1) ? (uint32_t)(fx >> 32) - kMagicBits : 0u;
+    atomicAdd(&hist[b0 & (kHistBins - 1)], f0);
+    atomicAdd(&hist[b1 & (kHistBins - 1)], f1);
   };
   for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
     float4 v[kU];

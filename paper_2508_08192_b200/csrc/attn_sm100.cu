@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem<NT> &sm = *reinterpret_cast<Smem<NT> *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const TreeAttnParams &p = sp.p;
+  griddep_launch_dependents();  // the fix-up grid may become resident (it waits for our completion)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = p.hq / p.hkv;
   const float sl2 = p.scale * 1.4426950408889634f;
@@ -283,6 +284,9 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
 // merges all of u's pieces (same math as merge_partials,
 // attention.py:108-124).  grid (n_workers - 1, rows_unit / 4), one warp per row.
 __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params sp) {
+  // launched as a programmatic dependent of the attention kernel: resident
+  // early, released when every attention CTA has finished and flushed
+  griddep_wait();
   const TreeAttnParams &p = sp.p;
   const int k = blockIdx.x + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -514,8 +518,16 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *wor
     SDB_CHECK_LAUNCH();
   }
   if (sp.n_workers > 1) {
-    dim3 fgrid(sp.n_workers - 1, cdiv(sp.rows_unit, 4));
-    tree_attn_fixup_kernel<<<fgrid, 128, 0, stream>>>(sp);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sp.n_workers - 1, cdiv(sp.rows_unit, 4));
+    cfg.blockDim = dim3(128);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, tree_attn_fixup_kernel, sp);
     SDB_CHECK_LAUNCH();
   }
   return SDB_OK;

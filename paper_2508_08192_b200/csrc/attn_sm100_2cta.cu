@@ -269,6 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const float sl2 = p.scale * 1.4426950408889634f;
   const uint32_t rank = cta_rank();
   const int worker = blockIdx.x >> 1;
+  griddep_launch_dependents();  // the fix-up grid may become resident (it waits for our completion)
 
   if (threadIdx.x == 0) {
     if (rank == 0) {

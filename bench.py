@@ -569,6 +569,13 @@ def main():
                 "unit": "TFLOP/s", "frac": achieved_tf / tc_peak, "traffic": traffic, "peak_source": peak_src,
                 "flops_per_launch": attn_flops, "hbm_gbs": attn_bytes / (t_attn_ms * 1e-3) / 1e9,
                 "accept_hbm_gbs": accept_gbs, "accept_hbm_frac": accept_gbs / hbm_peak}
+    # step-level roofline: the attention's binding bound (tensor at C3/C4)
+    # plus the acceptance's HBM bound, executed back to back
+    t_attn_star = 0.0 if accept_only else max(attn_flops / (tc_peak * 1e12), attn_bytes / (hbm_peak * 1e9))
+    t_star = t_attn_star + accept_bytes / (hbm_peak * 1e9)
+    step_roof = {"t_star_us": t_star * 1e6, "frac": t_star / (ms * 1e-3),
+                 "how": "max(attention FLOPs / measured bf16 peak, attention bytes / measured HBM) + acceptance "
+                        "bytes / measured HBM"}
     # library kernels per step: tree_build 1, attention 2 (persistent kernel +
     # LSE fix-up), acceptance 2 (greedy: keys + walk; stochastic: row stats +
     # walk, + 1 Philox), compaction 1
@@ -585,6 +592,7 @@ def main():
         "kernels_ms": parts,
         "mean_accepted": accept_len,
         "roofline": roof,
+        "step_roofline": step_roof,
         "clocks": sampler.summary(),
         "gpu_launches": n_launch * args.steps,
         "e2e": e2e,

@@ -45,6 +45,7 @@ extern "C" {
 #define SDB_ERR_UNIFORMS 8        /* SamplingError: uniform stream exhausted (sampling.py:179) */
 #define SDB_ERR_ALL_MASKED 16     /* AttentionError: row masked in every part (attention.py:117) */
 #define SDB_ERR_NO_ALLOWED 32     /* SamplingError: no token allowed (sampling.py:96-97)       */
+#define SDB_ERR_CACHE 64          /* CacheError: block pool exhausted / tape or table overflow */
 
 #define SDB_DTYPE_BF16 0
 #define SDB_DTYPE_F32 1
@@ -296,6 +297,37 @@ int sdb_compact_kv(const void *tree_k, const void *tree_v, void *k_cache, void *
                    const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
                    const int32_t *n_keep, int n_layers, int batch, int r_max, int hkv,
                    int head_dim, int block_size, int elem_bytes, void *stream);
+
+/* ---- bookkeeping either side of the step ----------
+ * Draft-cache write-back (engine.py:524-531): rows path[:n_keep-1] of the
+ * draft's carried suffix K/V suffix_k/v [n_layers][B][n_src][hkv][head_dim]
+ * (realized draft nodes in node order, no root row) written at positions
+ * ctx_len[b] + 1 .. (L; the alignment token already sits at L - 1). */
+int sdb_compact_draft_kv(const void *suffix_k, const void *suffix_v, void *k_cache, void *v_cache,
+                         int64_t cache_layer_stride, const int32_t *block_table, int max_blocks,
+                         const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
+                         const int32_t *n_keep, int n_layers, int batch, int r_max, int n_src, int hkv,
+                         int head_dim, int block_size, int elem_bytes, void *stream);
+
+/* Hidden tape append (engine.py:532-533 -> HiddenTape.append_rows,
+ * kvstore.py:405-409): rows [0] + [1 + a for a in path[:n_keep-1]] of hidden
+ * [B][r_max][row_bytes] appended to tape [B][tape_cap][row_bytes] at
+ * tape_len[b], which advances; overflow sets SDB_ERR_CACHE. */
+int sdb_tape_append(const void *hidden, void *tape, int64_t tape_cap, int32_t *tape_len, const int32_t *path,
+                    const int32_t *path_len, const int32_t *n_keep, int batch, int r_max, int row_bytes,
+                    int32_t *err, void *stream);
+
+/* Device block allocator (PagedKvCache.ensure / alloc_for_step / rewind,
+ * kvstore.py:195-203, 248-258): free_stack int32 [num_blocks] holds free block
+ * ids in [0, *free_top); n_mapped int32 [B] counts each sequence's mapped
+ * blocks (block_table[b][0..n_mapped)).  sdb_paged_alloc maps blocks until
+ * n_mapped * block_size >= need[b] (alloc_for_step: need = length +
+ * n_draft_nodes + 1); exhaustion sets SDB_ERR_CACHE.  sdb_paged_rewind
+ * unmaps the blocks beyond ceil(new_len / block_size) (entries -> -1). */
+int sdb_paged_alloc(int32_t *block_table, int max_blocks, int32_t *n_mapped, const int32_t *need, int batch,
+                    int block_size, int32_t *free_stack, int32_t *free_top, int32_t *err, void *stream);
+int sdb_paged_rewind(int32_t *block_table, int max_blocks, int32_t *n_mapped, const int32_t *new_len, int batch,
+                     int block_size, int32_t *free_stack, int32_t *free_top, void *stream);
 
 /* Generic row scatter / gather on one sequence's pages (PagedKvCache.write /
  * gather, kvstore.py:217-225, 235-246): rows [n][hkv*head_dim] <-> pages at

@@ -477,6 +477,101 @@ def gen_draft_attention():
     np.savez_compressed(os.path.join(OUT, "draft_attention.npz"), **store)
 
 
+def gen_bookkeep():
+    """Several engine rounds of bookkeeping on the reference caches
+    (engine.py:455-457 alloc_for_step, 504-533 write-back / rewind / set_len
+    for the base AND draft caches and the hidden tape, kvstore.py:195-258,
+    389-431).  The draft cache's alignment write at L - 1 (draft_stage's
+    first forward, engine.py:358-360) is replayed as a plain write."""
+    rng = np.random.default_rng(4242)
+    out = {}
+    k = 0
+    for bs, spec in ((16, TREE64), (4, N8), (8, "chain:3")):
+        tree = R_tree.parse_tree(spec)
+        aug = R_eng._augment(tree)
+        hkv, d, n_layers, dim, nb = 2, 8, 2, 16, 96
+        base = R_kv.PagedKvCache(n_layers, hkv * d, n_blocks=nb, block_size=bs)
+        dr = R_kv.PagedKvCache(n_layers, hkv * d, n_blocks=nb, block_size=bs)
+        tape = R_kv.HiddenTape(dim)
+        for c in (base, dr):
+            c.new_seq(0)
+        L = 9  # committed length after prefill
+        for c in (base, dr):
+            c.ensure(0, L)
+            for li in range(n_layers):
+                c.write(0, li, 0, rng.normal(size=(L, hkv * d)), rng.normal(size=(L, hkv * d)))
+            c.set_len(0, L)
+        # prefill leaves L - 1 committed K/V rows: drop the last (it is the root of round 1)
+        for c in (base, dr):
+            c.rewind(0, L - 1)
+            c.set_len(0, L)
+        tape.append_rows(rng.normal(size=(L - 1, dim)))
+        pre = f"b{k}_"
+        out[pre + "meta"] = np.array([bs, hkv, d, n_layers, dim, nb, L])
+        out[pre + "parent"] = np.array(tree.parent, dtype=np.int32)
+        init_b = [base.gather(0, li, L - 1) for li in range(n_layers)]
+        init_d = [dr.gather(0, li, L - 1) for li in range(n_layers)]
+        for li in range(n_layers):
+            out[pre + f"ib{li}"] = np.stack(init_b[li])
+            out[pre + f"id{li}"] = np.stack(init_d[li])
+        out[pre + "itape"] = tape.slice(0, len(tape))
+        rounds = 4
+        for rd in range(rounds):
+            L = base.committed_len(0)
+            base.alloc_for_step(0, tree.n_nodes)
+            dr.alloc_for_step(0, tree.n_nodes)
+            align = (rng.normal(size=(1, hkv * d)), rng.normal(size=(1, hkv * d)))
+            for li in range(n_layers):
+                dr.write(0, li, L - 1, align[0], align[1])
+            path, cur = [], -1
+            while True:
+                kids = tree.children(cur)
+                if not kids or rng.random() < 0.2:
+                    break
+                cur = kids[int(rng.integers(len(kids)))]
+                path.append(cur)
+            kept = len(path) + 1
+            if rng.random() < 0.3 and kept > 1:
+                kept = int(rng.integers(1, kept + 1))
+            base_kv = [(rng.normal(size=(aug.n_nodes, hkv * d)), rng.normal(size=(aug.n_nodes, hkv * d)))
+                       for _ in range(n_layers)]
+            suf_kv = [(rng.normal(size=(tree.n_nodes, hkv * d)), rng.normal(size=(tree.n_nodes, hkv * d)))
+                      for _ in range(n_layers)]
+            hid = rng.normal(size=(aug.n_nodes, dim))
+            write_path = path[:kept - 1]
+            rows = [0] + [1 + a for a in write_path]
+            for li in range(n_layers):
+                base.write(0, li, L - 1, base_kv[li][0][rows], base_kv[li][1][rows])
+            new_len = L + kept
+            base.rewind(0, new_len - 1)
+            base.set_len(0, new_len)
+            if write_path:
+                for li in range(n_layers):
+                    dr.write(0, li, L, suf_kv[li][0][write_path], suf_kv[li][1][write_path])
+            dr.rewind(0, new_len - 1)
+            dr.set_len(0, new_len)
+            tape.append_rows(np.stack([hid[0]] + [hid[1 + a] for a in write_path]))
+            q = f"{pre}r{rd}_"
+            out[q + "path"] = np.array(path, dtype=np.int32)
+            out[q + "kept"] = np.array(kept)
+            out[q + "align_k"], out[q + "align_v"] = align
+            out[q + "hid"] = hid
+            for li in range(n_layers):
+                out[q + f"bk{li}"], out[q + f"bv{li}"] = base_kv[li]
+                out[q + f"sk{li}"], out[q + f"sv{li}"] = suf_kv[li]
+        L = base.committed_len(0)
+        for li in range(n_layers):
+            out[pre + f"gb{li}"] = np.stack(base.gather(0, li, L - 1))
+            out[pre + f"gd{li}"] = np.stack(dr.gather(0, li, L - 1))
+        out[pre + "tape"] = tape.slice(0, len(tape))
+        out[pre + "final_len"] = np.array(L)
+        out[pre + "blocks_used"] = np.array([len(base._seqs[0].table), len(dr._seqs[0].table)])
+        out[pre + "rounds"] = np.array(rounds)
+        k += 1
+    out["n_cases"] = np.array(k)
+    np.savez_compressed(os.path.join(OUT, "bookkeep.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     if len(sys.argv) > 1:  # e.g. `make_golden.py gen_draft_attention`
@@ -490,5 +585,6 @@ if __name__ == "__main__":
     gen_philox()
     gen_compact()
     gen_draft_attention()
+    gen_bookkeep()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

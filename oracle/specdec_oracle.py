@@ -520,3 +520,49 @@ def compact_kv(k_pool, v_pool, block_table, ctx_len, tree_k, tree_v, path, n_kee
     paged_write(k_pool, block_table, ctx_len, tree_k[r].reshape(len(rows), hkv * d))
     paged_write(v_pool, block_table, ctx_len, tree_v[r].reshape(len(rows), hkv * d))
     return rows
+
+
+# ---------------------------------------------------------------------------
+# Bookkeeping either side of the step (engine.py:504-533), logical view
+# ---------------------------------------------------------------------------
+
+def bookkeep_round(base_rows, draft_rows, tape_rows, L, path, kept, base_kv, suffix_kv, hidden, align_kv):
+    """One round of the engine's bookkeeping on logical (position-indexed)
+    rows, restating engine.py:514-533 + PagedKvCache.write / rewind / set_len
+    (kvstore.py:217-225, 248-258) and HiddenTape.append_rows (405-409).
+
+    base_rows / draft_rows: per layer [k_rows, v_rows] lists (committed
+    positions 0 .. L-2); tape_rows: list of hidden rows.  The draft's
+    alignment write (align_kv per layer, position L-1) precedes the
+    write-back.  Returns the new committed length."""
+    write_path = list(path)[:kept - 1]
+    rows = accepted_rows(path, kept)
+    new_len = L + kept
+    for li, (k, v) in enumerate(base_kv):
+        for j, rr in enumerate(rows):
+            for col, src in ((0, k), (1, v)):
+                seq = base_rows[li][col]
+                pos = L - 1 + j
+                if pos < len(seq):
+                    seq[pos] = src[rr]
+                else:
+                    seq.append(src[rr])
+        for col in (0, 1):
+            del base_rows[li][col][new_len - 1:]
+    for li, (k, v) in enumerate(suffix_kv):
+        for col, src in ((0, k), (1, v)):
+            seq = draft_rows[li][col]
+            a = align_kv[li][col]
+            if L - 1 < len(seq):
+                seq[L - 1] = a
+            else:
+                seq.append(a)
+            for j, node in enumerate(write_path):
+                pos = L + j
+                if pos < len(seq):
+                    seq[pos] = src[node]
+                else:
+                    seq.append(src[node])
+            del seq[new_len - 1:]
+    tape_rows.extend([hidden[0]] + [hidden[1 + a] for a in write_path])
+    return new_len

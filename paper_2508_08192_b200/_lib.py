@@ -21,6 +21,7 @@ SDB_ERR_BAD_DIST = 4
 SDB_ERR_UNIFORMS = 8
 SDB_ERR_ALL_MASKED = 16
 SDB_ERR_NO_ALLOWED = 32
+SDB_ERR_CACHE = 64
 
 ATTN_FLAG_PDL = 1
 
@@ -100,6 +101,10 @@ _SIGNATURES = {
     "sdb_target_dist_f64": (I32, [P, P, I64, I32, F64, F64, P, P, P]),
     "sdb_mss_verify_f64": (I32, [P, P, I32, I32, P, P, P, I32, P, P, P, P, P]),
     "sdb_compact_kv": (I32, [P, P, P, P, I64, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, P]),
+    "sdb_compact_draft_kv": (I32, [P, P, P, P, I64, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, P]),
+    "sdb_tape_append": (I32, [P, P, I64, P, P, P, P, I32, I32, I32, P, P]),
+    "sdb_paged_alloc": (I32, [P, I32, P, P, I32, I32, P, P, P, P]),
+    "sdb_paged_rewind": (I32, [P, I32, P, P, I32, I32, P, P, P]),
     "sdb_paged_write": (I32, [P, P, I64, P, I64, I32, I32, I32, I32, P]),
     "sdb_paged_gather": (I32, [P, P, I64, P, I64, I32, I32, I32, I32, P]),
 }

@@ -121,3 +121,180 @@ extern "C" int sdb_paged_gather(const void *pool, const int32_t *block_table, in
   return paged_rows(false, const_cast<void *>(pool), block_table, start, rows, n, hkv, head_dim, block_size,
                     elem_bytes, stream);
 }
+
+// ---------------------------------------------------------------------------
+// Bookkeeping either side of the verify step
+// ---------------------------------------------------------------------------
+namespace sdb {
+
+// Draft-cache write-back (engine.py:524-531): rows write_path =
+// path[:n_keep-1] of the draft's carried suffix K/V (realized draft nodes, no
+// root row) at positions ctx_len + 1 .. (the draft cache holds the root --
+// the alignment token -- at ctx_len = L - 1 already).
+__global__ void compact_draft_kv_kernel(const uint8_t *__restrict__ suf_k, const uint8_t *__restrict__ suf_v,
+                                        uint8_t *__restrict__ k_cache, uint8_t *__restrict__ v_cache,
+                                        int64_t layer_stride_bytes, const int32_t *__restrict__ block_table,
+                                        int max_blocks, const int32_t *__restrict__ ctx_len,
+                                        const int32_t *__restrict__ path, const int32_t *__restrict__ path_len,
+                                        const int32_t *__restrict__ n_keep, int batch, int r_max, int n_src,
+                                        int hkv, int row_bytes, int block_size) {
+  const int slot = blockIdx.x, b = blockIdx.y, layer = blockIdx.z;
+  const int len = path_len[b];
+  const int keep = n_keep ? n_keep[b] : len + 1;
+  if (slot >= min(keep - 1, len)) return;
+  const int row = path[(int64_t)b * r_max + slot];
+  const int64_t pos = (int64_t)ctx_len[b] + 1 + slot;
+  const int page = block_table[(int64_t)b * max_blocks + pos / block_size];
+  const int off = (int)(pos % block_size);
+  const int64_t src_row = (((int64_t)layer * batch + b) * n_src + row) * hkv;
+  const int chunks = row_bytes / 16;
+  for (int idx = threadIdx.x; idx < hkv * chunks; idx += blockDim.x) {
+    const int h = idx / chunks, c = idx % chunks;
+    const int64_t src = (src_row + h) * row_bytes + (int64_t)c * 16;
+    const int64_t dst = layer * layer_stride_bytes + ((((int64_t)page * hkv + h) * block_size + off) * row_bytes) +
+                        (int64_t)c * 16;
+    *reinterpret_cast<int4 *>(k_cache + dst) = *reinterpret_cast<const int4 *>(suf_k + src);
+    *reinterpret_cast<int4 *>(v_cache + dst) = *reinterpret_cast<const int4 *>(suf_v + src);
+  }
+}
+
+// Hidden tape append (engine.py:532-533, HiddenTape.append_rows
+// kvstore.py:405-409): rows [0] + [1 + a for a in write_path] of the
+// verify step's hidden states appended at tape_len[b]; tape_len advances.
+__global__ void tape_append_kernel(const uint8_t *__restrict__ hidden, uint8_t *__restrict__ tape, int64_t tape_cap,
+                                   int32_t *__restrict__ tape_len, const int32_t *__restrict__ path,
+                                   const int32_t *__restrict__ path_len, const int32_t *__restrict__ n_keep,
+                                   int r_max, int row_bytes, int32_t *__restrict__ err) {
+  const int slot = blockIdx.x, b = blockIdx.y;
+  const int len = path_len[b];
+  const int keep = n_keep ? n_keep[b] : len + 1;
+  const int n_write = min(keep - 1, len) + 1;
+  const int base = tape_len[b];
+  if (slot >= n_write) return;
+  if (base + n_write > tape_cap) {
+    if (slot == 0 && threadIdx.x == 0) atomicOr(err, SDB_ERR_CACHE);
+    return;
+  }
+  const int row = slot == 0 ? 0 : 1 + path[(int64_t)b * r_max + slot - 1];
+  const uint8_t *src = hidden + ((int64_t)b * r_max + row) * row_bytes;
+  uint8_t *dst = tape + ((int64_t)b * tape_cap + base + slot) * row_bytes;
+  for (int c = threadIdx.x; c < row_bytes / 16; c += blockDim.x)
+    reinterpret_cast<int4 *>(dst)[c] = reinterpret_cast<const int4 *>(src)[c];
+}
+
+__global__ void tape_advance_kernel(int32_t *__restrict__ tape_len, int64_t tape_cap,
+                                    const int32_t *__restrict__ path_len, const int32_t *__restrict__ n_keep,
+                                    int batch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const int len = path_len[b];
+  const int keep = n_keep ? n_keep[b] : len + 1;
+  const int n_write = min(keep - 1, len) + 1;
+  if (tape_len[b] + n_write <= tape_cap) tape_len[b] += n_write;
+}
+
+// Device block allocator (PagedKvCache.ensure / alloc_for_step / rewind,
+// kvstore.py:195-203, 248-258): a free stack of block ids (top = count) and
+// per-sequence mapped-block counts.  alloc: map blocks until
+// n_mapped * bs >= need[b]; rewind: unmap blocks beyond ceil(new_len / bs).
+// One thread per sequence; the stack is shared through atomics (block ids
+// differ from the reference's list order; the logical mapping does not).
+__global__ void paged_alloc_kernel(int32_t *__restrict__ block_table, int max_blocks, int32_t *__restrict__ n_mapped,
+                                   const int32_t *__restrict__ need, int batch, int block_size,
+                                   int32_t *__restrict__ free_stack, int32_t *__restrict__ free_top,
+                                   int32_t *__restrict__ err) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const int want = min(max_blocks, (need[b] + block_size - 1) / block_size);
+  if ((int64_t)need[b] > (int64_t)max_blocks * block_size) atomicOr(err, SDB_ERR_CACHE);
+  int have = n_mapped[b];
+  while (have < want) {
+    const int t = atomicSub(free_top, 1) - 1;
+    if (t < 0) {  // pool exhausted (CacheError "block pool exhausted")
+      atomicAdd(free_top, 1);
+      atomicOr(err, SDB_ERR_CACHE);
+      break;
+    }
+    block_table[(int64_t)b * max_blocks + have++] = free_stack[t];
+  }
+  n_mapped[b] = have;
+}
+
+__global__ void paged_rewind_kernel(int32_t *__restrict__ block_table, int max_blocks, int32_t *__restrict__ n_mapped,
+                                    const int32_t *__restrict__ new_len, int batch, int block_size,
+                                    int32_t *__restrict__ free_stack, int32_t *__restrict__ free_top) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const int keep = (new_len[b] + block_size - 1) / block_size;
+  const int have = n_mapped[b];
+  if (have <= keep) return;
+  const int t = atomicAdd(free_top, have - keep);
+  for (int i = keep; i < have; ++i) {
+    free_stack[t + i - keep] = block_table[(int64_t)b * max_blocks + i];
+    block_table[(int64_t)b * max_blocks + i] = -1;
+  }
+  n_mapped[b] = keep;
+}
+
+}  // namespace sdb
+
+extern "C" int sdb_compact_draft_kv(const void *suffix_k, const void *suffix_v, void *k_cache, void *v_cache,
+                                    int64_t cache_layer_stride, const int32_t *block_table, int max_blocks,
+                                    const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
+                                    const int32_t *n_keep, int n_layers, int batch, int r_max, int n_src, int hkv,
+                                    int head_dim, int block_size, int elem_bytes, void *stream) {
+  if (!suffix_k || !suffix_v || !k_cache || !v_cache || !block_table || !ctx_len || !path || !path_len ||
+      n_layers < 1 || batch < 0 || r_max < 1 || n_src < 1 || hkv < 1 || block_size < 1 || max_blocks < 1)
+    return SDB_E_INVALID;
+  const int row_bytes = head_dim * elem_bytes;
+  if (row_bytes % 16 != 0) return SDB_E_UNSUPPORTED;
+  if (batch == 0) return SDB_OK;
+  dim3 grid(r_max, batch, n_layers);
+  sdb::compact_draft_kv_kernel<<<grid, 128, 0, sdb::as_stream(stream)>>>(
+      (const uint8_t *)suffix_k, (const uint8_t *)suffix_v, (uint8_t *)k_cache, (uint8_t *)v_cache,
+      cache_layer_stride * elem_bytes, block_table, max_blocks, ctx_len, path, path_len, n_keep, batch, r_max, n_src,
+      hkv, row_bytes, block_size);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+extern "C" int sdb_tape_append(const void *hidden, void *tape, int64_t tape_cap, int32_t *tape_len,
+                               const int32_t *path, const int32_t *path_len, const int32_t *n_keep, int batch,
+                               int r_max, int row_bytes, int32_t *err, void *stream) {
+  if (!hidden || !tape || !tape_len || !path || !path_len || !err || batch < 0 || r_max < 1 || tape_cap < 1 ||
+      row_bytes < 16 || row_bytes % 16 != 0)
+    return SDB_E_INVALID;
+  if (batch == 0) return SDB_OK;
+  cudaStream_t s = sdb::as_stream(stream);
+  sdb::tape_append_kernel<<<dim3(r_max, batch), 128, 0, s>>>((const uint8_t *)hidden, (uint8_t *)tape, tape_cap,
+                                                            tape_len, path, path_len, n_keep, r_max, row_bytes, err);
+  SDB_CHECK_LAUNCH();
+  sdb::tape_advance_kernel<<<(batch + 127) / 128, 128, 0, s>>>(tape_len, tape_cap, path_len, n_keep, batch);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+extern "C" int sdb_paged_alloc(int32_t *block_table, int max_blocks, int32_t *n_mapped, const int32_t *need,
+                               int batch, int block_size, int32_t *free_stack, int32_t *free_top, int32_t *err,
+                               void *stream) {
+  if (!block_table || !n_mapped || !need || !free_stack || !free_top || !err || batch < 0 || max_blocks < 1 ||
+      block_size < 1)
+    return SDB_E_INVALID;
+  if (batch == 0) return SDB_OK;
+  sdb::paged_alloc_kernel<<<(batch + 127) / 128, 128, 0, sdb::as_stream(stream)>>>(
+      block_table, max_blocks, n_mapped, need, batch, block_size, free_stack, free_top, err);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+extern "C" int sdb_paged_rewind(int32_t *block_table, int max_blocks, int32_t *n_mapped, const int32_t *new_len,
+                                int batch, int block_size, int32_t *free_stack, int32_t *free_top, void *stream) {
+  if (!block_table || !n_mapped || !new_len || !free_stack || !free_top || batch < 0 || max_blocks < 1 ||
+      block_size < 1)
+    return SDB_E_INVALID;
+  if (batch == 0) return SDB_OK;
+  sdb::paged_rewind_kernel<<<(batch + 127) / 128, 128, 0, sdb::as_stream(stream)>>>(
+      block_table, max_blocks, n_mapped, new_len, batch, block_size, free_stack, free_top);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}

@@ -224,3 +224,83 @@ def compact_kv(tree_k, tree_v, k_pools, v_pools, block_table, ctx_len, path, pat
                                    _lib.ptr(path), _lib.ptr(path_len), _lib.ptr(n_keep), n_layers, b, r, hkv, d, bs,
                                    tree_k.element_size(), _lib.stream_ptr(stream))
     _lib.check(rc, "compact_kv")
+
+
+# ---------------------------------------------------------------------------
+# bookkeeping either side of the step
+# ---------------------------------------------------------------------------
+
+def compact_draft_kv(suffix_k, suffix_v, k_pools, v_pools, block_table, ctx_len, path, path_len, n_keep=None,
+                     stream=None):
+    """Draft-cache write-back (engine.py:524-531): rows path[:n_keep-1] of the
+    draft's carried suffix K/V [L, B, n_src, Hkv, d] (realized draft nodes, no
+    root row) into the draft pages at positions ctx_len + 1 .. (= L)."""
+    n_layers, b, n_src, hkv, d = suffix_k.shape
+    bs = k_pools.shape[3]
+    if k_pools.shape[2] != hkv or k_pools.shape[4] != d or k_pools.dtype != suffix_k.dtype:
+        raise CacheError("compact_draft_kv: pool / suffix shape mismatch")
+    rc = _lib.lib().sdb_compact_draft_kv(_lib.ptr(suffix_k), _lib.ptr(suffix_v), _lib.ptr(k_pools),
+                                         _lib.ptr(v_pools), k_pools.stride(0), _lib.ptr(block_table),
+                                         block_table.shape[1], _lib.ptr(ctx_len), _lib.ptr(path), _lib.ptr(path_len),
+                                         _lib.ptr(n_keep), n_layers, b, path.shape[1], n_src, hkv, d, bs,
+                                         suffix_k.element_size(), _lib.stream_ptr(stream))
+    _lib.check(rc, "compact_draft_kv")
+
+
+def tape_append(hidden, tape, tape_len, path, path_len, err, n_keep=None, stream=None):
+    """HiddenTape.append_rows of the kept rows (engine.py:532-533): rows [0] +
+    [1 + a for a in path[:n_keep-1]] of hidden [B, R, dim] appended to tape
+    [B, cap, dim] at tape_len [B] (advanced in place)."""
+    b, r, dim = hidden.shape
+    if tape.shape[0] != b or tape.shape[2] != dim or tape.dtype != hidden.dtype:
+        raise CacheError("tape_append: tape / hidden shape mismatch")
+    rc = _lib.lib().sdb_tape_append(_lib.ptr(hidden), _lib.ptr(tape), tape.shape[1], _lib.ptr(tape_len),
+                                    _lib.ptr(path), _lib.ptr(path_len), _lib.ptr(n_keep), b, r,
+                                    dim * hidden.element_size(), _lib.ptr(err), _lib.stream_ptr(stream))
+    _lib.check(rc, "tape_append")
+
+
+class DeviceBlockAllocator:
+    """Device-resident block tables and free list for a batch of sequences:
+    the mapping half of PagedKvCache (ensure / alloc_for_step / rewind,
+    kvstore.py:195-203, 248-258) without host round trips.  Block ids differ
+    from the reference's list order; the logical position -> block mapping
+    (and thus every gather) does not.  Errors (pool exhausted) set
+    SDB_ERR_CACHE in ``err``."""
+
+    def __init__(self, num_blocks, batch, max_blocks, block_size, device):
+        import torch
+
+        self.block_size = block_size
+        self.free_stack = torch.arange(num_blocks - 1, -1, -1, dtype=torch.int32, device=device)
+        self.free_top = torch.tensor([num_blocks], dtype=torch.int32, device=device)
+        self.block_table = torch.full((batch, max_blocks), -1, dtype=torch.int32, device=device)
+        self.n_mapped = torch.zeros((batch,), dtype=torch.int32, device=device)
+        self.err = torch.zeros((1,), dtype=torch.int32, device=device)
+
+    def ensure(self, need, stream=None):
+        """Map blocks until every sequence covers need[b] positions."""
+        b, mb = self.block_table.shape
+        rc = _lib.lib().sdb_paged_alloc(_lib.ptr(self.block_table), mb, _lib.ptr(self.n_mapped), _lib.ptr(need), b,
+                                        self.block_size, _lib.ptr(self.free_stack), _lib.ptr(self.free_top),
+                                        _lib.ptr(self.err), _lib.stream_ptr(stream))
+        _lib.check(rc, "paged_alloc")
+
+    def alloc_for_step(self, length, n_draft_nodes, stream=None):
+        """Blocks for committed length + draft nodes + the bonus token
+        (length: int32 device tensor [B])."""
+        import torch
+
+        self.ensure((length + n_draft_nodes + 1).to(torch.int32), stream)
+
+    def rewind(self, new_len, stream=None):
+        """Unmap the blocks beyond ceil(new_len / block_size)."""
+        b, mb = self.block_table.shape
+        rc = _lib.lib().sdb_paged_rewind(_lib.ptr(self.block_table), mb, _lib.ptr(self.n_mapped), _lib.ptr(new_len),
+                                         b, self.block_size, _lib.ptr(self.free_stack), _lib.ptr(self.free_top),
+                                         _lib.stream_ptr(stream))
+        _lib.check(rc, "paged_rewind")
+
+    def check(self):
+        if int(self.err[0]):
+            raise CacheError("block pool exhausted")

@@ -677,3 +677,86 @@ def test_attention_fused_greedy_scan(B, V, tree):
     _, _, acc, _ = ver.step(x, compact=False)
     torch.cuda.synchronize()
     assert int(acc.err[0]) & 2
+
+
+def test_device_bookkeeping_replays_reference_rounds(golden):
+    """Base + draft cache write-back, rewind and block mapping on the device
+    allocator, and the hidden tape, over several engine rounds: the logical
+    contents equal the reference caches' gathers and tape (bit-exact)."""
+    from paper_2508_08192_b200.kvstore import DeviceBlockAllocator, compact_draft_kv, compact_kv, tape_append
+
+    g = golden("bookkeep")
+    dev = "cuda"
+    for k in range(int(g["n_cases"])):
+        p = f"b{k}_"
+        bs, hkv, d, n_layers, dim, nb, L = (int(x) for x in g[p + "meta"])
+        n_nodes = len(g[p + "parent"])
+        mb = nb
+        pools = {c: (torch.zeros((n_layers, nb, hkv, bs, d), device=dev), torch.zeros((n_layers, nb, hkv, bs, d),
+                                                                                      device=dev))
+                 for c in ("base", "draft")}
+        alloc = {c: DeviceBlockAllocator(nb, 1, mb, bs, dev) for c in ("base", "draft")}
+
+        def write_rows(c, li, start, kr, vr):
+            table = alloc[c].block_table[0].cpu().numpy()
+            for j in range(kr.shape[0]):
+                pos = start + j
+                blk, off = int(table[pos // bs]), pos % bs
+                pools[c][0][li, blk, :, off] = _cuda(kr[j].reshape(hkv, d), torch.float32)
+                pools[c][1][li, blk, :, off] = _cuda(vr[j].reshape(hkv, d), torch.float32)
+
+        def gather(c, li, n):
+            table = alloc[c].block_table[0].cpu().numpy()
+            kp, vp = pools[c][0][li].cpu().numpy(), pools[c][1][li].cpu().numpy()
+            ks = [kp[table[pos // bs], :, pos % bs].reshape(-1) for pos in range(n)]
+            vs = [vp[table[pos // bs], :, pos % bs].reshape(-1) for pos in range(n)]
+            return np.stack(ks), np.stack(vs)
+
+        for c, key in (("base", "ib"), ("draft", "id")):
+            alloc[c].ensure(_cuda([L - 1], torch.int32))
+            for li in range(n_layers):
+                write_rows(c, li, 0, g[p + f"{key}{li}"][0], g[p + f"{key}{li}"][1])
+        itape = g[p + "itape"]
+        cap = itape.shape[0] + int(g[p + "rounds"]) * (n_nodes + 1)
+        tape = torch.zeros((1, cap, dim), device=dev)
+        tape[0, :itape.shape[0]] = _cuda(itape, torch.float32)
+        tape_len = _cuda([itape.shape[0]], torch.int32)
+        err = torch.zeros((1,), dtype=torch.int32, device=dev)
+        for rd in range(int(g[p + "rounds"])):
+            q = f"{p}r{rd}_"
+            path = [int(x) for x in g[q + "path"]]
+            kept = int(g[q + "kept"])
+            for c in ("base", "draft"):
+                alloc[c].alloc_for_step(_cuda([L], torch.int32), n_nodes)
+            for li in range(n_layers):
+                write_rows("draft", li, L - 1, g[q + "align_k"], g[q + "align_v"])
+            pt = np.zeros((1, n_nodes + 1), dtype=np.int32)
+            pt[0, :len(path)] = path
+            pt, plen, nk, ctx = (_cuda(pt, torch.int32), _cuda([len(path)], torch.int32), _cuda([kept], torch.int32),
+                                 _cuda([L - 1], torch.int32))
+            bk = torch.stack([_cuda(g[q + f"bk{li}"].reshape(n_nodes + 1, hkv, d), torch.float32)
+                              for li in range(n_layers)])[:, None]
+            bv = torch.stack([_cuda(g[q + f"bv{li}"].reshape(n_nodes + 1, hkv, d), torch.float32)
+                              for li in range(n_layers)])[:, None]
+            sk = torch.stack([_cuda(g[q + f"sk{li}"].reshape(n_nodes, hkv, d), torch.float32)
+                              for li in range(n_layers)])[:, None]
+            sv = torch.stack([_cuda(g[q + f"sv{li}"].reshape(n_nodes, hkv, d), torch.float32)
+                              for li in range(n_layers)])[:, None]
+            compact_kv(bk, bv, pools["base"][0], pools["base"][1], alloc["base"].block_table, ctx, pt, plen, nk)
+            compact_draft_kv(sk, sv, pools["draft"][0], pools["draft"][1], alloc["draft"].block_table, ctx, pt, plen,
+                             nk)
+            tape_append(_cuda(g[q + "hid"][None], torch.float32), tape, tape_len, pt, plen, err, nk)
+            L = L + kept
+            for c in ("base", "draft"):
+                alloc[c].rewind(_cuda([L - 1], torch.int32))
+        torch.cuda.synchronize()
+        assert L == int(g[p + "final_len"]) and int(err[0]) == 0
+        for c in ("base", "draft"):
+            alloc[c].check()
+        assert [int(alloc[c].n_mapped[0]) for c in ("base", "draft")] == list(g[p + "blocks_used"])
+        for li in range(n_layers):
+            for c, key in (("base", "gb"), ("draft", "gd")):
+                gk, gv = gather(c, li, L - 1)
+                np.testing.assert_array_equal(gk, g[p + f"{key}{li}"][0].astype(np.float32))
+                np.testing.assert_array_equal(gv, g[p + f"{key}{li}"][1].astype(np.float32))
+        np.testing.assert_array_equal(tape[0, :int(tape_len[0])].cpu().numpy(), g[p + "tape"].astype(np.float32))

@@ -195,3 +195,29 @@ def test_draft_depth_attention_matches_reference(golden):
                                            g[p + "mask"], d ** -0.5, hq, hkv)
         np.testing.assert_allclose(out, g[p + "out"], atol=1e-12)
         np.testing.assert_allclose(lse, g[p + "lse"], atol=1e-12)
+
+
+def test_bookkeeping_replay_matches_reference(golden):
+    """Several rounds of base + draft cache write-back / rewind and the
+    hidden tape (engine.py:504-533) on logical rows == the reference caches'
+    gathers and tape."""
+    g = golden("bookkeep")
+    for k in range(int(g["n_cases"])):
+        p = f"b{k}_"
+        bs, hkv, d, n_layers, dim, nb, L = (int(x) for x in g[p + "meta"])
+        base = [[list(g[p + f"ib{li}"][0]), list(g[p + f"ib{li}"][1])] for li in range(n_layers)]
+        draft = [[list(g[p + f"id{li}"][0]), list(g[p + f"id{li}"][1])] for li in range(n_layers)]
+        tape = list(g[p + "itape"])
+        for rd in range(int(g[p + "rounds"])):
+            q = f"{p}r{rd}_"
+            L = O.bookkeep_round(base, draft, tape, L, list(g[q + "path"]), int(g[q + "kept"]),
+                                 [(g[q + f"bk{li}"], g[q + f"bv{li}"]) for li in range(n_layers)],
+                                 [(g[q + f"sk{li}"], g[q + f"sv{li}"]) for li in range(n_layers)], g[q + "hid"],
+                                 [(g[q + "align_k"][0], g[q + "align_v"][0])] * n_layers)
+        assert L == int(g[p + "final_len"])
+        for li in range(n_layers):
+            np.testing.assert_array_equal(np.stack(base[li][0]), g[p + f"gb{li}"][0])
+            np.testing.assert_array_equal(np.stack(base[li][1]), g[p + f"gb{li}"][1])
+            np.testing.assert_array_equal(np.stack(draft[li][0]), g[p + f"gd{li}"][0])
+            np.testing.assert_array_equal(np.stack(draft[li][1]), g[p + f"gd{li}"][1])
+        np.testing.assert_array_equal(np.stack(tape), g[p + "tape"])

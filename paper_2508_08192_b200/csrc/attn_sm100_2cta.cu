@@ -20,7 +20,10 @@ namespace sdb {
 namespace sm100 {
 
 constexpr int kStagesK = 6;  // K ring: S(n) is issued ~3 items before its PV, so K needs the deeper ring
-constexpr int kStagesV = 3;  // (3 suffice: V(n) is consumed by PV(n), ~3 items after its load is issued)
+#ifndef SDB_STAGES_V
+#define SDB_STAGES_V 3
+#endif
+constexpr int kStagesV = SDB_STAGES_V;  // (3 suffice: V(n) is consumed by PV(n), ~3 items after its load is issued)
 
 #ifdef SDB_TRACE
 // [event][iteration] clock64 stamps of worker 0 (debug builds only)
@@ -122,7 +125,7 @@ __host__ __device__ constexpr uint32_t make_idesc2(bool b_mn_major) {
          ((uint32_t)(256 >> 4) << 24);
 }
 
-constexpr int kLgStages = 5;     // fused argmax: 5 x 8 KB bulk-copy ring
+constexpr int kLgStages = kStagesV == 3 ? 5 : 3;  // fused argmax: 8 KB bulk-copy ring in the SMEM left over
 constexpr int kLgChunk = 2048;   // floats per chunk
 
 struct alignas(1024) Smem2 {

@@ -129,6 +129,14 @@ typedef struct sdb_tree_attn_args {
   int fused_vocab;
   int64_t *fused_keys;        /* [batch * r_max]                              */
   int32_t *fused_err;         /* NaN -> SDB_ERR_NAN                           */
+  int chunk_len;              /* iRoPE local attention (attention.py:33-40,
+                                 76-84): 0 = none; else every tree row sees the
+                                 prefix keys [floor(C / chunk) * chunk, C) --
+                                 exact when the tree was truncated at the
+                                 chunk boundary (truncate_draft_at_boundary,
+                                 attention.py:189-206; engine.py:486-487).
+                                 tcgen05 path: chunk % 128 == 0 and
+                                 chunk % block_size == 0, else SIMT */
 } sdb_tree_attn_args;
 
 /* The kernel launched just before on the stream is sdb_tree_build (the only

@@ -228,7 +228,7 @@ def paged_write(pool, block_table, start, rows):
 
 
 def tree_verify_attention_batch(q, k_pool, v_pool, block_table, ctx_len, tree_k, tree_v,
-                                parents, scale):
+                                parents, scale, chunk_len=None):
     """Batched oracle of the device op ``tree_verify_attn``.
 
     q (B, R, Hq, d); pools (nb, Hkv, bs, d); tree_k/v (B, R, Hkv, d);
@@ -247,7 +247,7 @@ def tree_verify_attention_batch(q, k_pool, v_pool, block_table, ctx_len, tree_k,
         cv = paged_gather(v_pool, block_table[b], c)
         o, l = tree_attention(q[b, :n].reshape(n, hq * d), ck, cv,
                               tree_k[b, :n].reshape(n, hkv * d), tree_v[b, :n].reshape(n, hkv * d),
-                              parents[b], scale, hq, hkv)
+                              parents[b], scale, hq, hkv, chunk_len)
         out[b, :n] = o.reshape(n, hq, d)
         lse[b, :, :n] = l
     return out, lse

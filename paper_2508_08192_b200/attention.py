@@ -247,7 +247,7 @@ class TreeVerifyAttention:
 
     def _args(self, q, k_cache, v_cache, block_table, ctx_len, tree_k, tree_v, mask_words, n_rows, scale,
                  out=None, lse=None, max_ctx=None, num_splits=0, kernel=KERNEL_AUTO, stream=None, q_row0=None,
-                 max_q_nodes=None, after_tree_build=False, fused_argmax=None):
+                 max_q_nodes=None, after_tree_build=False, fused_argmax=None, chunk_len=None):
         import torch
 
         b, r, hq, d = q.shape
@@ -283,6 +283,8 @@ class TreeVerifyAttention:
             a.q_row0 = q_row0.data_ptr()
         if max_q_nodes is not None:
             a.max_q_nodes = int(max_q_nodes)
+        if chunk_len:  # iRoPE: every row sees prefix keys [floor(C / chunk) * chunk, C)
+            a.chunk_len = int(chunk_len)
         if after_tree_build:  # the previous kernel on `stream` is tree_build: PDL launch
             a.flags |= _lib.ATTN_FLAG_PDL
         if fused_argmax is not None:

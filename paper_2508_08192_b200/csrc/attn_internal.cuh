@@ -16,6 +16,7 @@ struct TreeAttnParams {
   float *ws_lse;  // [splits][B][hq][r_max]
   int batch, r_max, n_words, hq, hkv, head_dim, block_size, num_blocks, max_blocks, max_ctx;
   int max_q_nodes;  // query nodes per sequence (<= r_max); plans the row blocks
+  int chunk_len;    // iRoPE local chunk: prefix keys [floor(C / chunk) * chunk, C); 0 = all
   int pdl;          // launch the tcgen05 kernel as a programmatic dependent of the previous kernel
   // fused greedy-acceptance scan (idle warp of the pair kernel): packed
   // argmax keys of the fp32 logits rows [B][r_max][vocab] (n_rows gated)
@@ -30,6 +31,10 @@ struct TreeAttnParams {
 
 // First query row of sequence b: rows [q0, n_rows) attend, keys are all the
 // tree rows [0, n_rows) (the draft stage's depth step, engine.py:424-432).
+__device__ __forceinline__ int prefix_start(const TreeAttnParams &p, int ctx) {
+  return p.chunk_len > 0 ? (ctx / p.chunk_len) * p.chunk_len : 0;
+}
+
 __device__ __forceinline__ int q_first(const TreeAttnParams &p, int b, int n_nodes) {
   return p.q_row0 ? min(max(p.q_row0[b], 0), n_nodes) : 0;
 }

@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) tree_attn_simt_kernel(TreeAtt
     return;
   }
   const int C = p.ctx_len[b];
+  const int kstart = prefix_start(p, C);  // iRoPE: prefix keys [kstart, C)
   const int T_keys = C + n_nodes;
   // split range, tile aligned
   const int tiles = cdiv(T_keys, kSimtKeys);
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) tree_attn_simt_kernel(TreeAtt
 #pragma unroll
     for (int r = 0; r < kSimtRowsPerWarp; ++r) {
       int rho = row0 + wrow0 + r;
-      bool vis = key < T_keys && rho < rows_total;
+      bool vis = key < T_keys && rho < rows_total && key >= kstart;
       if (vis && key >= C) {
         int node = q0 + rho / g, j = key - C;
         uint32_t w = p.mask_words[((int64_t)b * p.r_max + node) * p.n_words + (j >> 5)];

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
             if (pref) {
               const CUtensorMap *m = kv ? &tm_v : &tm_k;
               for (int r0 = 0; r0 < kTileN; r0 += seg_rows) {
-                const int key = tile * kTileN + r0;
+                const int key = geo.k0 + tile * kTileN + r0;
                 const int lp = key / bs;
                 const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;  // OOB page -> zero fill
                 const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
       for (int it = 0; it < geo.n_tiles; ++it) {
         const uint32_t gt = g_tile + it;
         const bool pref = it < geo.n_pref;
-        const int key0 = pref ? (geo.pa + it) * kTileN : (geo.sa + it - geo.n_pref) * kTileN;
+        const int key0 = pref ? geo.k0 + (geo.pa + it) * kTileN : (geo.sa + it - geo.n_pref) * kTileN;
         const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
         mbar_wait(&sm.s_full[t], gt & 1);
         tc_fence_after();
@@ -386,6 +386,8 @@ bool tree_attn_sm100_supported(const TreeAttnParams &p) {
        reinterpret_cast<uintptr_t>(p.tree_v)) & 15)
     return false;
   if (p.r_max > 128) return false;  // one suffix tile (<= 4 mask words)
+  // local chunks must start on a key tile and a page boundary
+  if (p.chunk_len > 0 && (p.chunk_len % sm100::kTileN != 0 || p.chunk_len % p.block_size != 0)) return false;
   int dev = 0, major = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
@@ -409,7 +411,8 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   sp.rows_unit = sp.nt * per_tile;
   sp.m_blocks = cdiv(rows, sp.rows_unit);
   sp.units = p.batch * p.hkv * sp.m_blocks;
-  sp.w_pref = cdiv(max(p.max_ctx, 0), kTileN);
+  // nominal prefix tiles per unit: the context, or at most one local chunk
+  sp.w_pref = cdiv(max(p.chunk_len > 0 ? std::min(p.max_ctx, p.chunk_len) : p.max_ctx, 0), kTileN);
   sp.w_unit = sp.w_pref + cdiv(p.r_max, kTileN);
   sp.total = (int64_t)sp.units * sp.w_unit;
   int n = ctas_override > 0 ? ctas_override : num_sms() / sp.cta_group;

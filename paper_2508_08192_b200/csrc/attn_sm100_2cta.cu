@@ -352,7 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const uint32_t l_kfull = leader_addr(&sm.k_full[s]);
             if (pref) {
               for (int r0 = 0; r0 < 64; r0 += seg_rows) {
-                const int key = tile * kTileN + (int)rank * 64 + r0;
+                const int key = geo.k0 + tile * kTileN + (int)rank * 64 + r0;
                 const int lp = key / bs;
                 const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;  // OOB page -> zero fill
                 const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
@@ -371,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const uint32_t l_vfull = leader_addr(&sm.v_full[s]);
             if (pref) {
               for (int r0 = 0; r0 < kTileN; r0 += seg_rows) {
-                const int key = tile * kTileN + r0;
+                const int key = geo.k0 + tile * kTileN + r0;
                 const int lp = key / bs;
                 const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;
                 const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
@@ -585,7 +585,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const uint32_t gi = g_item + n;
         const int slot = wg;
         const bool pref = n < geo.n_pref;
-        const int key0 = pref ? (geo.pa + n) * kTileN : (geo.sa + n - geo.n_pref) * kTileN;
+        const int key0 = pref ? geo.k0 + (geo.pa + n) * kTileN : (geo.sa + n - geo.n_pref) * kTileN;
         const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
         const bool full = pref && kvalid >= kTileN;
         if (tr) TRACE(3, gi);

@@ -319,6 +319,7 @@ struct ItemIter {
 struct ItemGeo {
   int b, kvh, row0, n_nodes, rows_total, C;
   int q0;  // first query node; query row rho is node q0 + rho / g
+  int k0;  // first prefix key (iRoPE local chunk start; 0 without chunking)
   int pa, n_pref, sa, n_suf, n_tiles;
   bool active;
 };
@@ -337,7 +338,8 @@ __device__ __forceinline__ ItemGeo item_geo(const Sm100Params &sp, const Item &i
   o.q0 = q_first(p, o.b, o.n_nodes);
   o.rows_total = (o.n_nodes - o.q0) * g;
   o.C = p.ctx_len[o.b];
-  const int pb = (o.C + kTileN - 1) / kTileN;
+  o.k0 = prefix_start(p, o.C);
+  const int pb = (o.C - o.k0 + kTileN - 1) / kTileN;
   const int sb = (o.n_nodes + kTileN - 1) / kTileN;
   o.pa = min(it.t0, pb);
   const int pe = min(min(it.t1, sp.w_pref), pb);

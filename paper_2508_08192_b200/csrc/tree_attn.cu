@@ -30,6 +30,7 @@ static bool fill_params(const sdb_tree_attn_args *a, TreeAttnParams &p) {
   p.q_row0 = a->q_row0;
   p.max_q_nodes = (a->max_q_nodes > 0 && a->max_q_nodes < a->r_max) ? a->max_q_nodes : a->r_max;
   p.pdl = (a->flags & SDB_ATTN_FLAG_PDL) != 0;
+  p.chunk_len = a->chunk_len > 0 ? a->chunk_len : 0;
   p.fa_logits = nullptr;
   p.fa_keys = nullptr;
   p.fa_err = nullptr;

@@ -54,13 +54,15 @@ def _num_sms(device):
 
 
 class TreeVerifier:
-    def __init__(self, scale, temperature=0.0, top_p=1.0, max_ctx=None, num_splits=0, kernel=0, fuse_greedy=True):
+    def __init__(self, scale, temperature=0.0, top_p=1.0, max_ctx=None, num_splits=0, kernel=0, fuse_greedy=True,
+                 chunk_len=None):
         self.scale = scale
         self.temperature = temperature
         self.top_p = top_p
         self.max_ctx = max_ctx
         self.num_splits = num_splits
         self.kernel = kernel
+        self.chunk_len = chunk_len  # iRoPE local chunk (tree truncated at the boundary by the caller)
         self.fuse_greedy = fuse_greedy  # greedy scan inside the attention kernel: True (when it hides), "always", False
         self.attn = TreeVerifyAttention()
         self.greedy = GreedyAcceptor()
@@ -102,7 +104,7 @@ class TreeVerifier:
         attn_args = (x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
                      self.scale)
         attn_kw = dict(out=o["out"], lse=o["lse"], max_ctx=self.max_ctx, num_splits=self.num_splits,
-                       kernel=self.kernel)
+                       kernel=self.kernel, chunk_len=self.chunk_len)
         # small batches: the attention's persistent grid leaves SMs free ->
         # run acceptance beside it; full occupancy -> fold the greedy scan
         # into the attention kernel (its otherwise idle warp + TMA ring)

@@ -760,3 +760,42 @@ def test_device_bookkeeping_replays_reference_rounds(golden):
                 np.testing.assert_array_equal(gk, g[p + f"{key}{li}"][0].astype(np.float32))
                 np.testing.assert_array_equal(gv, g[p + f"{key}{li}"][1].astype(np.float32))
         np.testing.assert_array_equal(tape[0, :int(tape_len[0])].cpu().numpy(), g[p + "tape"].astype(np.float32))
+
+
+@pytest.mark.parametrize("chunk,kernel", [(512, 1), (512, 2), (384, 0)])
+def test_tree_verify_attention_irope_local_chunk(chunk, kernel):
+    """iRoPE local attention: with the tree truncated at
+    the chunk boundary (truncate_draft_at_boundary), every row sees prefix
+    keys [floor(C / chunk) * chunk, C) -- vs the oracle's LocalChunk mask
+    (attention.py:76-84); includes an empty local prefix (C on a boundary).
+    chunk 384 is not a tile multiple: the auto path takes the SIMT kernel."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+    from paper_2508_08192_b200.drafttree import tree_build
+
+    B, Hq, Hkv, d, bs = 4, 64, 8, 128, 64
+    aug = O.augment(tuple(TREE64))
+    R = len(aug)
+    rng = np.random.default_rng(chunk)
+    ctx = np.array([3 * chunk + 17, chunk, 2 * chunk + chunk - 8, 5 * chunk + 100], dtype=np.int32)
+    pages = -(-(int(ctx.max()) + R) // bs)
+    nb = B * pages + 3
+    table = rng.permutation(nb)[:B * pages].reshape(B, pages).astype(np.int32)
+    gen = torch.Generator(device="cuda").manual_seed(chunk)
+    kp = torch.randn((nb, Hkv, bs, d), generator=gen, device="cuda").to(torch.bfloat16)
+    vp = torch.randn((nb, Hkv, bs, d), generator=gen, device="cuda").to(torch.bfloat16)
+    q = torch.randn((B, R, Hq, d), generator=gen, device="cuda").to(torch.bfloat16)
+    tk = torch.randn((B, R, Hkv, d), generator=gen, device="cuda").to(torch.bfloat16)
+    tv = torch.randn((B, R, Hkv, d), generator=gen, device="cuda").to(torch.bfloat16)
+    par = torch.tensor([list(aug)] * B, dtype=torch.int32, device="cuda")
+    nr = torch.full((B,), R, dtype=torch.int32, device="cuda")
+    ctx_t = torch.tensor(ctx, device="cuda")
+    mask, _, _, _ = tree_build(par, nr, ctx_t)
+    out, lse = tree_verify_attention(q, kp, vp, torch.tensor(table, device="cuda"), ctx_t, tk, tv, mask, nr,
+                                     d ** -0.5, kernel=kernel, chunk_len=chunk)
+    torch.cuda.synchronize()
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(q), f64(kp), f64(vp), table, ctx, f64(tk), f64(tv),
+                                                   [aug] * B, d ** -0.5, chunk_len=chunk)
+    err = np.abs(out.float().cpu().numpy() - want_o)
+    assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+    assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3

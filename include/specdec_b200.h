@@ -184,6 +184,18 @@ int sdb_accept_greedy(const void *logits, int dtype, int batch, int r_max, int v
                       int64_t *next_token, int32_t *uniforms_used, int32_t *err,
                       void *stream);
 
+/* Greedy acceptance over FSM-masked rows (guided decoding: target_dist(row,
+ * 0, ., allowed), sampling.py:94-99 -- the argmax of the ALLOWED logits;
+ * engine.py:465-475 gives each tree row the FSM state after its token).
+ * allowed uint32 [B][r_max][allowed_words], bit j of word w = token 32 w + j
+ * allowed; NULL = sdb_accept_greedy (fp32).  A row with no allowed token sets
+ * SDB_ERR_NO_ALLOWED.  keys: batch * r_max int64. */
+int sdb_accept_greedy_ex(const float *logits, int batch, int r_max, int vocab, int64_t row_stride,
+                         const int32_t *parent, const int32_t *n_rows, const int32_t *tokens,
+                         const uint32_t *allowed, int allowed_words, int64_t *keys, int32_t *path,
+                         int32_t *path_len, int64_t *next_token, int32_t *uniforms_used, int32_t *err,
+                         void *stream);
+
 /* ---- K4/K5: stochastic (T > 0) acceptance ------------------------------
  * Replaces target_dist(row, T, top_p) for every tree row, the draft q
  * target_dist(draft_row, T, 1.0) (engine.py:266-269; siblings share their
@@ -264,6 +276,16 @@ typedef struct sdb_sharded_accept_args {
 
 int sdb_sharded_accept_sizes(const sdb_sharded_accept_args *a, int64_t *sizes /* [SDB_SH_N_BUFS] */);
 int sdb_sharded_accept_phase(const sdb_sharded_accept_args *a, int phase, int level, void *stream);
+
+/* sdb_accept_stochastic with FSM masks: allowed (as in sdb_accept_greedy_ex)
+ * masks row r's target dist AND the q its children were drafted from (the
+ * same FSM state, engine.py:266-269, 465-475); NULL = unmasked. */
+int sdb_accept_stochastic_ex(const float *target_logits, const float *draft_logits, int batch, int r_max,
+                             int vocab, float temperature, float top_p, const int32_t *parent,
+                             const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
+                             int n_uniforms, void *workspace, int64_t workspace_bytes, int32_t *path,
+                             int32_t *path_len, int64_t *next_token, int32_t *uniforms_used, float *residual,
+                             int32_t *err, const uint32_t *allowed, int allowed_words, void *stream);
 
 /* ---- uniforms: device Philox4x64-10 ----------------------------------------
  * Replaces rank_sliced_uniforms (sampling.py:112-124) as the engine consumes

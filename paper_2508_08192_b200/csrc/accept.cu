@@ -179,6 +179,38 @@ __global__ void __launch_bounds__(kArgmaxThreads, 2) argmax_keys_kernel(const T 
   if (threadIdx.x == 0) keys[row * split + seg] = best;
 }
 
+// Greedy acceptance over FSM-masked rows (target_dist(row, 0, ., allowed),
+// sampling.py:94-99: the argmax of the ALLOWED logits, lowest index on ties;
+// a row with no allowed token is SamplingError).  Simple per-element keys:
+// the unmasked rows keep the chunk-max fast path above.
+__global__ void __launch_bounds__(kArgmaxThreads) argmax_keys_masked_kernel(
+    const float *__restrict__ logits, int vocab, int64_t row_stride, const int32_t *__restrict__ n_rows, int r_max,
+    const uint32_t *__restrict__ allowed, int n_mw, long long *__restrict__ keys, int32_t *__restrict__ err) {
+  __shared__ long long red[kArgmaxThreads / 32];
+  const int r = blockIdx.x, b = blockIdx.y;
+  if (r >= n_rows[b]) return;
+  const int64_t row = (int64_t)b * r_max + r;
+  const float *lr = logits + row * row_stride;
+  const uint32_t *mw = allowed + row * n_mw;
+  long long best = LLONG_MIN;
+  bool nan = false, any = false;
+  for (int j = threadIdx.x; j < vocab; j += kArgmaxThreads) {
+    if (!((__ldg(mw + (j >> 5)) >> (j & 31)) & 1u)) continue;
+    any = true;
+    const float e = lr[j];
+    nan |= e != e;
+    const long long k = argmax_key(e, (uint32_t)j);
+    best = k > best ? k : best;
+  }
+  best = block_max_i64<kArgmaxThreads>(best, red);
+  const bool any_b = __syncthreads_or(any);
+  if (__syncthreads_or(nan) && threadIdx.x == 0) atomicOr(err, SDB_ERR_NAN);
+  if (threadIdx.x == 0) {
+    if (!any_b) atomicOr(err, SDB_ERR_NO_ALLOWED);
+    keys[row * 1] = best;
+  }
+}
+
 // One warp per sequence: the argmax walk in the augmented frame (row 0 =
 // root; children of row r = rows j > r with parent[j] == r, index order).
 __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int32_t *__restrict__ parent,
@@ -296,9 +328,27 @@ struct StSmem {
   double tot;
 };
 
+// Guided-decoding masks (target_dist(allowed=...), sampling.py:94-97): one
+// bit per token, word j of a row covers tokens [32 j, 32 j + 32); a cleared
+// bit turns the logit into -inf before anything else (nullptr = all allowed).
+__device__ __forceinline__ float4 mask4(float4 v, const uint32_t *mw, int i4) {
+  if (mw) {
+    const uint32_t bits = (__ldg(mw + (i4 >> 3)) >> ((i4 & 7) * 4)) & 0xFu;
+    if (!(bits & 1u)) v.x = -INFINITY;
+    if (!(bits & 2u)) v.y = -INFINITY;
+    if (!(bits & 4u)) v.z = -INFINITY;
+    if (!(bits & 8u)) v.w = -INFINITY;
+  }
+  return v;
+}
+__device__ __forceinline__ float mask1(float v, const uint32_t *mw, int j) {
+  return (mw && !((__ldg(mw + (j >> 5)) >> (j & 31)) & 1u)) ? -INFINITY : v;
+}
+
 // Streaming max (+ NaN flag) of a row: 4 independent 16-byte loads in flight
 // per thread.
-__device__ __forceinline__ void row_max_nan(const float *row, int vocab, bool vec, float &mx, bool &nan) {
+__device__ __forceinline__ void row_max_nan(const float *row, int vocab, bool vec, float &mx, bool &nan,
+                                            const uint32_t *mw) {
   mx = -INFINITY;
   nan = false;
   if (vec) {
@@ -308,7 +358,7 @@ __device__ __forceinline__ void row_max_nan(const float *row, int vocab, bool ve
     for (; i + 3 * kStThreads < n4; i += 4 * kStThreads) {
       float4 v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(r4 + i + u * kStThreads);
+      for (int u = 0; u < 4; ++u) v[u] = mask4(__ldg(r4 + i + u * kStThreads), mw, i + u * kStThreads);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         nan |= (v[u].x != v[u].x) | (v[u].y != v[u].y) | (v[u].z != v[u].z) | (v[u].w != v[u].w);
@@ -316,18 +366,18 @@ __device__ __forceinline__ void row_max_nan(const float *row, int vocab, bool ve
       }
     }
     for (; i < n4; i += kStThreads) {
-      const float4 v = __ldg(r4 + i);
+      const float4 v = mask4(__ldg(r4 + i), mw, i);
       nan |= (v.x != v.x) | (v.y != v.y) | (v.z != v.z) | (v.w != v.w);
       mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
     }
     for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) {
-      const float v = row[j];
+      const float v = mask1(row[j], mw, j);
       nan |= v != v;
       mx = fmaxf(mx, v);
     }
   } else {
     for (int j = threadIdx.x; j < vocab; j += kStThreads) {
-      const float v = row[j];
+      const float v = mask1(row[j], mw, j);
       nan |= v != v;
       mx = fmaxf(mx, v);
     }
@@ -397,10 +447,11 @@ __device__ double exact_cut(StSmem &sm, int count, double mass_above, double tau
 // one pass that sums the exact (f64) mass above the bins straddling the cut
 // and collects their few elements, which are sorted exactly by (key desc,
 // index asc) -- the reference's top_p_mask order (sampling.py:57-72).
+template <bool kMasked>
 __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
     float top_p, const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows,
-    RowStats *__restrict__ stats, int32_t *__restrict__ err) {
+    RowStats *__restrict__ stats, int32_t *__restrict__ err, const uint32_t *__restrict__ allowed, int n_mw) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   StSmem &sm = *reinterpret_cast<StSmem *>(smem_raw);
   const int r = blockIdx.x, b = blockIdx.y, is_draft = blockIdx.z;
@@ -421,6 +472,9 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     }
   }
   const float *row = (is_draft ? draft : target) + ((int64_t)b * r_max + r) * vocab;
+  // the row's FSM mask masks its target dist and the q its children were
+  // drafted from alike (engine.py:465-475, 266-269: same FSM state)
+  const uint32_t *mw = kMasked ? allowed + ((int64_t)b * r_max + r) * n_mw : nullptr;
   const bool vec = (vocab & 3) == 0 && ((uintptr_t)row & 15) == 0;
   const bool nucleus = !is_draft && top_p < 1.0f;
   // the whole row streams into L2 through the TMA engine (deep memory-level
@@ -442,12 +496,12 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int i = i0 + u * kStThreads + threadIdx.x;
-      v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) mx = max3_nan(mx, max3_nan(v[u].x, v[u].y, v[u].z), v[u].w);
   }
-  for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) mx = max3_nan(mx, row[j], row[j]);
+  for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) mx = max3_nan(mx, mask1(row[j], mw, j), mask1(row[j], mw, j));
   if (__syncthreads_or(mx != mx)) {
     if (threadIdx.x == 0) {
       atomicOr(err, SDB_ERR_NAN);
@@ -456,6 +510,13 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     return;
   }
   mx = block_max<kStThreads>(mx, sm.redf);
+  if (mx == -INFINITY) {  // no allowed token (dead FSM state, sampling.py:96-97) / no finite logit
+    if (threadIdx.x == 0) {
+      atomicOr(err, mw ? SDB_ERR_NO_ALLOWED : SDB_ERR_BAD_DIST);
+      out->valid = 0;
+    }
+    return;
+  }
   const float m2 = mx * a;
   if (!nucleus) {
     // draft rows (and top_p = 1): the normaliser, two elements per packed op
@@ -466,7 +527,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kStThreads + threadIdx.x;
-        v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -479,7 +540,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     float s_lo, s_hi;
     f2unpack(s2, s_lo, s_hi);
     float s_loc = s_lo + s_hi;
-    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) s_loc += ex2(fmaf(row[j], a, -m2));
+    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) s_loc += ex2(fmaf(mask1(row[j], mw, j), a, -m2));
     const double s = block_sum<kStThreads>((double)s_loc, sm.red);
     if (threadIdx.x == 0) {
       RowStats st;
@@ -529,7 +590,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int i = i0 + u * kStThreads + threadIdx.x;
-      v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -541,7 +602,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   f2unpack(s2, s_lo, s_hi);
   float s_loc = s_lo + s_hi;
   for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) {
-    const float x = row[j];
+    const float x = mask1(row[j], mw, j);
     const uint64_t l2 = f2pack(x, -INFINITY);
     s2 = 0;
     acc2(l2);
@@ -618,7 +679,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kStThreads + threadIdx.x;
-        v[u] = i < n4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       }
       uint32_t mask = 0;  // bit 4u+e: element e of v[u] lies in the window
 #pragma unroll
@@ -656,7 +717,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
       float x = 0.f;
       int cnt = 0;
       if (j < vocab) {
-        x = row[j];
+        x = mask1(row[j], mw, j);
         float d0, d1, e0, e1;
         const uint64_t l2 = f2pack(x, x);
         f2unpack(ffma2(l2, DA2, DM2), d0, d1);
@@ -691,7 +752,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
       if (threadIdx.x == 0) sm.count = 0;
       __syncthreads();
       for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-        const uint32_t k = prob_key(row[i]);
+        const uint32_t k = prob_key(mask1(row[i], mw, i));
         if (k >= klo && k <= khi) {
           const int slot = atomicAdd(&sm.count, 1);
           if (slot < kCandCap) sm.cand[slot] = ((unsigned long long)k << 32) | (0xffffffffu - (uint32_t)i);
@@ -723,7 +784,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
       long long seen = 0;
       for (int c0 = 0; c0 < vocab; c0 += kStThreads) {
         const int i = c0 + threadIdx.x;
-        const bool t = i < vocab && prob_key(row[i]) == klo;
+        const bool t = i < vocab && prob_key(mask1(row[i], mw, i)) == klo;
         const double pre = block_inclusive_scan(t ? 1.0 : 0.0, sm.red);
         if (t && seen + (long long)pre == need) sm.idx = i;
         if (threadIdx.x == kStThreads - 1) sm.tot = pre;
@@ -743,7 +804,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     __syncthreads();
     const unsigned long long span = (unsigned long long)(khi - klo) + 1ull;
     for (int i = threadIdx.x; i < vocab; i += kStThreads) {
-      const float l = row[i];
+      const float l = mask1(row[i], mw, i);
       const uint32_t k = prob_key(l);
       if (k >= klo && k <= khi) {
         const int bin = (int)(((unsigned long long)(khi - k) * kRefBins) / span);
@@ -801,6 +862,7 @@ struct WalkRow {
   float p_off, q_off;  // -(m2 + log2 Z) of the target / draft softmax
   float cut_l;         // nucleus cut logit (keys above are kept; ties by index)
   int cut_idx, keep_all;
+  const uint32_t *mw;  // FSM allowed-token bits of the row (nullptr = all)
 };
 
 __device__ __forceinline__ float key_to_logit(uint32_t k) {
@@ -813,8 +875,12 @@ __device__ __forceinline__ float p_val(const WalkRow &w, float a, float l, int i
   return keep ? ex2(fmaf(l, a, w.p_off)) : 0.f;
 }
 __device__ __forceinline__ float q_val(const WalkRow &w, float a, float d) { return ex2(fmaf(d, a, w.q_off)); }
-__device__ __forceinline__ float p_of(const WalkRow &w, float a, int t) { return p_val(w, a, w.tl[t], t); }
-__device__ __forceinline__ float q_of(const WalkRow &w, float a, int t) { return w.dl ? q_val(w, a, w.dl[t]) : 0.f; }
+__device__ __forceinline__ float p_of(const WalkRow &w, float a, int t) {
+  return p_val(w, a, mask1(w.tl[t], w.mw, t), t);
+}
+__device__ __forceinline__ float q_of(const WalkRow &w, float a, int t) {
+  return w.dl ? q_val(w, a, mask1(w.dl[t], w.mw, t)) : 0.f;
+}
 
 // sum over [v0, v1) of max(P - c Q, 0) / M (per-element fp32, f64
 // accumulation), with the values optionally stored (residual); 16-byte
@@ -839,17 +905,18 @@ __device__ __forceinline__ double residual_part(const WalkRow &w, float a, doubl
     const int n4 = (v1 - v0) >> 2;
 #pragma unroll 4
     for (int i = threadIdx.x; i < n4; i += kWThreads) {
-      const float4 t = __ldg(t4 + i);
-      const float4 d = d4 ? __ldg(d4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 t = mask4(__ldg(t4 + i), w.mw, (v0 >> 2) + i);
+      const float4 d = d4 ? mask4(__ldg(d4 + i), w.mw, (v0 >> 2) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
       const int base = v0 + 4 * i;
       one(t.x, d.x, base);
       one(t.y, d.y, base + 1);
       one(t.z, d.z, base + 2);
       one(t.w, d.w, base + 3);
     }
-    for (int i = v0 + (n4 << 2) + threadIdx.x; i < v1; i += kWThreads) one(tl[i], dl ? dl[i] : 0.f, i);
+    for (int i = v0 + (n4 << 2) + threadIdx.x; i < v1; i += kWThreads)
+      one(mask1(tl[i], w.mw, i), dl ? mask1(dl[i], w.mw, i) : 0.f, i);
   } else {
-    for (int i = v0 + threadIdx.x; i < v1; i += kWThreads) one(tl[i], dl ? dl[i] : 0.f, i);
+    for (int i = v0 + threadIdx.x; i < v1; i += kWThreads) one(mask1(tl[i], w.mw, i), dl ? mask1(dl[i], w.mw, i) : 0.f, i);
   }
   return part;
 }
@@ -867,13 +934,14 @@ __device__ __forceinline__ void cluster_exchange(double v, double *slots, int &p
   ++phase;
 }
 
-template <int kCl>
+template <int kCl, bool kMasked>
 __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
     const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, const int32_t *__restrict__ tokens,
     const double *__restrict__ uniforms, int n_uniforms, const RowStats *__restrict__ stats,
     int32_t *__restrict__ path, int32_t *__restrict__ path_len, int64_t *__restrict__ next_token,
-    int32_t *__restrict__ uniforms_used, float *__restrict__ residual, int32_t *__restrict__ err) {
+    int32_t *__restrict__ uniforms_used, float *__restrict__ residual, int32_t *__restrict__ err,
+    const uint32_t *__restrict__ allowed, int n_mw) {
   __shared__ double red[32];
   __shared__ double slots[2];
   __shared__ int s_flag;
@@ -918,6 +986,7 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     w.keep_all = ts.keep_all;
     w.cut_l = key_to_logit(ts.cut_key);
     w.cut_idx = ts.cut_idx;
+    w.mw = kMasked ? allowed + ((int64_t)b * r_max + r) * n_mw : nullptr;
     // this CTA's slices of the node's rows stream into L2 while the
     // (latency-bound) sibling decisions run
     if (vec && threadIdx.x == 0 && v1 > v0) {
@@ -1111,6 +1180,28 @@ extern "C" int sdb_greedy_walk(const int64_t *keys, const int32_t *parent, const
   return SDB_OK;
 }
 
+extern "C" int sdb_accept_greedy_ex(const float *logits, int batch, int r_max, int vocab, int64_t row_stride,
+                                    const int32_t *parent, const int32_t *n_rows, const int32_t *tokens,
+                                    const uint32_t *allowed, int allowed_words, int64_t *keys, int32_t *path,
+                                    int32_t *path_len, int64_t *next_token, int32_t *uniforms_used, int32_t *err,
+                                    void *stream) {
+  if (!allowed)
+    return sdb_accept_greedy(logits, SDB_DTYPE_F32, batch, r_max, vocab, row_stride, parent, n_rows, tokens, keys,
+                             path, path_len, next_token, uniforms_used, err, stream);
+  if (!logits || !keys || !parent || !n_rows || !tokens || !err || batch < 0 || r_max < 1 || vocab < 1 ||
+      row_stride < vocab || allowed_words < (vocab + 31) / 32)
+    return SDB_E_INVALID;
+  if (batch == 0) return SDB_OK;
+  cudaStream_t s = sdb::as_stream(stream);
+  sdb::argmax_keys_masked_kernel<<<dim3(r_max, batch), sdb::kArgmaxThreads, 0, s>>>(
+      logits, vocab, row_stride, n_rows, r_max, allowed, allowed_words, (long long *)keys, err);
+  SDB_CHECK_LAUNCH();
+  sdb::greedy_walk_kernel<<<sdb::cdiv(batch * 32, 128), 128, 0, s>>>(
+      (const long long *)keys, parent, n_rows, tokens, batch, r_max, path, path_len, next_token, uniforms_used, 1);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
 extern "C" int sdb_accept_greedy(const void *logits, int dtype, int batch, int r_max, int vocab,
                                  int64_t row_stride, const int32_t *parent, const int32_t *n_rows,
                                  const int32_t *tokens, int64_t *keys, int32_t *path, int32_t *path_len,
@@ -1155,6 +1246,19 @@ extern "C" int sdb_accept_stochastic(const float *target_logits, const float *dr
                                      int n_uniforms, void *workspace, int64_t workspace_bytes, int32_t *path,
                                      int32_t *path_len, int64_t *next_token, int32_t *uniforms_used,
                                      float *residual, int32_t *err, void *stream) {
+  return sdb_accept_stochastic_ex(target_logits, draft_logits, batch, r_max, vocab, temperature, top_p, parent, n_rows,
+                                  tokens, uniforms, n_uniforms, workspace, workspace_bytes, path, path_len,
+                                  next_token, uniforms_used, residual, err, nullptr, 0, stream);
+}
+
+extern "C" int sdb_accept_stochastic_ex(const float *target_logits, const float *draft_logits, int batch, int r_max,
+                                        int vocab, float temperature, float top_p, const int32_t *parent,
+                                        const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
+                                        int n_uniforms, void *workspace, int64_t workspace_bytes, int32_t *path,
+                                        int32_t *path_len, int64_t *next_token, int32_t *uniforms_used,
+                                        float *residual, int32_t *err, const uint32_t *allowed, int allowed_words,
+                                        void *stream) {
+  if (allowed && allowed_words < (vocab + 31) / 32) return SDB_E_INVALID;
   if (!target_logits || !draft_logits || !parent || !n_rows || !tokens || !uniforms || !path || !path_len ||
       !next_token || !uniforms_used || !err || batch < 0 || r_max < 1 || vocab < 1 || n_uniforms < 0)
     return SDB_E_INVALID;
@@ -1165,9 +1269,15 @@ extern "C" int sdb_accept_stochastic(const float *target_logits, const float *dr
   sdb::RowStats *stats = reinterpret_cast<sdb::RowStats *>(workspace);
   cudaStream_t s = sdb::as_stream(stream);
   const size_t smem = sizeof(sdb::StSmem);
-  cudaFuncSetAttribute(sdb::row_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  sdb::row_stats_kernel<<<dim3(r_max, batch, 2), sdb::kStThreads, smem, s>>>(
-      target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err);
+  if (allowed) {
+    cudaFuncSetAttribute(sdb::row_stats_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sdb::row_stats_kernel<true><<<dim3(r_max, batch, 2), sdb::kStThreads, smem, s>>>(
+        target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err, allowed, allowed_words);
+  } else {
+    cudaFuncSetAttribute(sdb::row_stats_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sdb::row_stats_kernel<false><<<dim3(r_max, batch, 2), sdb::kStThreads, smem, s>>>(
+        target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err, nullptr, 0);
+  }
   SDB_CHECK_LAUNCH();
   // cluster size: enough CTAs to cover the SMs (8 = portable maximum)
   const int ncl = batch * 8 <= 4 * sdb::num_sms() ? 8 : 4;
@@ -1183,14 +1293,15 @@ extern "C" int sdb_accept_stochastic(const float *target_logits, const float *dr
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   cudaError_t le;
+#define SDB_WALK(CL, M)                                                                                           \
+  cudaLaunchKernelEx(&cfg, sdb::stochastic_walk_kernel<CL, M>, target_logits, draft_logits, r_max, vocab, a, parent, \
+                     n_rows, tokens, uniforms, n_uniforms, (const sdb::RowStats *)stats, path, path_len, next_token, \
+                     uniforms_used, residual, err, allowed, allowed_words)
   if (ncl == 4)
-    le = cudaLaunchKernelEx(&cfg, sdb::stochastic_walk_kernel<4>, target_logits, draft_logits, r_max, vocab, a,
-                            parent, n_rows, tokens, uniforms, n_uniforms, (const sdb::RowStats *)stats, path,
-                            path_len, next_token, uniforms_used, residual, err);
+    le = allowed ? SDB_WALK(4, true) : SDB_WALK(4, false);
   else
-    le = cudaLaunchKernelEx(&cfg, sdb::stochastic_walk_kernel<8>, target_logits, draft_logits, r_max, vocab, a,
-                            parent, n_rows, tokens, uniforms, n_uniforms, (const sdb::RowStats *)stats, path,
-                            path_len, next_token, uniforms_used, residual, err);
+    le = allowed ? SDB_WALK(8, true) : SDB_WALK(8, false);
+#undef SDB_WALK
   if (le != cudaSuccess) return sdb::record_cuda_error(le);
   SDB_CHECK_LAUNCH();
   return SDB_OK;

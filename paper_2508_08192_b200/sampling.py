@@ -225,10 +225,12 @@ class GreedyAcceptor:
                 err=torch.zeros((1,), dtype=torch.int32, device=dev)))
         return self._bufs[1]
 
-    def __call__(self, logits, parent, n_rows, tokens, stream=None):
+    def __call__(self, logits, parent, n_rows, tokens, stream=None, allowed=None):
         import torch
 
         b, r, v = logits.shape
+        if allowed is not None:
+            return self._masked(logits, parent, n_rows, tokens, allowed, stream)
         if logits.dtype == torch.float32:
             dt = _lib.DTYPE_F32
         elif logits.dtype == torch.bfloat16:
@@ -251,6 +253,22 @@ class GreedyAcceptor:
         return AcceptResult(o["path"], o["path_len"], o["next_token"], o["used"], o["err"])
 
 
+    def _masked(self, logits, parent, n_rows, tokens, allowed, stream):
+        import torch
+
+        b, r, v = logits.shape
+        if logits.dtype != torch.float32 or logits.stride(2) != 1 or allowed.dtype != torch.int32:
+            raise SamplingError("masked greedy acceptance takes fp32 logits and int32 allowed words")
+        o = self._alloc(b, r, logits.device)
+        o["err"].zero_()
+        rc = _lib.lib().sdb_accept_greedy_ex(_lib.ptr(logits), b, r, v, logits.stride(1), _lib.ptr(parent),
+                                             _lib.ptr(n_rows), _lib.ptr(tokens), _lib.ptr(allowed), allowed.shape[-1],
+                                             _lib.ptr(o["keys"]), _lib.ptr(o["path"]), _lib.ptr(o["path_len"]),
+                                             _lib.ptr(o["next_token"]), _lib.ptr(o["used"]), _lib.ptr(o["err"]),
+                                             _lib.stream_ptr(stream))
+        _lib.check(rc, "accept_greedy_ex")
+        return AcceptResult(o["path"], o["path_len"], o["next_token"], o["used"], o["err"])
+
     def fused_keys(self, b, r, dev):
         """Key buffer + error word for the attention-fused argmax scan."""
         o = self._alloc(b, r, dev)
@@ -268,14 +286,29 @@ class GreedyAcceptor:
         return AcceptResult(o["path"], o["path_len"], o["next_token"], o["used"], o["err"])
 
 
-def accept_greedy(logits, parent, n_rows, tokens, stream=None):
+def pack_allowed(mask):
+    """bool [..., V] allowed-token mask -> int32 words [..., ceil(V / 32)]
+    (bit j of word w = token 32 w + j), the layout of the masked acceptance."""
+    import torch
+
+    v = mask.shape[-1]
+    w = -(-v // 32)
+    pad = torch.zeros(mask.shape[:-1] + (w * 32,), dtype=torch.int64, device=mask.device)
+    pad[..., :v] = mask.to(torch.int64)
+    bits = pad.reshape(mask.shape[:-1] + (w, 32)) << torch.arange(32, device=mask.device, dtype=torch.int64)
+    words = bits.sum(-1)
+    return torch.where(words >= 2**31, words - 2**32, words).to(torch.int32)
+
+
+def accept_greedy(logits, parent, n_rows, tokens, stream=None, allowed=None):
     """Batched temperature-0 acceptance.
 
     logits [B, R, V] fp32/bf16 (row r = augmented tree row r); parent int32
     [B, R] augmented (row 0 = root, parent -1); tokens int32 [B, R] (token of
     row r, row 0 ignored); n_rows int32 [B].  Returns device tensors; no host
-    synchronisation."""
-    return GreedyAcceptor()(logits, parent, n_rows, tokens, stream)
+    synchronisation.  ``allowed``: int32 words from ``pack_allowed`` (FSM
+    masks per row, guided decoding) or None."""
+    return GreedyAcceptor()(logits, parent, n_rows, tokens, stream, allowed)
 
 
 def argmax_keys(logits2d, vocab_offset=0, stream=None):
@@ -340,7 +373,7 @@ class StochasticAcceptor:
         self._bufs = None
 
     def __call__(self, target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms=None,
-                 want_residual=False, stream=None, seeds=None, steps=None):
+                 want_residual=False, stream=None, seeds=None, steps=None, allowed=None):
         import torch
 
         b, r, v = target_logits.shape
@@ -372,22 +405,23 @@ class StochasticAcceptor:
             if "uni" not in o or o["uni"].shape != (b, r):
                 o["uni"] = torch.empty((b, r), dtype=torch.float64, device=dev)
             uniforms = device_uniforms(seeds, steps, r, out=o["uni"], stream=stream)
-        rc = lib.sdb_accept_stochastic(_lib.ptr(target_logits), _lib.ptr(draft_logits), b, r, v, float(temperature),
-                                       float(top_p), _lib.ptr(parent), _lib.ptr(n_rows), _lib.ptr(tokens),
-                                       _lib.ptr(uniforms), uniforms.shape[1], _lib.ptr(self._ws), self._ws.numel(),
-                                       _lib.ptr(o["path"]), _lib.ptr(o["path_len"]), _lib.ptr(o["next_token"]),
-                                       _lib.ptr(o["used"]), _lib.ptr(o["residual"]), _lib.ptr(o["err"]),
-                                       _lib.stream_ptr(stream))
+        rc = lib.sdb_accept_stochastic_ex(_lib.ptr(target_logits), _lib.ptr(draft_logits), b, r, v,
+                                          float(temperature), float(top_p), _lib.ptr(parent), _lib.ptr(n_rows),
+                                          _lib.ptr(tokens), _lib.ptr(uniforms), uniforms.shape[1], _lib.ptr(self._ws),
+                                          self._ws.numel(), _lib.ptr(o["path"]), _lib.ptr(o["path_len"]),
+                                          _lib.ptr(o["next_token"]), _lib.ptr(o["used"]), _lib.ptr(o["residual"]),
+                                          _lib.ptr(o["err"]), _lib.ptr(allowed),
+                                          allowed.shape[-1] if allowed is not None else 0, _lib.stream_ptr(stream))
         _lib.check(rc, "accept_stochastic")
         return AcceptResult(o["path"], o["path_len"], o["next_token"], o["used"], o["err"], o["residual"])
 
 
 def accept_stochastic(target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms=None,
-                      want_residual=False, stream=None, seeds=None, steps=None):
+                      want_residual=False, stream=None, seeds=None, steps=None, allowed=None):
     """Batched T > 0 acceptance (target_dist for every row, draft q per parent
     row, MSS walk).  uniforms float64 [B, n_uniforms] (the reference's
     rank_sliced_uniforms row per sequence), or ``uniforms=None`` with int64
     ``seeds``/``steps`` [B] to draw row 0 of the reference's Philox matrix on
     the device (engine.py:251-254)."""
     return StochasticAcceptor()(target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms,
-                                want_residual, stream, seeds, steps)
+                                want_residual, stream, seeds, steps, allowed)

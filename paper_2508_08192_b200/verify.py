@@ -40,6 +40,7 @@ class StepInputs:
     uniforms: "object" = None      # float64 [B, n_uniforms]
     seeds: "object" = None         # int64 [B] Philox keys (uniforms=None: drawn on the device)
     steps: "object" = None         # int64 [B]
+    allowed: "object" = None       # int32 [B, R, ceil(V/32)] FSM allowed-token words (sampling.pack_allowed)
 
 
 _SMS = {}
@@ -111,6 +112,7 @@ class TreeVerifier:
         can_overlap = overlap and self.attn.sms(*attn_args, **attn_kw) + 16 <= _num_sms(main.device)
         fused = None
         if (not can_overlap and self.fuse_greedy and self.temperature == 0 and isinstance(self.greedy, GreedyAcceptor)
+                and x.allowed is None
                 and x.logits.dtype == torch.float32 and x.logits.stride(2) == 1
                 and (self.fuse_greedy == "always" or self._scan_hides(x, b, r, main.device))):
             keys, err = self.greedy.fused_keys(b, r, x.logits.device)
@@ -143,10 +145,12 @@ class TreeVerifier:
             side.wait_event(fork)
         with torch.cuda.stream(side):
             if self.temperature == 0:
-                acc = self.greedy(x.logits, x.parent, x.n_rows, x.tokens, stream=side)
+                acc = (self.greedy(x.logits, x.parent, x.n_rows, x.tokens, stream=side) if x.allowed is None else
+                       self.greedy(x.logits, x.parent, x.n_rows, x.tokens, stream=side, allowed=x.allowed))
             else:
                 acc = self.stochastic(x.logits, x.draft_logits, self.temperature, self.top_p, x.parent, x.n_rows,
-                                      x.tokens, x.uniforms, stream=side, seeds=x.seeds, steps=x.steps)
+                                      x.tokens, x.uniforms, stream=side, seeds=x.seeds, steps=x.steps,
+                                      **({} if x.allowed is None else {"allowed": x.allowed}))
             if compact:
                 # writes cache rows >= ctx_len only: disjoint from what the
                 # attention reads (prefix keys < ctx_len are the only unmasked ones)

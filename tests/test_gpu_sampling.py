@@ -289,3 +289,98 @@ def test_accept_greedy_small_batch_split_rows_vs_oracle(B):
         plen = int(res.path_len[b])
         assert res.path[b, :plen].cpu().tolist() == list(path)
         assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used
+
+
+# ---------------------------------------------------------------------------
+# FSM-masked rows (guided decoding, target_dist(allowed=...), sampling.py:94-99)
+# ---------------------------------------------------------------------------
+
+def _fsm_masks(rng, B, R, V, density):
+    m = rng.random((B, R, V)) < density
+    m[:, :, 0] = True  # every row keeps at least one token
+    return m
+
+
+def test_accept_greedy_fsm_masked_vs_oracle():
+    from paper_2508_08192_b200.sampling import accept_greedy, pack_allowed
+
+    B, V = 3, 5003
+    rng = np.random.default_rng(8)
+    aug = O.augment(tuple(TREE64))
+    R = len(aug)
+    lg = (2.0 * rng.normal(size=(B, R, V))).astype(np.float32)
+    allowed = _fsm_masks(rng, B, R, V, 0.3)
+    masked = np.where(allowed, lg, -np.inf)
+    am = masked.argmax(-1)
+    tokens = np.zeros((B, R), dtype=np.int32)
+    for b in range(B):
+        for i in range(1, R):
+            tokens[b, i] = am[b, aug[i]] if rng.random() < 0.7 else rng.integers(V)
+    res = accept_greedy(torch.tensor(lg, device="cuda"), torch.tensor([aug] * B, dtype=torch.int32, device="cuda"),
+                        torch.full((B,), R, dtype=torch.int32, device="cuda"), torch.tensor(tokens, device="cuda"),
+                        allowed=pack_allowed(torch.tensor(allowed, device="cuda")))
+    torch.cuda.synchronize()
+    assert int(res.err[0]) == 0
+    for b in range(B):
+        # the reference: target_dist(row, 0, 1, allowed) = one-hot at the allowed argmax
+        dists = [O.target_dist(lg[b, r].astype(np.float64), 0.0, 1.0, allowed[b, r]) for r in range(R)]
+        path, nxt, used = O.greedy_walk(tuple(p - 1 if p > 0 else -1 for p in aug[1:]), tokens[b, 1:],
+                                        [int(np.argmax(d)) for d in dists])
+        plen = int(res.path_len[b])
+        assert res.path[b, :plen].cpu().tolist() == list(path)
+        assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used
+
+
+@pytest.mark.parametrize("top_p", [0.9, 1.0])
+def test_accept_stochastic_fsm_masked_vs_oracle(top_p):
+    from paper_2508_08192_b200.sampling import accept_stochastic, pack_allowed
+
+    B, V, T = 3, 8192, 1.0
+    rng = np.random.default_rng(9)
+    aug = O.augment(tuple(TREE64))
+    R = len(aug)
+    tl = (2.0 * rng.normal(size=(B, R, V))).astype(np.float32)
+    dl = (tl + 0.5 * rng.normal(size=(B, R, V))).astype(np.float32)
+    allowed = _fsm_masks(rng, B, R, V, 0.4)
+    tokens = np.zeros((B, R), dtype=np.int32)
+    for b in range(B):
+        for i in range(1, R):
+            q = O.target_dist(dl[b, aug[i]].astype(np.float64), T, 1.0, allowed[b, aug[i]])
+            tokens[b, i] = int(O.sample_from(q, rng.random()))
+    seeds, steps = [77 + b for b in range(B)], [6 for _ in range(B)]
+    res = accept_stochastic(torch.tensor(tl, device="cuda"), torch.tensor(dl, device="cuda"), T, top_p,
+                            torch.tensor([aug] * B, dtype=torch.int32, device="cuda"),
+                            torch.full((B,), R, dtype=torch.int32, device="cuda"), torch.tensor(tokens, device="cuda"),
+                            seeds=_i64(seeds), steps=_i64(steps),
+                            allowed=pack_allowed(torch.tensor(allowed, device="cuda")))
+    torch.cuda.synchronize()
+    assert int(res.err[0]) == 0
+    for b in range(B):
+        uni = O.rank_sliced_uniforms(seeds[b], steps[b], 1, R)[0]
+        tdists = [O.target_dist(tl[b, r].astype(np.float64), T, top_p, allowed[b, r]) for r in range(R)]
+        nd = [O.target_dist(dl[b, aug[i]].astype(np.float64), T, 1.0, allowed[b, aug[i]]) for i in range(1, R)]
+        path, nxt, _res, used = O.mss_verify(tuple(p - 1 if p > 0 else -1 for p in aug[1:]), tokens[b, 1:], nd,
+                                             tdists, uni)
+        plen = int(res.path_len[b])
+        assert res.path[b, :plen].cpu().tolist() == list(path), b
+        assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used, b
+
+
+def test_fsm_dead_row_raises_flag():
+    from paper_2508_08192_b200.sampling import accept_greedy, accept_stochastic, pack_allowed
+
+    aug = O.augment((-1, -1, 0))
+    R, V = len(aug), 300
+    rng = np.random.default_rng(3)
+    lg = torch.tensor(rng.normal(size=(1, R, V)).astype(np.float32), device="cuda")
+    allowed = np.ones((1, R, V), dtype=bool)
+    allowed[0, 1] = False  # dead FSM state on row 1
+    words = pack_allowed(torch.tensor(allowed, device="cuda"))
+    par = torch.tensor([aug], dtype=torch.int32, device="cuda")
+    nr = torch.tensor([R], dtype=torch.int32, device="cuda")
+    tok = torch.zeros((1, R), dtype=torch.int32, device="cuda")
+    g = accept_greedy(lg, par, nr, tok, allowed=words)
+    s = accept_stochastic(lg, lg, 1.0, 0.9, par, nr, tok, torch.tensor(rng.random((1, R)), device="cuda"),
+                          allowed=words)
+    torch.cuda.synchronize()
+    assert int(g.err[0]) & 32 and int(s.err[0]) & 32

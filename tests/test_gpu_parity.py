@@ -799,3 +799,80 @@ def test_tree_verify_attention_irope_local_chunk(chunk, kernel):
     err = np.abs(out.float().cpu().numpy() - want_o)
     assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
     assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
+
+
+@pytest.mark.parametrize("mode", ["greedy", "stochastic"])
+def test_verifier_step_mixed_batch_edge_cases(mode):
+    """One TreeVerifier step over a batch mixing the live edge cases of
+    SURVEY 8(a) a2: a root-only tree (R = 1, the non-speculative / truncated
+    round), an empty prefix (C = 0), the 8-node tree, the 64-row EAGLE tree
+    and a chain; 70B head shapes through the tcgen05 path.  Attention vs the
+    float64 oracle, acceptance and compaction exact."""
+    from paper_2508_08192_b200.sampling import device_uniforms
+    from paper_2508_08192_b200.verify import StepInputs, TreeVerifier
+
+    trees = [O.augment(()), O.augment((-1, -1, 0, 0, 1, 2, 2, 5)), O.augment(tuple(TREE64)), O.augment((-1, 0, 1)),
+             O.augment((-1, -1, 0))]
+    ctx = np.array([300, 0, 1029, 77, 4096], dtype=np.int32)
+    B, Hq, Hkv, d, bs, V, T, top_p = len(trees), 64, 8, 128, 64, 1000, 1.0, 0.9
+    R = max(len(t) for t in trees)
+    rng = np.random.default_rng(17)
+    nbl = [-(-(int(c) + R) // bs) for c in ctx]
+    nb = sum(nbl) + 2
+    perm = rng.permutation(nb).astype(np.int32)
+    table = np.zeros((B, max(nbl)), dtype=np.int32)
+    o = 0
+    for b in range(B):
+        table[b, :nbl[b]] = perm[o:o + nbl[b]]
+        o += nbl[b]
+    gen = torch.Generator(device="cuda").manual_seed(17)
+    rb = lambda *s: torch.randn(*s, generator=gen, device="cuda").to(torch.bfloat16)
+    k_pool, v_pool = rb(nb, Hkv, bs, d), rb(nb, Hkv, bs, d)
+    q, tk, tv = rb(B, R, Hq, d), rb(B, R, Hkv, d), rb(B, R, Hkv, d)
+    par = np.full((B, R), -1, dtype=np.int32)
+    nr = np.array([len(t) for t in trees], dtype=np.int32)
+    for b, t in enumerate(trees):
+        par[b, :len(t)] = t
+    tl = (2.0 * rng.normal(size=(B, R, V))).astype(np.float32)
+    dl = (tl + 0.5 * rng.normal(size=(B, R, V))).astype(np.float32)
+    tokens = np.zeros((B, R), dtype=np.int32)
+    for b, t in enumerate(trees):
+        for i in range(1, len(t)):
+            if mode == "greedy":
+                tokens[b, i] = int(np.argmax(tl[b, t[i]])) if rng.random() < 0.6 else int(rng.integers(V))
+            else:
+                tokens[b, i] = int(O.sample_from(O.target_dist(dl[b, t[i]].astype(np.float64), T, 1.0), rng.random()))
+    seeds = torch.arange(B, dtype=torch.int64, device="cuda") + 5
+    steps = torch.full((B,), 8, dtype=torch.int64, device="cuda")
+    kp0 = k_pool.float().cpu().numpy().astype(np.float64)
+    x = StepInputs(parent=torch.tensor(par, device="cuda"), n_rows=torch.tensor(nr, device="cuda"),
+                   ctx_len=torch.tensor(ctx, device="cuda"), tokens=torch.tensor(tokens, device="cuda"), q=q,
+                   tree_k=tk, tree_v=tv, logits=torch.tensor(tl, device="cuda"), k_pool=k_pool.contiguous(),
+                   v_pool=v_pool.contiguous(), block_table=torch.tensor(table, device="cuda"),
+                   draft_logits=torch.tensor(dl, device="cuda"), seeds=seeds, steps=steps)
+    ver = TreeVerifier(scale=d ** -0.5, temperature=0.0 if mode == "greedy" else T,
+                       top_p=1.0 if mode == "greedy" else top_p)
+    out, lse, acc, terr = ver.step(x)
+    uni = device_uniforms(seeds, steps, R).cpu().numpy()
+    torch.cuda.synchronize()
+    assert int(terr.abs().sum()) == 0 and int(acc.err[0]) == 0
+    f64 = lambda t_: t_.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(q), kp0, f64(v_pool), table, ctx, f64(tk), f64(tv),
+                                                   [tuple(t) for t in trees], d ** -0.5)
+    got_o, got_l = out.float().cpu().numpy(), lse.cpu().numpy()
+    for b in range(B):
+        n = nr[b]
+        assert np.abs(got_o[b, :n] - want_o[b, :n]).max() < 2e-2, b
+        assert np.abs(got_l[b, :, :n] - want_l[b, :, :n]).max() < 2e-3, b
+        raw = tuple(p - 1 if p > 0 else -1 for p in trees[b][1:])
+        if mode == "greedy":
+            path, nxt, used = O.greedy_walk(raw, tokens[b, 1:], np.argmax(tl[b].astype(np.float64), axis=1))
+        else:
+            tdists = [O.target_dist(tl[b, r].astype(np.float64), T, top_p) for r in range(n)]
+            nd = [O.target_dist(dl[b, trees[b][i]].astype(np.float64), T, 1.0) for i in range(1, n)]
+            path, nxt, _res, used = O.mss_verify(raw, tokens[b, 1:], nd, tdists, uni[b])
+        plen = int(acc.path_len[b])
+        assert acc.path[b, :plen].cpu().tolist() == list(path), (b, mode)
+        assert int(acc.next_token[b]) == nxt and int(acc.uniforms_used[b]) == used, (b, mode)
+        O.compact_kv(kp0, kp0.copy(), table[b], int(ctx[b]), f64(tk)[b], f64(tv)[b], list(path), plen + 1)
+    np.testing.assert_array_equal(x.k_pool.float().cpu().numpy(), kp0.astype(np.float32))

@@ -373,7 +373,8 @@ def main():
     n_parent_rows = len(set(p for p in aug[1:]))
     temperature = 0.0 if mode == "greedy" else TEMPERATURE
     ver = TreeVerifier(scale=cfg["d"] ** -0.5, temperature=temperature, top_p=TOP_P if mode != "greedy" else 1.0,
-                       max_ctx=max(cfg["ctx"], 1), num_splits=args.splits, kernel=args.kernel)
+                       max_ctx=max(cfg["ctx"], 1), num_splits=args.splits, kernel=args.kernel,
+                       reserve_sms=(int(os.environ["SDB_RESERVE_SMS"]) if "SDB_RESERVE_SMS" in os.environ else None))
     if world > 1:
         if mode == "greedy":
             sharded = ShardedGreedyAcceptor(shard)

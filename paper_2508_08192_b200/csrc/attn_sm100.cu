@@ -420,6 +420,10 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   // for the acceptance branch running concurrently (verify.TreeVerifier.step)
   // at no cost -- their time is set by the per-unit pipeline latency
   n = (int)std::max<int64_t>(1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : sp.total / 16));
+  // a multiple of the row blocks per KV head keeps those blocks in step on
+  // workers n / m_blocks apart (L2 serves the second read of each K/V tile);
+  // a misaligned count reads K/V twice (C3, 63 pairs: +7 %)
+  if (sp.m_blocks > 1 && n > sp.m_blocks) n -= n % sp.m_blocks;
   sp.n_workers = n;
   sp.part_out = nullptr;
   sp.part_lse = nullptr;

@@ -56,7 +56,7 @@ def _num_sms(device):
 
 class TreeVerifier:
     def __init__(self, scale, temperature=0.0, top_p=1.0, max_ctx=None, num_splits=0, kernel=0, fuse_greedy=True,
-                 chunk_len=None):
+                 chunk_len=None, reserve_sms=None):
         self.scale = scale
         self.temperature = temperature
         self.top_p = top_p
@@ -64,6 +64,7 @@ class TreeVerifier:
         self.num_splits = num_splits
         self.kernel = kernel
         self.chunk_len = chunk_len  # iRoPE local chunk (tree truncated at the boundary by the caller)
+        self.reserve_sms = reserve_sms  # SMs kept free of the attention for the concurrent acceptance (None: auto)
         self.fuse_greedy = fuse_greedy  # greedy scan inside the attention kernel: True (when it hides), "always", False
         self.attn = TreeVerifyAttention()
         self.greedy = GreedyAcceptor()
@@ -109,7 +110,23 @@ class TreeVerifier:
         # small batches: the attention's persistent grid leaves SMs free ->
         # run acceptance beside it; full occupancy -> fold the greedy scan
         # into the attention kernel (its otherwise idle warp + TMA ring)
-        can_overlap = overlap and self.attn.sms(*attn_args, **attn_kw) + 16 <= _num_sms(main.device)
+        n_sms = _num_sms(main.device)
+        attn_sms = self.attn.sms(*attn_args, **attn_kw)
+        reserve = self.reserve_sms
+        if reserve is None:
+            reserve = self._auto_reserve(x, b, r, n_sms)
+        if (overlap and reserve and attn_sms + 16 > n_sms and self.num_splits == 0
+                and not (self.fuse_greedy and self.temperature == 0 and x.allowed is None
+                         and self._scan_hides(x, b, r, main.device))):
+            # full occupancy: shrink the attention's persistent grid so the
+            # HBM-bound acceptance streams beside the tensor-bound attention
+            group = max(1, self.attn.sms(*attn_args, **dict(attn_kw, num_splits=1)))  # SMs per worker
+            # an even worker count keeps the two row blocks of a KV head in
+            # step (an odd count misaligns them: K/V read twice; C3 with 63
+            # pairs measured 693 us vs 646-657 with 62 / 64)
+            attn_kw["num_splits"] = max(2, ((n_sms - reserve) // group) & ~1)
+            attn_sms = self.attn.sms(*attn_args, **attn_kw)
+        can_overlap = overlap and attn_sms + 16 <= n_sms
         fused = None
         if (not can_overlap and self.fuse_greedy and self.temperature == 0 and isinstance(self.greedy, GreedyAcceptor)
                 and x.allowed is None
@@ -160,6 +177,25 @@ class TreeVerifier:
         if side is not main:
             main.wait_stream(side)
         return o["out"], o["lse"], acc, o["tree_err"]
+
+    def _auto_reserve(self, x, b, r, n_sms):
+        """SMs to leave to a greedy acceptance running beside a full-occupancy
+        attention: k such that the scan on k SMs (~80 GB/s each, measured)
+        takes as long as the attention on n_sms - k (~1.1 PFLOP/s on all
+        SMs, measured).  C3: k ~= 22 (step 690 -> 635 us).  Stochastic
+        acceptance is instruction-bound on every SM: no reserve."""
+        import torch
+
+        if self.temperature != 0 or x.logits.dtype != torch.float32:
+            return 0
+        hq, d = x.q.shape[2], x.q.shape[3]
+        ctx = self.max_ctx if self.max_ctx else x.block_table.shape[1] * x.k_pool.shape[2]
+        t_att = 4.0 * d * hq * b * r * ctx / 1.1e15
+        acc_sm_s = b * r * x.logits.shape[2] * 4 / 80.0e9  # scan time on one SM
+        # acc_sm_s / k = t_att * n / (n - k)  ->  k = acc_sm_s * n / (t_att * n + acc_sm_s)
+        k = acc_sm_s * n_sms / (t_att * n_sms + acc_sm_s)
+        k = int(round(k))
+        return k if 8 <= k <= n_sms // 2 else 0
 
     def _scan_hides(self, x, b, r, device):
         """Fold the greedy scan into the attention kernel only when one warp

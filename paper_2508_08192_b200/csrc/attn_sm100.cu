@@ -419,7 +419,11 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   // at least ~16 tiles per worker: small batches (bs 1) then leave SMs free
   // for the acceptance branch running concurrently (verify.TreeVerifier.step)
   // at no cost -- their time is set by the per-unit pipeline latency
-  n = (int)std::max<int64_t>(1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : sp.total / 16));
+  // >= ~16 tiles per worker (small batches then leave SMs to the acceptance
+  // branch) but never fewer workers than units: a unit costs ~6 us of
+  // prologue / pipeline fill / epilogue, so units must not serialise
+  n = (int)std::max<int64_t>(
+      1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : std::max<int64_t>(sp.units, sp.total / 16)));
   // a multiple of the row blocks per KV head keeps those blocks in step on
   // workers n / m_blocks apart (L2 serves the second read of each K/V tile);
   // a misaligned count reads K/V twice (C3, 63 pairs: +7 %)

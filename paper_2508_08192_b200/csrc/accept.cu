@@ -389,24 +389,39 @@ __device__ __forceinline__ void row_max_nan(const float *row, int vocab, bool ve
 // cumulative mass reaches tau.  Returns the kept mass; sets cut key / index.
 __device__ double exact_cut(StSmem &sm, int count, double mass_above, double tau, float a, float m2,
                             uint32_t &cut_key, int &cut_idx) {
-  int np2 = 1;
-  while (np2 < count) np2 <<= 1;
-  for (int i = count + threadIdx.x; i < np2; i += kStThreads) sm.cand[i] = 0ull;
-  __syncthreads();
-  for (int size = 2; size <= np2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < np2; i += kStThreads) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool desc = (i & size) == 0;
-          const unsigned long long x = sm.cand[i], y = sm.cand[j];
-          if (desc ? (x < y) : (x > y)) {
-            sm.cand[i] = y;
-            sm.cand[j] = x;
+  const unsigned long long *buf = sm.cand;
+  if (count <= kStThreads) {
+    // rank sort (keys are unique: the low word is ~index): one pass over the
+    // candidates per thread and a scatter, instead of log^2 barrier stages
+    unsigned long long *sorted = reinterpret_cast<unsigned long long *>(&sm.hist[0][0]);  // histogram is done
+    if ((int)threadIdx.x < count) {
+      const unsigned long long me = sm.cand[threadIdx.x];
+      int rank = 0;
+      for (int j = 0; j < count; ++j) rank += sm.cand[j] > me;
+      sorted[rank] = me;
+    }
+    __syncthreads();
+    buf = sorted;
+  } else {
+    int np2 = 1;
+    while (np2 < count) np2 <<= 1;
+    for (int i = count + threadIdx.x; i < np2; i += kStThreads) sm.cand[i] = 0ull;
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < np2; i += kStThreads) {
+          const int j = i ^ stride;
+          if (j > i) {
+            const bool desc = (i & size) == 0;
+            const unsigned long long x = sm.cand[i], y = sm.cand[j];
+            if (desc ? (x < y) : (x > y)) {
+              sm.cand[i] = y;
+              sm.cand[j] = x;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
   // per-thread chunk of 4 consecutive sorted candidates
@@ -416,7 +431,7 @@ __device__ double exact_cut(StSmem &sm, int count, double mass_above, double tau
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
     const int i = threadIdx.x * kPer + u;
-    wv[u] = i < count ? (double)key_weight((uint32_t)(sm.cand[i] >> 32), a, m2) : 0.0;
+    wv[u] = i < count ? (double)key_weight((uint32_t)(buf[i] >> 32), a, m2) : 0.0;
     tot += wv[u];
     loc[u] = tot;
   }
@@ -436,8 +451,8 @@ __device__ double exact_cut(StSmem &sm, int count, double mass_above, double tau
   for (int u = 0; u < kPer; ++u)
     if (threadIdx.x * kPer + u <= cpos) zz += wv[u];
   const double z = mass_above + block_sum<kStThreads>(zz, sm.red);
-  cut_key = (uint32_t)(sm.cand[cpos] >> 32);
-  cut_idx = (int)(0xffffffffu - (uint32_t)(sm.cand[cpos] & 0xffffffffu));
+  cut_key = (uint32_t)(buf[cpos] >> 32);
+  cut_idx = (int)(0xffffffffu - (uint32_t)(buf[cpos] & 0xffffffffu));
   return z;
 }
 

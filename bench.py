@@ -54,6 +54,13 @@ def _augment(parent):
     return [-1] + [0 if p == -1 else p + 1 for p in parent]
 
 
+def _tree_levels(aug):
+    depth = []
+    for p in aug:
+        depth.append(0 if p < 0 else depth[p] + 1)
+    return max(depth) + 1
+
+
 def _measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -374,7 +381,10 @@ def main():
     temperature = 0.0 if mode == "greedy" else TEMPERATURE
     ver = TreeVerifier(scale=cfg["d"] ** -0.5, temperature=temperature, top_p=TOP_P if mode != "greedy" else 1.0,
                        max_ctx=max(cfg["ctx"], 1), num_splits=args.splits, kernel=args.kernel,
-                       reserve_sms=(int(os.environ["SDB_RESERVE_SMS"]) if "SDB_RESERVE_SMS" in os.environ else None))
+                       reserve_sms=(int(os.environ["SDB_RESERVE_SMS"]) if "SDB_RESERVE_SMS" in os.environ else None),
+                       tree_levels=_tree_levels(aug))
+    if os.environ.get("SDB_STOCH_EAGER"):  # A/B: reduce every row (no lazy walk)
+        ver.stochastic.lazy = False
     if world > 1:
         if mode == "greedy":
             sharded = ShardedGreedyAcceptor(shard)

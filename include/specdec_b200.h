@@ -287,6 +287,24 @@ int sdb_accept_stochastic_ex(const float *target_logits, const float *draft_logi
                              int32_t *path_len, int64_t *next_token, int32_t *uniforms_used, float *residual,
                              int32_t *err, const uint32_t *allowed, int allowed_words, void *stream);
 
+/* Lazy stochastic acceptance: the same results as sdb_accept_stochastic_ex,
+ * but only the rows the walk visits are reduced (mss_verify reads the target
+ * dist of the nodes on its path and the q of their children only,
+ * sampling.py:173-202): `levels` (>= the tree's max depth + 1) rounds of
+ * {row stats of each sequence's current node, one walk step}.  Pair it with
+ * sdb_stochastic_validate (may run concurrently on another stream) to keep
+ * the reference's error behaviour, which checks EVERY row (engine.py:474-475:
+ * NaN -> SDB_ERR_NAN, dead FSM row -> SDB_ERR_NO_ALLOWED). */
+int sdb_accept_stochastic_lazy(const float *target_logits, const float *draft_logits, int batch, int r_max,
+                               int vocab, float temperature, float top_p, const int32_t *parent,
+                               const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
+                               int n_uniforms, void *workspace, int64_t workspace_bytes, int32_t *path,
+                               int32_t *path_len, int64_t *next_token, int32_t *uniforms_used, float *residual,
+                               int32_t *err, const uint32_t *allowed, int allowed_words, int levels, void *stream);
+int sdb_stochastic_validate(const float *target_logits, const float *draft_logits, int batch, int r_max, int vocab,
+                            const int32_t *parent, const int32_t *n_rows, const uint32_t *allowed,
+                            int allowed_words, int32_t *err, void *stream);
+
 /* ---- uniforms: device Philox4x64-10 ----------------------------------------
  * Replaces rank_sliced_uniforms (sampling.py:112-124) as the engine consumes
  * it (engine.py:251-254): out[b][i] = element (row, i) of the (padded_batch,

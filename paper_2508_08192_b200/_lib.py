@@ -95,6 +95,9 @@ _SIGNATURES = {
     "sdb_accept_greedy_ex": (I32, [P, I32, I32, I32, I64, P, P, P, P, I32, P, P, P, P, P, P, P]),
     "sdb_accept_stochastic_ex": (I32, [P, P, I32, I32, I32, F32, F32, P, P, P, P, I32, P, I64, P, P, P, P, P,
                                        P, P, I32, P]),
+    "sdb_accept_stochastic_lazy": (I32, [P, P, I32, I32, I32, F32, F32, P, P, P, P, I32, P, I64, P, P, P, P, P,
+                                         P, P, I32, I32, P]),
+    "sdb_stochastic_validate": (I32, [P, P, I32, I32, I32, P, P, P, I32, P, P]),
     "sdb_accept_stochastic_workspace": (I64, [I32, I32, I32]),
     "sdb_accept_stochastic": (I32, [P, P, I32, I32, I32, F32, F32, P, P, P, P, I32, P, I64, P, P, P, P, P,
                                     P, P]),

@@ -466,10 +466,13 @@ template <bool kMasked>
 __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
     float top_p, const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows,
-    RowStats *__restrict__ stats, int32_t *__restrict__ err, const uint32_t *__restrict__ allowed, int n_mw) {
+    RowStats *__restrict__ stats, int32_t *__restrict__ err, const uint32_t *__restrict__ allowed, int n_mw,
+    const int32_t *__restrict__ cur_rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   StSmem &sm = *reinterpret_cast<StSmem *>(smem_raw);
-  const int r = blockIdx.x, b = blockIdx.y, is_draft = blockIdx.z;
+  // lazy mode (cur_rows): the one row per sequence the walk is at (-1: done)
+  const int r = cur_rows ? cur_rows[blockIdx.y] : (int)blockIdx.x, b = blockIdx.y, is_draft = blockIdx.z;
+  if (r < 0) return;
   const int n = min(n_rows[b], r_max);
   RowStats *out = stats + ((int64_t)b * r_max + r) * 2 + is_draft;
   if (r >= n) {
@@ -949,14 +952,23 @@ __device__ __forceinline__ void cluster_exchange(double v, double *slots, int &p
   ++phase;
 }
 
-template <int kCl, bool kMasked>
+// Lazy mode (kLazy): one tree level per launch.  The walk state lives in
+// `lw` and the current node in `cur_rows`; row_stats ran for exactly those
+// rows beforehand.  Only the rows the walk visits are ever reduced
+// (mss_verify reads no other target dist, sampling.py:173-202).
+struct LazyWalk {
+  double c, M;
+  int32_t cur, used, len, done;
+};
+
+template <int kCl, bool kMasked, bool kLazy>
 __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
     const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, const int32_t *__restrict__ tokens,
     const double *__restrict__ uniforms, int n_uniforms, const RowStats *__restrict__ stats,
     int32_t *__restrict__ path, int32_t *__restrict__ path_len, int64_t *__restrict__ next_token,
     int32_t *__restrict__ uniforms_used, float *__restrict__ residual, int32_t *__restrict__ err,
-    const uint32_t *__restrict__ allowed, int n_mw) {
+    const uint32_t *__restrict__ allowed, int n_mw, LazyWalk *__restrict__ lw, int32_t *__restrict__ cur_rows) {
   __shared__ double red[32];
   __shared__ double slots[2];
   __shared__ int s_flag;
@@ -974,22 +986,43 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
   const bool vec = (vocab & 3) == 0 && ((uintptr_t)target & 15) == 0 && ((uintptr_t)draft & 15) == 0;
   int phase = 0;
   double vals[kCl];
+  int cur = 0, used = 0, len = 0;
+  double c = 0.0, M = 1.0;
+  if (kLazy) {
+    const LazyWalk s0 = lw[b];
+    if (s0.done) return;  // uniform across the cluster: no exchange follows
+    cur = s0.cur;
+    used = s0.used;
+    len = s0.len;
+    c = s0.c;
+    M = s0.M;
+  }
   if (threadIdx.x == 0) s_flag = 0;
   __syncthreads();
-  // any invalid (NaN) row in this sequence aborts it
-  for (int r = threadIdx.x; r < n; r += kWThreads)
-    if (!st[2 * r].valid) atomicOr(&s_flag, 1);
+  if (kLazy) {
+    // the visited row (and the q of its children) must be valid
+    bool has = false;
+    for (int j = cur + 1 + threadIdx.x; j < n; j += kWThreads) has |= par[j] == cur;
+    has = __syncthreads_or(has);
+    if (threadIdx.x == 0 && (!st[2 * cur].valid || (has && !st[2 * cur + 1].valid))) s_flag = 1;
+  } else {
+    // any invalid (NaN) row in this sequence aborts it
+    for (int r = threadIdx.x; r < n; r += kWThreads)
+      if (!st[2 * r].valid) atomicOr(&s_flag, 1);
+  }
   __syncthreads();
   if (s_flag) {
     if (threadIdx.x == 0 && crank == 0) {
       path_len[b] = 0;
       next_token[b] = 0;
       uniforms_used[b] = 0;
+      if (kLazy) {
+        lw[b].done = 1;
+        cur_rows[b] = -1;
+      }
     }
     return;  // uniform across the cluster: no exchange follows
   }
-  int cur = 0, used = 0, len = 0;
-  double c = 0.0, M = 1.0;
   bool failed = false;
   auto make_row = [&](int r) {
     WalkRow w;
@@ -1031,6 +1064,21 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
         cur = j;
         c = 0.0;
         M = 1.0;
+        if (kLazy) {  // the next level reduces row j first
+          if (threadIdx.x == 0 && crank == 0) {
+            LazyWalk s1;
+            s1.c = 0.0;
+            s1.M = 1.0;
+            s1.cur = j;
+            s1.used = used;
+            s1.len = len;
+            s1.done = 0;
+            lw[b] = s1;
+            cur_rows[b] = j;
+          }
+          cl.sync();  // peers may still read this CTA's exchange slots
+          return;
+        }
         w = make_row(cur);
         descended = true;
         break;
@@ -1059,6 +1107,10 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
       path_len[b] = len;
       next_token[b] = -1;
       uniforms_used[b] = used;
+      if (kLazy) {
+        lw[b].done = 1;
+        cur_rows[b] = -1;
+      }
     }
     cl.sync();
     return;
@@ -1141,8 +1193,96 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
   if (threadIdx.x == 0 && crank == 0) {
     path_len[b] = len;
     uniforms_used[b] = used;
+    if (kLazy) {
+      lw[b].done = 1;
+      cur_rows[b] = -1;
+    }
   }
   cl.sync();  // peers may still read this CTA's exchange slots
+}
+
+// lazy walk start: every sequence at its root row
+__global__ void lazy_walk_init_kernel(const int32_t *__restrict__ n_rows, int batch, LazyWalk *__restrict__ lw,
+                                      int32_t *__restrict__ cur_rows) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  LazyWalk s;
+  s.c = 0.0;
+  s.M = 1.0;
+  s.cur = 0;
+  s.used = 0;
+  s.len = 0;
+  s.done = n_rows[b] < 1;
+  lw[b] = s;
+  cur_rows[b] = s.done ? -1 : 0;
+}
+
+// Validation scan for the lazy mode: the reference computes target_dist for
+// EVERY tree row and the q of every parent row (engine.py:474-475), raising
+// on NaN (numcore.py:47-48) or a dead FSM row (sampling.py:96-97) anywhere;
+// this streams every such row once (max.NaN) so the error semantics hold
+// while the walk only reduces the rows it visits.  HBM-bound, independent
+// of the walk: it runs beside it.
+template <bool kMasked>
+__global__ void __launch_bounds__(kArgmaxThreads) stochastic_validate_kernel(
+    const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab,
+    const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, const uint32_t *__restrict__ allowed,
+    int n_mw, int32_t *__restrict__ err, int batch) {
+  // persistent: gridDim.x CTAs (half the SMs) stride over the B * R * 2 rows,
+  // leaving the other SMs to the lazy walk running concurrently
+  for (int64_t job = blockIdx.x; job < (int64_t)batch * r_max * 2; job += gridDim.x) {
+  const int r = (int)(job % r_max), b = (int)((job / r_max) % batch), z = (int)(job / ((int64_t)r_max * batch));
+  const int n = min(n_rows[b], r_max);
+  if (r >= n) continue;
+  if (z) {
+    const int32_t *par = parent + (int64_t)b * r_max;
+    int has = 0;
+    for (int j = r + 1 + threadIdx.x; j < n; j += kArgmaxThreads) has |= par[j] == r;
+    if (!__syncthreads_or(has)) continue;
+  }
+  const float *row = (z ? draft : target) + ((int64_t)b * r_max + r) * vocab;
+  const uint32_t *mw = kMasked ? allowed + ((int64_t)b * r_max + r) * n_mw : nullptr;
+  float nacc = -INFINITY;
+  bool any = !kMasked;
+  if ((vocab & 3) == 0 && ((uintptr_t)row & 15) == 0) {
+    const float4 *r4 = reinterpret_cast<const float4 *>(row);
+    const int n4 = vocab >> 2;
+    for (int i0 = 0; i0 < n4; i0 += 4 * kArgmaxThreads) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kArgmaxThreads + threadIdx.x;
+        v[u] = i < n4 ? __ldcs(r4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kMasked && i < n4) {
+          const float4 m = mask4(v[u], mw, i);
+          any |= (m.x != -INFINITY) | (m.y != -INFINITY) | (m.z != -INFINITY) | (m.w != -INFINITY) |
+                 (((__ldg(mw + (i >> 3)) >> ((i & 7) * 4)) & 0xFu) != 0);
+          v[u] = make_float4(m.x == -INFINITY ? 0.f : m.x, m.y == -INFINITY ? 0.f : m.y,
+                             m.z == -INFINITY ? 0.f : m.z, m.w == -INFINITY ? 0.f : m.w);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) nacc = max_nan(nacc, max_nan(max_nan3(v[u].x, v[u].y, v[u].z), v[u].w));
+    }
+    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kArgmaxThreads) {
+      const float x = kMasked ? mask1(row[j], mw, j) : row[j];
+      if (kMasked && ((__ldg(mw + (j >> 5)) >> (j & 31)) & 1u)) any = true;
+      nacc = max_nan(nacc, x == -INFINITY ? 0.f : x);
+    }
+  } else {
+    for (int j = threadIdx.x; j < vocab; j += kArgmaxThreads) {
+      const float x = kMasked ? mask1(row[j], mw, j) : row[j];
+      if (kMasked && ((__ldg(mw + (j >> 5)) >> (j & 31)) & 1u)) any = true;
+      nacc = max_nan(nacc, x == -INFINITY ? 0.f : x);
+    }
+  }
+  const bool nan = __syncthreads_or(nacc != nacc);
+  const bool alive = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    if (nan) atomicOr(err, SDB_ERR_NAN);
+    if (!alive) atomicOr(err, SDB_ERR_NO_ALLOWED);
+  }
+  }
 }
 
 }  // namespace sdb
@@ -1252,9 +1392,10 @@ extern "C" int sdb_accept_greedy(const void *logits, int dtype, int batch, int r
 extern "C" int64_t sdb_accept_stochastic_workspace(int batch, int r_max, int vocab) {
   (void)vocab;
   if (batch < 0 || r_max < 1) return SDB_E_INVALID;
-  return (int64_t)batch * r_max * 2 * (int64_t)sizeof(sdb::RowStats) + 256;
+  // RowStats [B][R][2] | LazyWalk [B] | cur_rows [B]
+  return (int64_t)batch * r_max * 2 * (int64_t)sizeof(sdb::RowStats) + 256 +
+         (int64_t)batch * (int64_t)(sizeof(sdb::LazyWalk) + 4) + 256;
 }
-
 extern "C" int sdb_accept_stochastic(const float *target_logits, const float *draft_logits, int batch, int r_max,
                                      int vocab, float temperature, float top_p, const int32_t *parent,
                                      const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
@@ -1266,34 +1407,31 @@ extern "C" int sdb_accept_stochastic(const float *target_logits, const float *dr
                                   next_token, uniforms_used, residual, err, nullptr, 0, stream);
 }
 
-extern "C" int sdb_accept_stochastic_ex(const float *target_logits, const float *draft_logits, int batch, int r_max,
-                                        int vocab, float temperature, float top_p, const int32_t *parent,
-                                        const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
-                                        int n_uniforms, void *workspace, int64_t workspace_bytes, int32_t *path,
-                                        int32_t *path_len, int64_t *next_token, int32_t *uniforms_used,
-                                        float *residual, int32_t *err, const uint32_t *allowed, int allowed_words,
-                                        void *stream) {
+static int accept_stochastic_impl(const float *target_logits, const float *draft_logits, int batch, int r_max,
+                                  int vocab, float temperature, float top_p, const int32_t *parent,
+                                  const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
+                                  int n_uniforms, void *workspace, int64_t workspace_bytes, int32_t *path,
+                                  int32_t *path_len, int64_t *next_token, int32_t *uniforms_used, float *residual,
+                                  int32_t *err, const uint32_t *allowed, int allowed_words, int levels,
+                                  void *stream) {
   if (allowed && allowed_words < (vocab + 31) / 32) return SDB_E_INVALID;
   if (!target_logits || !draft_logits || !parent || !n_rows || !tokens || !uniforms || !path || !path_len ||
-      !next_token || !uniforms_used || !err || batch < 0 || r_max < 1 || vocab < 1 || n_uniforms < 0)
+      !next_token || !uniforms_used || !err || batch < 0 || r_max < 1 || vocab < 1 || n_uniforms < 0 ||
+      levels > r_max)
     return SDB_E_INVALID;
   if (!(temperature > 0.0f) || !(top_p > 0.0f) || top_p > 1.0f) return SDB_E_INVALID;
   if (batch == 0) return SDB_OK;
   if (!workspace || workspace_bytes < sdb_accept_stochastic_workspace(batch, r_max, vocab)) return SDB_E_WORKSPACE;
   const float a = 1.4426950408889634f / temperature;
   sdb::RowStats *stats = reinterpret_cast<sdb::RowStats *>(workspace);
+  char *tail = (char *)workspace + (((int64_t)batch * r_max * 2 * (int64_t)sizeof(sdb::RowStats) + 255) & ~255ll);
+  sdb::LazyWalk *lw = reinterpret_cast<sdb::LazyWalk *>(tail);
+  int32_t *cur_rows = reinterpret_cast<int32_t *>(tail + (((int64_t)batch * sizeof(sdb::LazyWalk) + 15) & ~15ll));
+  const bool lazy = levels > 0;
   cudaStream_t s = sdb::as_stream(stream);
   const size_t smem = sizeof(sdb::StSmem);
-  if (allowed) {
-    cudaFuncSetAttribute(sdb::row_stats_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sdb::row_stats_kernel<true><<<dim3(r_max, batch, 2), sdb::kStThreads, smem, s>>>(
-        target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err, allowed, allowed_words);
-  } else {
-    cudaFuncSetAttribute(sdb::row_stats_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sdb::row_stats_kernel<false><<<dim3(r_max, batch, 2), sdb::kStThreads, smem, s>>>(
-        target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err, nullptr, 0);
-  }
-  SDB_CHECK_LAUNCH();
+  cudaFuncSetAttribute(sdb::row_stats_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(sdb::row_stats_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // cluster size: enough CTAs to cover the SMs (8 = portable maximum)
   const int ncl = batch * 8 <= 4 * sdb::num_sms() ? 8 : 4;
   cudaLaunchConfig_t cfg = {};
@@ -1307,17 +1445,88 @@ extern "C" int sdb_accept_stochastic_ex(const float *target_logits, const float 
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  cudaError_t le;
-#define SDB_WALK(CL, M)                                                                                           \
-  cudaLaunchKernelEx(&cfg, sdb::stochastic_walk_kernel<CL, M>, target_logits, draft_logits, r_max, vocab, a, parent, \
-                     n_rows, tokens, uniforms, n_uniforms, (const sdb::RowStats *)stats, path, path_len, next_token, \
-                     uniforms_used, residual, err, allowed, allowed_words)
-  if (ncl == 4)
-    le = allowed ? SDB_WALK(4, true) : SDB_WALK(4, false);
-  else
-    le = allowed ? SDB_WALK(8, true) : SDB_WALK(8, false);
+  auto stats_launch = [&](dim3 grid, const int32_t *rows) {
+    if (allowed)
+      sdb::row_stats_kernel<true><<<grid, sdb::kStThreads, smem, s>>>(
+          target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err, allowed, allowed_words, rows);
+    else
+      sdb::row_stats_kernel<false><<<grid, sdb::kStThreads, smem, s>>>(
+          target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err, nullptr, 0, rows);
+  };
+#define SDB_WALK(CL, M, L)                                                                                        \
+  cudaLaunchKernelEx(&cfg, sdb::stochastic_walk_kernel<CL, M, L>, target_logits, draft_logits, r_max, vocab, a,    \
+                     parent, n_rows, tokens, uniforms, n_uniforms, (const sdb::RowStats *)stats, path, path_len,  \
+                     next_token, uniforms_used, residual, err, allowed, allowed_words, lw, cur_rows)
+  auto walk_launch = [&]() {
+    if (lazy) {
+      if (ncl == 4) return allowed ? SDB_WALK(4, true, true) : SDB_WALK(4, false, true);
+      return allowed ? SDB_WALK(8, true, true) : SDB_WALK(8, false, true);
+    }
+    if (ncl == 4) return allowed ? SDB_WALK(4, true, false) : SDB_WALK(4, false, false);
+    return allowed ? SDB_WALK(8, true, false) : SDB_WALK(8, false, false);
+  };
 #undef SDB_WALK
-  if (le != cudaSuccess) return sdb::record_cuda_error(le);
+  if (!lazy) {
+    stats_launch(dim3(r_max, batch, 2), nullptr);
+    SDB_CHECK_LAUNCH();
+    cudaError_t le = walk_launch();
+    if (le != cudaSuccess) return sdb::record_cuda_error(le);
+    SDB_CHECK_LAUNCH();
+    return SDB_OK;
+  }
+  // lazy: one level per (row stats of the current rows, walk step) pair
+  sdb::lazy_walk_init_kernel<<<(batch + 127) / 128, 128, 0, s>>>(n_rows, batch, lw, cur_rows);
+  SDB_CHECK_LAUNCH();
+  for (int lvl = 0; lvl < levels; ++lvl) {
+    stats_launch(dim3(1, batch, 2), cur_rows);
+    SDB_CHECK_LAUNCH();
+    cudaError_t le = walk_launch();
+    if (le != cudaSuccess) return sdb::record_cuda_error(le);
+    SDB_CHECK_LAUNCH();
+  }
+  return SDB_OK;
+}
+
+extern "C" int sdb_accept_stochastic_ex(const float *target_logits, const float *draft_logits, int batch, int r_max,
+                                        int vocab, float temperature, float top_p, const int32_t *parent,
+                                        const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
+                                        int n_uniforms, void *workspace, int64_t workspace_bytes, int32_t *path,
+                                        int32_t *path_len, int64_t *next_token, int32_t *uniforms_used,
+                                        float *residual, int32_t *err, const uint32_t *allowed, int allowed_words,
+                                        void *stream) {
+  return accept_stochastic_impl(target_logits, draft_logits, batch, r_max, vocab, temperature, top_p, parent, n_rows,
+                                tokens, uniforms, n_uniforms, workspace, workspace_bytes, path, path_len, next_token,
+                                uniforms_used, residual, err, allowed, allowed_words, 0, stream);
+}
+
+extern "C" int sdb_accept_stochastic_lazy(const float *target_logits, const float *draft_logits, int batch, int r_max,
+                                          int vocab, float temperature, float top_p, const int32_t *parent,
+                                          const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
+                                          int n_uniforms, void *workspace, int64_t workspace_bytes, int32_t *path,
+                                          int32_t *path_len, int64_t *next_token, int32_t *uniforms_used,
+                                          float *residual, int32_t *err, const uint32_t *allowed, int allowed_words,
+                                          int levels, void *stream) {
+  if (levels < 1) return SDB_E_INVALID;
+  return accept_stochastic_impl(target_logits, draft_logits, batch, r_max, vocab, temperature, top_p, parent, n_rows,
+                                tokens, uniforms, n_uniforms, workspace, workspace_bytes, path, path_len, next_token,
+                                uniforms_used, residual, err, allowed, allowed_words, levels, stream);
+}
+
+extern "C" int sdb_stochastic_validate(const float *target_logits, const float *draft_logits, int batch, int r_max,
+                                       int vocab, const int32_t *parent, const int32_t *n_rows,
+                                       const uint32_t *allowed, int allowed_words, int32_t *err, void *stream) {
+  if (!target_logits || !draft_logits || !parent || !n_rows || !err || batch < 0 || r_max < 1 || vocab < 1 ||
+      (allowed && allowed_words < (vocab + 31) / 32))
+    return SDB_E_INVALID;
+  if (batch == 0) return SDB_OK;
+  dim3 grid(std::max(1, sdb::num_sms() / 2));
+  cudaStream_t s = sdb::as_stream(stream);
+  if (allowed)
+    sdb::stochastic_validate_kernel<true><<<grid, sdb::kArgmaxThreads, 0, s>>>(
+        target_logits, draft_logits, r_max, vocab, parent, n_rows, allowed, allowed_words, err, batch);
+  else
+    sdb::stochastic_validate_kernel<false><<<grid, sdb::kArgmaxThreads, 0, s>>>(
+        target_logits, draft_logits, r_max, vocab, parent, n_rows, nullptr, 0, err, batch);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

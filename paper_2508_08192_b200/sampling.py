@@ -365,12 +365,32 @@ def device_uniforms(seeds, steps, width, row=0, out=None, stream=None):
     return out
 
 
-class StochasticAcceptor:
-    """T > 0 acceptance with a cached workspace (graph-capturable)."""
+def tree_levels(parent):
+    """Max depth + 1 of augmented parent rows [B, R] (host sync)."""
+    par = parent.cpu().numpy()
+    best = 1
+    for row in par:
+        depth = [0] * len(row)
+        for i, p in enumerate(row):
+            depth[i] = 0 if p < 0 else depth[p] + 1
+        best = max(best, max(depth) + 1)
+    return best
 
-    def __init__(self):
+
+class StochasticAcceptor:
+    """T > 0 acceptance with a cached workspace (graph-capturable).
+
+    ``lazy`` (default): only the rows the MSS walk visits are reduced, one
+    tree level per launch pair, while a validation scan of every row (the
+    reference's error behaviour) runs concurrently on a side stream.
+    ``levels`` (tree depth + 1) must be given when capturing a CUDA graph."""
+
+    def __init__(self, lazy=True, levels=None):
         self._ws = None
         self._bufs = None
+        self.lazy = lazy
+        self.levels = levels
+        self._side = None
 
     def __call__(self, target_logits, draft_logits, temperature, top_p, parent, n_rows, tokens, uniforms=None,
                  want_residual=False, stream=None, seeds=None, steps=None, allowed=None):
@@ -405,14 +425,31 @@ class StochasticAcceptor:
             if "uni" not in o or o["uni"].shape != (b, r):
                 o["uni"] = torch.empty((b, r), dtype=torch.float64, device=dev)
             uniforms = device_uniforms(seeds, steps, r, out=o["uni"], stream=stream)
-        rc = lib.sdb_accept_stochastic_ex(_lib.ptr(target_logits), _lib.ptr(draft_logits), b, r, v,
-                                          float(temperature), float(top_p), _lib.ptr(parent), _lib.ptr(n_rows),
-                                          _lib.ptr(tokens), _lib.ptr(uniforms), uniforms.shape[1], _lib.ptr(self._ws),
-                                          self._ws.numel(), _lib.ptr(o["path"]), _lib.ptr(o["path_len"]),
-                                          _lib.ptr(o["next_token"]), _lib.ptr(o["used"]), _lib.ptr(o["residual"]),
-                                          _lib.ptr(o["err"]), _lib.ptr(allowed),
-                                          allowed.shape[-1] if allowed is not None else 0, _lib.stream_ptr(stream))
-        _lib.check(rc, "accept_stochastic")
+        n_words = allowed.shape[-1] if allowed is not None else 0
+        levels = self.levels
+        if self.lazy and levels is None and not torch.cuda.is_current_stream_capturing():
+            levels = tree_levels(parent)
+        args = (_lib.ptr(target_logits), _lib.ptr(draft_logits), b, r, v, float(temperature), float(top_p),
+                _lib.ptr(parent), _lib.ptr(n_rows), _lib.ptr(tokens), _lib.ptr(uniforms), uniforms.shape[1],
+                _lib.ptr(self._ws), self._ws.numel(), _lib.ptr(o["path"]), _lib.ptr(o["path_len"]),
+                _lib.ptr(o["next_token"]), _lib.ptr(o["used"]), _lib.ptr(o["residual"]), _lib.ptr(o["err"]),
+                _lib.ptr(allowed), n_words)
+        if self.lazy and levels:
+            main = stream if stream is not None else torch.cuda.current_stream()
+            if self._side is None or self._side.device != main.device:
+                self._side = torch.cuda.Stream(device=main.device)
+            self._side.wait_stream(main)  # err zeroed, inputs ready
+            # every row checked beside the lazy walk (HBM-bound vs latency-bound)
+            rc = lib.sdb_stochastic_validate(_lib.ptr(target_logits), _lib.ptr(draft_logits), b, r, v,
+                                             _lib.ptr(parent), _lib.ptr(n_rows), _lib.ptr(allowed), n_words,
+                                             _lib.ptr(o["err"]), _lib.stream_ptr(self._side))
+            _lib.check(rc, "stochastic_validate")
+            rc = lib.sdb_accept_stochastic_lazy(*args, int(levels), _lib.stream_ptr(main))
+            _lib.check(rc, "accept_stochastic_lazy")
+            main.wait_stream(self._side)
+        else:
+            rc = lib.sdb_accept_stochastic_ex(*args, _lib.stream_ptr(stream))
+            _lib.check(rc, "accept_stochastic")
         return AcceptResult(o["path"], o["path_len"], o["next_token"], o["used"], o["err"], o["residual"])
 
 

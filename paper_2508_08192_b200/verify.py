@@ -56,7 +56,7 @@ def _num_sms(device):
 
 class TreeVerifier:
     def __init__(self, scale, temperature=0.0, top_p=1.0, max_ctx=None, num_splits=0, kernel=0, fuse_greedy=True,
-                 chunk_len=None, reserve_sms=None):
+                 chunk_len=None, reserve_sms=None, tree_levels=None):
         self.scale = scale
         self.temperature = temperature
         self.top_p = top_p
@@ -68,7 +68,8 @@ class TreeVerifier:
         self.fuse_greedy = fuse_greedy  # greedy scan inside the attention kernel: True (when it hides), "always", False
         self.attn = TreeVerifyAttention()
         self.greedy = GreedyAcceptor()
-        self.stochastic = StochasticAcceptor()
+        # lazy stochastic acceptance needs the tree depth + 1 to be capturable
+        self.stochastic = StochasticAcceptor(levels=tree_levels)
         self._out = None
         self._side = None
         self.graph = None

@@ -327,11 +327,15 @@ def _margin_ok(g, k, res_path, res_next, res_used):
             and res_used == int(g[f"s{k}_used"]))
 
 
-def test_accept_stochastic_golden(golden):
+@pytest.mark.parametrize("lazy", [True, False])
+def test_accept_stochastic_golden(golden, lazy):
     """Stochastic acceptance vs the reference (fp32 pipeline; decisions whose
     reference margin is < 1e-6 may differ and are counted -- none expected
-    on these fixtures)."""
-    from paper_2508_08192_b200.sampling import accept_stochastic
+    on these fixtures); lazy (visited rows only) and eager (every row)."""
+    from paper_2508_08192_b200.sampling import StochasticAcceptor
+
+    def accept_stochastic(*a, **k):
+        return StochasticAcceptor(lazy=lazy)(*a, **k)
 
     g = golden("accept_stochastic")
     mism = []

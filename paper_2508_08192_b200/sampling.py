@@ -377,6 +377,10 @@ def tree_levels(parent):
     return best
 
 
+# diagnostics only (timing the lazy walk alone): skips the every-row validation
+_DIAG_SKIP_VALIDATE = bool(__import__("os").environ.get("SDB_DIAG_SKIP_VALIDATE"))
+
+
 class StochasticAcceptor:
     """T > 0 acceptance with a cached workspace (graph-capturable).
 
@@ -440,10 +444,11 @@ class StochasticAcceptor:
                 self._side = torch.cuda.Stream(device=main.device)
             self._side.wait_stream(main)  # err zeroed, inputs ready
             # every row checked beside the lazy walk (HBM-bound vs latency-bound)
-            rc = lib.sdb_stochastic_validate(_lib.ptr(target_logits), _lib.ptr(draft_logits), b, r, v,
-                                             _lib.ptr(parent), _lib.ptr(n_rows), _lib.ptr(allowed), n_words,
-                                             _lib.ptr(o["err"]), _lib.stream_ptr(self._side))
-            _lib.check(rc, "stochastic_validate")
+            if not _DIAG_SKIP_VALIDATE:
+                rc = lib.sdb_stochastic_validate(_lib.ptr(target_logits), _lib.ptr(draft_logits), b, r, v,
+                                                 _lib.ptr(parent), _lib.ptr(n_rows), _lib.ptr(allowed), n_words,
+                                                 _lib.ptr(o["err"]), _lib.stream_ptr(self._side))
+                _lib.check(rc, "stochastic_validate")
             rc = lib.sdb_accept_stochastic_lazy(*args, int(levels), _lib.stream_ptr(main))
             _lib.check(rc, "accept_stochastic_lazy")
             main.wait_stream(self._side)

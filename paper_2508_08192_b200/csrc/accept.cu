@@ -1228,17 +1228,17 @@ __global__ void __launch_bounds__(kArgmaxThreads) stochastic_validate_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab,
     const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, const uint32_t *__restrict__ allowed,
     int n_mw, int32_t *__restrict__ err, int batch) {
-  // persistent: gridDim.x CTAs (half the SMs) stride over the B * R * 2 rows,
-  // leaving the other SMs to the lazy walk running concurrently
-  for (int64_t job = blockIdx.x; job < (int64_t)batch * r_max * 2; job += gridDim.x) {
-  const int r = (int)(job % r_max), b = (int)((job / r_max) % batch), z = (int)(job / ((int64_t)r_max * batch));
+  // one row per CTA, launched at the lowest priority: SMs freed by these
+  // short CTAs go to the latency-bound lazy walk's CTAs first
+  (void)batch;
+  const int r = blockIdx.x, b = blockIdx.y, z = blockIdx.z;
   const int n = min(n_rows[b], r_max);
-  if (r >= n) continue;
+  if (r >= n) return;
   if (z) {
     const int32_t *par = parent + (int64_t)b * r_max;
     int has = 0;
     for (int j = r + 1 + threadIdx.x; j < n; j += kArgmaxThreads) has |= par[j] == r;
-    if (!__syncthreads_or(has)) continue;
+    if (!__syncthreads_or(has)) return;
   }
   const float *row = (z ? draft : target) + ((int64_t)b * r_max + r) * vocab;
   const uint32_t *mw = kMasked ? allowed + ((int64_t)b * r_max + r) * n_mw : nullptr;
@@ -1281,7 +1281,6 @@ __global__ void __launch_bounds__(kArgmaxThreads) stochastic_validate_kernel(
   if (threadIdx.x == 0) {
     if (nan) atomicOr(err, SDB_ERR_NAN);
     if (!alive) atomicOr(err, SDB_ERR_NO_ALLOWED);
-  }
   }
 }
 
@@ -1438,20 +1437,33 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
   cfg.gridDim = dim3(batch * ncl);
   cfg.blockDim = dim3(sdb::kWThreads);
   cfg.stream = s;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = ncl;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
+  // lazy mode: the walk's launches at the highest priority (a validation
+  // scan may be streaming beside them at the lowest)
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ncl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = greatest;
+  cfg.attrs = attr;
+  cfg.numAttrs = lazy ? 2 : 1;
+  cudaLaunchConfig_t scfg = {};
+  scfg.blockDim = dim3(sdb::kStThreads);
+  scfg.dynamicSmemBytes = smem;
+  scfg.stream = s;
+  scfg.attrs = &attr[1];
+  scfg.numAttrs = lazy ? 1 : 0;
   auto stats_launch = [&](dim3 grid, const int32_t *rows) {
+    scfg.gridDim = grid;
     if (allowed)
-      sdb::row_stats_kernel<true><<<grid, sdb::kStThreads, smem, s>>>(
-          target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err, allowed, allowed_words, rows);
+      cudaLaunchKernelEx(&scfg, sdb::row_stats_kernel<true>, target_logits, draft_logits, r_max, vocab, a, top_p,
+                         parent, n_rows, stats, err, allowed, allowed_words, rows);
     else
-      sdb::row_stats_kernel<false><<<grid, sdb::kStThreads, smem, s>>>(
-          target_logits, draft_logits, r_max, vocab, a, top_p, parent, n_rows, stats, err, nullptr, 0, rows);
+      cudaLaunchKernelEx(&scfg, sdb::row_stats_kernel<false>, target_logits, draft_logits, r_max, vocab, a, top_p,
+                         parent, n_rows, stats, err, (const uint32_t *)nullptr, 0, rows);
   };
 #define SDB_WALK(CL, M, L)                                                                                        \
   cudaLaunchKernelEx(&cfg, sdb::stochastic_walk_kernel<CL, M, L>, target_logits, draft_logits, r_max, vocab, a,    \
@@ -1519,14 +1531,23 @@ extern "C" int sdb_stochastic_validate(const float *target_logits, const float *
       (allowed && allowed_words < (vocab + 31) / 32))
     return SDB_E_INVALID;
   if (batch == 0) return SDB_OK;
-  dim3 grid(std::max(1, sdb::num_sms() / 2));
-  cudaStream_t s = sdb::as_stream(stream);
-  if (allowed)
-    sdb::stochastic_validate_kernel<true><<<grid, sdb::kArgmaxThreads, 0, s>>>(
-        target_logits, draft_logits, r_max, vocab, parent, n_rows, allowed, allowed_words, err, batch);
-  else
-    sdb::stochastic_validate_kernel<false><<<grid, sdb::kArgmaxThreads, 0, s>>>(
-        target_logits, draft_logits, r_max, vocab, parent, n_rows, nullptr, 0, err, batch);
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(r_max, batch, 2);
+  cfg.blockDim = dim3(sdb::kArgmaxThreads);
+  cfg.stream = sdb::as_stream(stream);
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributePriority;
+  attr.val.priority = least;  // below the lazy walk's launches
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  cudaError_t le =
+      allowed ? cudaLaunchKernelEx(&cfg, sdb::stochastic_validate_kernel<true>, target_logits, draft_logits, r_max,
+                                   vocab, parent, n_rows, allowed, allowed_words, err, batch)
+              : cudaLaunchKernelEx(&cfg, sdb::stochastic_validate_kernel<false>, target_logits, draft_logits, r_max,
+                                   vocab, parent, n_rows, (const uint32_t *)nullptr, 0, err, batch);
+  if (le != cudaSuccess) return sdb::record_cuda_error(le);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

@@ -89,12 +89,15 @@ def _oracle_accept(aug, tl, dl, tokens, uniforms, temperature, top_p):
     return O.mss_verify(parent, tokens[1:], ndists, tdists, uniforms)
 
 
-@pytest.mark.parametrize("top_p", [0.9, 1.0])
-def test_accept_stochastic_full_vocab_vs_oracle(top_p):
+@pytest.mark.parametrize("top_p,lazy", [(0.9, True), (0.9, False), (1.0, True)])
+def test_accept_stochastic_full_vocab_vs_oracle(top_p, lazy):
     """Llama-3 vocabulary (128,256), the 64-row EAGLE tree, uniforms drawn on
     the device from (seed, step): path, next token and uniforms_used must
-    equal the float64 oracle's."""
-    from paper_2508_08192_b200.sampling import accept_stochastic
+    equal the float64 oracle's (lazy walk and eager every-row reduction)."""
+    from paper_2508_08192_b200.sampling import StochasticAcceptor
+
+    def accept_stochastic(*a, **k):
+        return StochasticAcceptor(lazy=lazy)(*a, **k)
 
     B, V, T = 3, 128256, 1.0
     aug, tl, dl, tokens, seeds, steps = _stochastic_case(B, V, TREE64, T, top_p, seed=11)
@@ -331,9 +334,12 @@ def test_accept_greedy_fsm_masked_vs_oracle():
         assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used
 
 
-@pytest.mark.parametrize("top_p", [0.9, 1.0])
-def test_accept_stochastic_fsm_masked_vs_oracle(top_p):
-    from paper_2508_08192_b200.sampling import accept_stochastic, pack_allowed
+@pytest.mark.parametrize("top_p,lazy", [(0.9, True), (0.9, False), (1.0, True)])
+def test_accept_stochastic_fsm_masked_vs_oracle(top_p, lazy):
+    from paper_2508_08192_b200.sampling import StochasticAcceptor, pack_allowed
+
+    def accept_stochastic(*a, **k):
+        return StochasticAcceptor(lazy=lazy)(*a, **k)
 
     B, V, T = 3, 8192, 1.0
     rng = np.random.default_rng(9)
@@ -376,11 +382,17 @@ def test_fsm_dead_row_raises_flag():
     allowed = np.ones((1, R, V), dtype=bool)
     allowed[0, 1] = False  # dead FSM state on row 1
     words = pack_allowed(torch.tensor(allowed, device="cuda"))
+    from paper_2508_08192_b200.sampling import StochasticAcceptor
+
     par = torch.tensor([aug], dtype=torch.int32, device="cuda")
     nr = torch.tensor([R], dtype=torch.int32, device="cuda")
     tok = torch.zeros((1, R), dtype=torch.int32, device="cuda")
     g = accept_greedy(lg, par, nr, tok, allowed=words)
     s = accept_stochastic(lg, lg, 1.0, 0.9, par, nr, tok, torch.tensor(rng.random((1, R)), device="cuda"),
                           allowed=words)
+    # lazy: the dead row is never visited (path stops at the root); the
+    # validation scan still raises, like the reference's every-row target_dist
+    s2 = StochasticAcceptor(lazy=True)(lg, lg, 1.0, 0.9, par, nr, tok,
+                                       torch.tensor(rng.random((1, R)), device="cuda"), allowed=words)
     torch.cuda.synchronize()
-    assert int(g.err[0]) & 32 and int(s.err[0]) & 32
+    assert int(g.err[0]) & 32 and int(s.err[0]) & 32 and int(s2.err[0]) & 32

@@ -31,6 +31,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "tree-verify μs/step & HBM GB/s (% of 8 TB/s) at bs1–64, 8k ctx, 1/2/4/8 GPU"
 
+# the 63-node EAGLE tree of SURVEY.md 8(d) (R = 64 rows with the root); the
+# mandatory R = 65 variant appends a 7th child of node 0 (`--tree 65`)
 TREE64 = [-1, -1, -1, -1, -1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 4, 4, 5, 5, 6, 7,
           8, 8, 8, 8, 9, 9, 9, 10, 10, 10, 11, 11, 12, 13, 14, 15, 32, 32, 32, 33, 33, 34, 34, 35, 36, 37, 48, 48, 49,
           50, 51]
@@ -48,6 +50,7 @@ CONFIGS = {
                ctx=0, bs=64, V=128256, accept_only=True, mode="stochastic"),
 }
 TEMPERATURE, TOP_P = 1.0, 0.9
+TREE = TREE64  # set from --tree
 
 
 def _augment(parent):
@@ -126,7 +129,7 @@ def make_inputs(cfg, shard, device, seed=0, mode="greedy"):
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     B, Hq, Hkv, d, C, bs, V = (cfg[k] for k in ("B", "Hq", "Hkv", "d", "ctx", "bs", "V"))
-    aug = _augment(TREE64)
+    aug = _augment(TREE)
     R = len(aug)
     hkv_l, hq_l = shard.n_kv, shard.n_q
     pages = -(-(C + R) // bs)
@@ -212,7 +215,7 @@ def cpu_sample(cfg, seed=0, mode="greedy"):
     rng = np.random.default_rng(seed)
     B, Hq, Hkv, d, C, bs, V = (cfg[k] for k in ("B", "Hq", "Hkv", "d", "ctx", "bs", "V"))
     g = Hq // Hkv
-    aug = tuple(_augment(TREE64))
+    aug = tuple(_augment(TREE))
     R = len(aug)
     parent = tuple(p - 1 if p > 0 else -1 for p in aug[1:])
     ta = 0.0
@@ -333,11 +336,14 @@ def main():
     ap.add_argument("--mode", default=None, choices=["greedy", "stochastic"],
                     help="acceptance mode (default: greedy, c5: stochastic)")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 tcgen05, 2 SIMT")
+    ap.add_argument("--tree", type=int, default=64, choices=[64, 65], help="R = tree rows (63 or 64 drafts + root)")
     ap.add_argument("--splits", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    global TREE
+    TREE = TREE64 + [0] if args.tree == 65 else TREE64
     cfg = dict(CONFIGS[args.config])
     mode = args.mode or cfg.get("mode", "greedy")
     accept_only = bool(cfg.get("accept_only"))
@@ -375,7 +381,7 @@ def main():
     x, R = make_inputs(cfg, shard, dev, mode=mode)
     from oracle import specdec_oracle as O  # checker only (mask popcount for the FLOP count)
 
-    aug = tuple(_augment(TREE64))
+    aug = tuple(_augment(TREE))
     anc_pairs = int(O.suffix_mask(aug).sum())
     n_parent_rows = len(set(p for p in aug[1:]))
     temperature = 0.0 if mode == "greedy" else TEMPERATURE

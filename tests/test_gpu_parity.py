@@ -880,3 +880,23 @@ def test_verifier_step_mixed_batch_edge_cases(mode):
         assert int(acc.next_token[b]) == nxt and int(acc.uniforms_used[b]) == used, (b, mode)
         O.compact_kv(kp0, kp0.copy(), table[b], int(ctx[b]), f64(tk)[b], f64(tv)[b], list(path), plen + 1)
     np.testing.assert_array_equal(x.k_pool.float().cpu().numpy(), kp0.astype(np.float32))
+
+
+def test_tcgen05_r65_variant_vs_oracle():
+    """The mandatory R = 65 variant (64 drafts: TREE64 + a 7th child of node
+    0, not breadth-first) at 70B shapes: 520 query rows per KV head = three
+    256-row pair tiles, the last one 8 rows deep."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    c = _rand_paged_case(2, 64, 8, 128, 3000, 64, TREE64 + [0], seed=65)
+    assert c["R"] == 65
+    out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                     c["nr"], 128 ** -0.5, kernel=1)
+    torch.cuda.synchronize()
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(c["q"]), f64(c["kp"]), f64(c["vp"]), c["table_np"],
+                                                   c["ctx_np"], f64(c["tk"]), f64(c["tv"]), [c["aug"]] * 2,
+                                                   128 ** -0.5)
+    err = np.abs(out.float().cpu().numpy() - want_o)
+    assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+    assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3

@@ -1227,10 +1227,9 @@ template <bool kMasked>
 __global__ void __launch_bounds__(kArgmaxThreads) stochastic_validate_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab,
     const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, const uint32_t *__restrict__ allowed,
-    int n_mw, int32_t *__restrict__ err, int batch) {
+    int n_mw, int32_t *__restrict__ err) {
   // one row per CTA, launched at the lowest priority: SMs freed by these
   // short CTAs go to the latency-bound lazy walk's CTAs first
-  (void)batch;
   const int r = blockIdx.x, b = blockIdx.y, z = blockIdx.z;
   const int n = min(n_rows[b], r_max);
   if (r >= n) return;
@@ -1242,8 +1241,17 @@ __global__ void __launch_bounds__(kArgmaxThreads) stochastic_validate_kernel(
   }
   const float *row = (z ? draft : target) + ((int64_t)b * r_max + r) * vocab;
   const uint32_t *mw = kMasked ? allowed + ((int64_t)b * r_max + r) * n_mw : nullptr;
+  // NaN only counts at allowed positions (the reference masks first); a
+  // masked row needs at least one allowed token
   float nacc = -INFINITY;
   bool any = !kMasked;
+  auto one = [&](float x, int j) {
+    if (kMasked) {
+      if (!((__ldg(mw + (j >> 5)) >> (j & 31)) & 1u)) return;
+      any = true;
+    }
+    nacc = max_nan(nacc, x);
+  };
   if ((vocab & 3) == 0 && ((uintptr_t)row & 15) == 0) {
     const float4 *r4 = reinterpret_cast<const float4 *>(row);
     const int n4 = vocab >> 2;
@@ -1252,29 +1260,24 @@ __global__ void __launch_bounds__(kArgmaxThreads) stochastic_validate_kernel(
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = i0 + u * kArgmaxThreads + threadIdx.x;
-        v[u] = i < n4 ? __ldcs(r4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (kMasked && i < n4) {
-          const float4 m = mask4(v[u], mw, i);
-          any |= (m.x != -INFINITY) | (m.y != -INFINITY) | (m.z != -INFINITY) | (m.w != -INFINITY) |
-                 (((__ldg(mw + (i >> 3)) >> ((i & 7) * 4)) & 0xFu) != 0);
-          v[u] = make_float4(m.x == -INFINITY ? 0.f : m.x, m.y == -INFINITY ? 0.f : m.y,
-                             m.z == -INFINITY ? 0.f : m.z, m.w == -INFINITY ? 0.f : m.w);
-        }
+        v[u] = i < n4 ? __ldcs(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) nacc = max_nan(nacc, max_nan(max_nan3(v[u].x, v[u].y, v[u].z), v[u].w));
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kArgmaxThreads + threadIdx.x;
+        if (!kMasked) {
+          nacc = max_nan(nacc, max_nan(max_nan3(v[u].x, v[u].y, v[u].z), v[u].w));
+        } else if (i < n4) {
+          one(v[u].x, 4 * i);
+          one(v[u].y, 4 * i + 1);
+          one(v[u].z, 4 * i + 2);
+          one(v[u].w, 4 * i + 3);
+        }
+      }
     }
-    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kArgmaxThreads) {
-      const float x = kMasked ? mask1(row[j], mw, j) : row[j];
-      if (kMasked && ((__ldg(mw + (j >> 5)) >> (j & 31)) & 1u)) any = true;
-      nacc = max_nan(nacc, x == -INFINITY ? 0.f : x);
-    }
+    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kArgmaxThreads) one(row[j], j);
   } else {
-    for (int j = threadIdx.x; j < vocab; j += kArgmaxThreads) {
-      const float x = kMasked ? mask1(row[j], mw, j) : row[j];
-      if (kMasked && ((__ldg(mw + (j >> 5)) >> (j & 31)) & 1u)) any = true;
-      nacc = max_nan(nacc, x == -INFINITY ? 0.f : x);
-    }
+    for (int j = threadIdx.x; j < vocab; j += kArgmaxThreads) one(row[j], j);
   }
   const bool nan = __syncthreads_or(nacc != nacc);
   const bool alive = __syncthreads_or(any);
@@ -1544,9 +1547,9 @@ extern "C" int sdb_stochastic_validate(const float *target_logits, const float *
   cfg.numAttrs = 1;
   cudaError_t le =
       allowed ? cudaLaunchKernelEx(&cfg, sdb::stochastic_validate_kernel<true>, target_logits, draft_logits, r_max,
-                                   vocab, parent, n_rows, allowed, allowed_words, err, batch)
+                                   vocab, parent, n_rows, allowed, allowed_words, err)
               : cudaLaunchKernelEx(&cfg, sdb::stochastic_validate_kernel<false>, target_logits, draft_logits, r_max,
-                                   vocab, parent, n_rows, (const uint32_t *)nullptr, 0, err, batch);
+                                   vocab, parent, n_rows, (const uint32_t *)nullptr, 0, err);
   if (le != cudaSuccess) return sdb::record_cuda_error(le);
   SDB_CHECK_LAUNCH();
   return SDB_OK;

@@ -408,6 +408,7 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   const int per_tile = kTileM * sp.cta_group;
   // pair kernel: one 256-row query tile per unit (three S slots fill TMEM)
   sp.nt = (sp.cta_group == 1 && rows > per_tile) ? 2 : 1;
+  if (const char *fnt = getenv("SDB_ATTN_NT")) sp.nt = atoi(fnt) == 1 ? 1 : sp.nt;  // testing knob
   sp.rows_unit = sp.nt * per_tile;
   sp.m_blocks = cdiv(rows, sp.rows_unit);
   sp.units = p.batch * p.hkv * sp.m_blocks;

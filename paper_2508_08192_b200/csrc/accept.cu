@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <math.h>
+#include <stdlib.h>
 
 #include <cooperative_groups.h>
 
@@ -903,9 +904,9 @@ __device__ __forceinline__ float q_of(const WalkRow &w, float a, int t) {
 // sum over [v0, v1) of max(P - c Q, 0) / M (per-element fp32, f64
 // accumulation), with the values optionally stored (residual); 16-byte
 // loads, 4 iterations in flight.
-template <bool kStore>
+// `store` (global, vocab-indexed) and `sst` (shared, slice-indexed) are optional.
 __device__ __forceinline__ double residual_part(const WalkRow &w, float a, double c, double M, int v0, int v1,
-                                                bool vec, float *__restrict__ store) {
+                                                bool vec, float *__restrict__ store, float *__restrict__ sst) {
   double part = 0.0;
   const float *__restrict__ tl = w.tl;
   const float *__restrict__ dl = w.dl;
@@ -914,7 +915,8 @@ __device__ __forceinline__ double residual_part(const WalkRow &w, float a, doubl
     const float p = p_val(w, a, l, i);
     const float q = dl ? q_val(w, a, d) : 0.f;
     const float v = fmaxf(fmaf(-cf, q, p), 0.f) * inv_m;
-    if (kStore) store[i] = v;
+    if (store) store[i] = v;
+    if (sst) sst[i - v0] = v;
     part += (double)v;
   };
   if (vec) {
@@ -935,6 +937,84 @@ __device__ __forceinline__ double residual_part(const WalkRow &w, float a, doubl
       one(mask1(tl[i], w.mw, i), dl ? mask1(dl[i], w.mw, i) : 0.f, i);
   } else {
     for (int i = v0 + threadIdx.x; i < v1; i += kWThreads) one(mask1(tl[i], w.mw, i), dl ? mask1(dl[i], w.mw, i) : 0.f, i);
+  }
+  return part;
+}
+
+// A node's first rejection pass also compacts the (P, Q) pairs with P > 0
+// into shared memory (kWCap pairs per CTA): every later sibling's residual
+// sum then reads only the nucleus -- elements with P == 0 add exactly 0 to
+// sum max(P - c Q, 0).  Overflow (a nucleus wider than kWCap per slice, e.g.
+// top_p = 1) falls back to full-row passes.
+constexpr int kWCap = 12288;  // 96 KB of float2 per CTA (two CTAs per SM)
+
+__device__ __forceinline__ double residual_compact(const WalkRow &w, float a, float cf, int v0, int v1, bool vec,
+                                                   float2 *__restrict__ list, int *s_cnt) {
+  double part = 0.0;
+  const float *__restrict__ tl = w.tl;
+  const float *__restrict__ dl = w.dl;
+  const int lane = threadIdx.x & 31;
+  // warp-aggregated, order-free append of this thread's kept pairs
+  auto append = [&](int n, const float *pp, const float *qq) {
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(SDB_FULL_MASK, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(SDB_FULL_MASK, incl, 31);
+    int base = 0;
+    if (lane == 31 && total) base = atomicAdd(s_cnt, total);
+    base = __shfl_sync(SDB_FULL_MASK, base, 31) + incl - n;
+    for (int k = 0; k < n; ++k)
+      if (base + k < kWCap) list[base + k] = make_float2(pp[k], qq[k]);
+  };
+  auto one = [&](float l, float d, int i, float *pp, float *qq, int &n) {
+    const float p = p_val(w, a, l, i);
+    const float q = dl ? q_val(w, a, d) : 0.f;
+    part += (double)fmaxf(fmaf(-cf, q, p), 0.f);
+    if (p > 0.f) {
+      pp[n] = p;
+      qq[n] = q;
+      ++n;
+    }
+  };
+  const int start = vec ? v0 + (((v1 - v0) >> 2) << 2) : v0;
+  if (vec) {
+    const float4 *__restrict__ t4 = reinterpret_cast<const float4 *>(tl + v0);
+    const float4 *__restrict__ d4 = dl ? reinterpret_cast<const float4 *>(dl + v0) : nullptr;
+    const int n4 = (v1 - v0) >> 2;
+    // warp-uniform trip count (every lane takes part in the append)
+    for (int i = threadIdx.x; i - lane < n4; i += kWThreads) {
+      float pp[4], qq[4];
+      int n = 0;
+      if (i < n4) {
+        const float4 t = mask4(__ldg(t4 + i), w.mw, (v0 >> 2) + i);
+        const float4 d = d4 ? mask4(__ldg(d4 + i), w.mw, (v0 >> 2) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int base = v0 + 4 * i;
+        one(t.x, d.x, base, pp, qq, n);
+        one(t.y, d.y, base + 1, pp, qq, n);
+        one(t.z, d.z, base + 2, pp, qq, n);
+        one(t.w, d.w, base + 3, pp, qq, n);
+      }
+      append(n, pp, qq);
+    }
+  }
+  for (int i = start + threadIdx.x; i - lane < v1; i += kWThreads) {
+    float pp[1], qq[1];
+    int n = 0;
+    if (i < v1) one(mask1(tl[i], w.mw, i), dl ? mask1(dl[i], w.mw, i) : 0.f, i, pp, qq, n);
+    append(n, pp, qq);
+  }
+  return part;
+}
+
+__device__ __forceinline__ double residual_list(const float2 *__restrict__ list, int cnt, float cf) {
+  double part = 0.0;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < cnt; i += kWThreads) {
+    const float2 pq = list[i];
+    part += (double)fmaxf(fmaf(-cf, pq.y, pq.x), 0.f);
   }
   return part;
 }
@@ -962,7 +1042,7 @@ struct LazyWalk {
 };
 
 template <int kCl, bool kMasked, bool kLazy>
-__global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
+__global__ void __launch_bounds__(kWThreads, 2) stochastic_walk_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
     const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, const int32_t *__restrict__ tokens,
     const double *__restrict__ uniforms, int n_uniforms, const RowStats *__restrict__ stats,
@@ -971,7 +1051,8 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     const uint32_t *__restrict__ allowed, int n_mw, LazyWalk *__restrict__ lw, int32_t *__restrict__ cur_rows) {
   __shared__ double red[32];
   __shared__ double slots[2];
-  __shared__ int s_flag;
+  __shared__ int s_flag, s_cnt;
+  extern __shared__ float2 wlist[];  // kWCap compacted (P, Q) pairs of the current node
   cg::cluster_group cl = cg::this_cluster();
   const int crank = (int)cl.block_rank();
   const int b = blockIdx.x / kCl;
@@ -997,7 +1078,10 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     c = s0.c;
     M = s0.M;
   }
-  if (threadIdx.x == 0) s_flag = 0;
+  if (threadIdx.x == 0) {
+    s_flag = 0;
+    s_cnt = 0;
+  }
   __syncthreads();
   if (kLazy) {
     // the visited row (and the q of its children) must be valid
@@ -1012,6 +1096,7 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
   }
   __syncthreads();
   if (s_flag) {
+    cl.sync();  // uniform across the cluster; lw[b] read by every CTA first
     if (threadIdx.x == 0 && crank == 0) {
       path_len[b] = 0;
       next_token[b] = 0;
@@ -1021,7 +1106,7 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
         cur_rows[b] = -1;
       }
     }
-    return;  // uniform across the cluster: no exchange follows
+    return;
   }
   bool failed = false;
   auto make_row = [&](int r) {
@@ -1044,64 +1129,112 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     return w;
   };
   WalkRow w = make_row(cur);
+  int comp = 0;  // 0: no list for this node yet, 1: list valid (cnt pairs), 2: overflowed
+  int cnt = 0;
+  // children of the current node, a window of kWThreads rows at a time:
+  // ordered compaction + every child's p(t), q(t) and uniform fetched in
+  // parallel, so the sequential decisions below read shared memory only
+  __shared__ int s_wcnt[kWThreads / 32];
+  __shared__ int s_child[kWThreads];
+  __shared__ float s_pt[kWThreads], s_qt[kWThreads];
+  __shared__ double s_u[kWThreads];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   while (true) {
     bool descended = false;
-    for (int j = cur + 1; j < n; ++j) {
-      if (par[j] != cur) continue;
-      if (used >= n_uniforms) {
-        failed = true;
-        break;
-      }
-      const double u = uni[used++];
-      const int t = tok[j];
-      const double pt_full = (double)p_of(w, a, t);
-      const double qt = (double)q_of(w, a, t);
-      const double pt = fmax(pt_full - c * qt, 0.0) / M;
-      const bool acc = qt <= 0.0 ? pt > 0.0 : u < fmin(1.0, pt / qt);
-      if (acc) {
-        if (threadIdx.x == 0 && crank == 0) path[(int64_t)b * r_max + len] = j - 1;
-        ++len;
-        cur = j;
-        c = 0.0;
-        M = 1.0;
-        if (kLazy) {  // the next level reduces row j first
-          if (threadIdx.x == 0 && crank == 0) {
-            LazyWalk s1;
-            s1.c = 0.0;
-            s1.M = 1.0;
-            s1.cur = j;
-            s1.used = used;
-            s1.len = len;
-            s1.done = 0;
-            lw[b] = s1;
-            cur_rows[b] = j;
-          }
-          cl.sync();  // peers may still read this CTA's exchange slots
-          return;
-        }
-        w = make_row(cur);
-        descended = true;
-        break;
-      }
-      // rejection: residual norm(max(p - q, 0)) == max(P - c' Q, 0) / M'
-      const double cn = c + M;
-      const double part = block_sum<kWThreads>(residual_part<false>(w, a, cn, 1.0, v0, v1, vec, nullptr), red);
-      cluster_exchange<kCl>(part, slots, phase, vals);
-      double Mn = 0.0;
+    for (int lo = cur + 1; lo < n && !descended && !failed; lo += kWThreads) {
+      const int jj = lo + threadIdx.x;
+      const bool is_child = jj < n && par[jj] == cur;
+      const unsigned bal = __ballot_sync(SDB_FULL_MASK, is_child);
+      __syncthreads();  // the previous window's values are consumed
+      if (lane == 0) s_wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int off = 0, nch = 0;
 #pragma unroll
-      for (int q = 0; q < kCl; ++q) Mn += vals[q];
-      if (Mn / M <= 1e-12) {
-        c = 0.0;  // anchor fallback (sampling.py:193-195)
-        M = 1.0;
-      } else {
-        c = cn;
-        M = Mn;
+      for (int q = 0; q < kWThreads / 32; ++q) {
+        off += q < warp ? s_wcnt[q] : 0;
+        nch += s_wcnt[q];
+      }
+      if (is_child) {
+        const int k = off + __popc(bal & ((1u << lane) - 1u));
+        const int t = tok[jj];
+        s_child[k] = jj;
+        s_pt[k] = p_of(w, a, t);
+        s_qt[k] = q_of(w, a, t);
+        s_u[k] = used + k < n_uniforms ? uni[used + k] : 0.0;
+      }
+      __syncthreads();
+      for (int k = 0; k < nch; ++k) {
+        const int j = s_child[k];
+        if (used >= n_uniforms) {
+          failed = true;
+          break;
+        }
+        const double u = s_u[k];
+        ++used;
+        const double pt_full = (double)s_pt[k];
+        const double qt = (double)s_qt[k];
+        const double pt = fmax(pt_full - c * qt, 0.0) / M;
+        const bool acc = qt <= 0.0 ? pt > 0.0 : u < fmin(1.0, pt / qt);
+        if (acc) {
+          if (threadIdx.x == 0 && crank == 0) path[(int64_t)b * r_max + len] = j - 1;
+          ++len;
+          cur = j;
+          c = 0.0;
+          M = 1.0;
+          if (kLazy) {  // the next level reduces row j first
+            // every CTA of the cluster has read lw[b] (kernel start) and is
+            // done with this CTA's exchange slots before lw[b] changes
+            cl.sync();
+            if (threadIdx.x == 0 && crank == 0) {
+              LazyWalk s1;
+              s1.c = 0.0;
+              s1.M = 1.0;
+              s1.cur = j;
+              s1.used = used;
+              s1.len = len;
+              s1.done = 0;
+              lw[b] = s1;
+              cur_rows[b] = j;
+            }
+            return;
+          }
+          w = make_row(cur);
+          comp = 0;
+          descended = true;
+          break;
+        }
+        // rejection: residual norm(max(p - q, 0)) == max(P - c' Q, 0) / M'
+        const double cn = c + M;
+        double part;
+        if (comp == 0) {
+          part = block_sum<kWThreads>(residual_compact(w, a, (float)cn, v0, v1, vec, wlist, &s_cnt), red);
+          cnt = s_cnt;  // final: block_sum's barriers follow every append
+          comp = cnt <= kWCap ? 1 : 2;
+          __syncthreads();
+          if (threadIdx.x == 0) s_cnt = 0;  // ordered before the next node's appends by the exchange barrier
+        } else if (comp == 1) {
+          part = block_sum<kWThreads>(residual_list(wlist, cnt, (float)cn), red);
+        } else {
+          part = block_sum<kWThreads>(residual_part(w, a, cn, 1.0, v0, v1, vec, nullptr, nullptr), red);
+        }
+        cluster_exchange<kCl>(part, slots, phase, vals);
+        double Mn = 0.0;
+#pragma unroll
+        for (int q = 0; q < kCl; ++q) Mn += vals[q];
+        if (Mn / M <= 1e-12) {
+          c = 0.0;  // anchor fallback (sampling.py:193-195)
+          M = 1.0;
+        } else {
+          c = cn;
+          M = Mn;
+        }
       }
     }
     if (failed || !descended) break;
   }
   if (!failed && used >= n_uniforms) failed = true;
   if (failed) {
+    cl.sync();  // (as above: lw[b] read by every CTA, exchange slots free)
     if (threadIdx.x == 0 && crank == 0) {
       atomicOr(err, SDB_ERR_UNIFORMS);
       path_len[b] = len;
@@ -1112,17 +1245,17 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
         cur_rows[b] = -1;
       }
     }
-    cl.sync();
     return;
   }
   const double u = uni[used++];
   // bonus: inverse CDF of p = max(P - c Q, 0) / M over the vocab in index
   // order (sample_from, sampling.py:105-109): slice masses -> owning CTA.
   float *res_row = residual ? residual + (int64_t)b * vocab : nullptr;
-  const double mine = block_sum<kWThreads>(
-      res_row ? residual_part<true>(w, a, c, M, v0, v1, vec, res_row) : residual_part<false>(w, a, c, M, v0, v1, vec,
-                                                                                           nullptr),
-      red);
+  // the slice's values stay in shared memory (the compaction list is dead)
+  // for the owner's inverse CDF
+  float *sv = v1 - v0 <= 2 * kWCap ? reinterpret_cast<float *>(wlist) : nullptr;
+  __syncthreads();
+  const double mine = block_sum<kWThreads>(residual_part(w, a, c, M, v0, v1, vec, res_row, sv), red);
   cluster_exchange<kCl>(mine, slots, phase, vals);
   double base = 0.0, total = 0.0;
   int owner = -1;
@@ -1141,12 +1274,14 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     __shared__ double segsum[kWThreads / 32];
     __shared__ double s_prefix;
     __shared__ int s_seg, s_tok;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // (warp, lane as above)
     constexpr int nw = kWThreads / 32;
     const int seg = (v1 - v0 + nw - 1) / nw;
     const int s0 = v0 + warp * seg, s1 = min(v1, s0 + seg);
     const float cf = (float)c, inv_m = (float)(1.0 / M);
-    auto pval = [&](int i) { return (double)(fmaxf(fmaf(-cf, q_of(w, a, i), p_of(w, a, i)), 0.f) * inv_m); };
+    auto pval = [&](int i) {
+      return sv ? (double)sv[i - v0] : (double)(fmaxf(fmaf(-cf, q_of(w, a, i), p_of(w, a, i)), 0.f) * inv_m);
+    };
     double wsum = 0.0;
     for (int i = s0 + lane; i < s1; i += 32) wsum += pval(i);
     wsum = warp_sum(wsum);
@@ -1190,6 +1325,7 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
     __syncthreads();
     if (threadIdx.x == 0) next_token[b] = min(s_tok, vocab - 1);
   }
+  cl.sync();  // peers may still read this CTA's exchange slots; lw[b] read by all
   if (threadIdx.x == 0 && crank == 0) {
     path_len[b] = len;
     uniforms_used[b] = used;
@@ -1198,7 +1334,6 @@ __global__ void __launch_bounds__(kWThreads) stochastic_walk_kernel(
       cur_rows[b] = -1;
     }
   }
-  cl.sync();  // peers may still read this CTA's exchange slots
 }
 
 // lazy walk start: every sequence at its root row
@@ -1409,6 +1544,43 @@ extern "C" int sdb_accept_stochastic(const float *target_logits, const float *dr
                                   next_token, uniforms_used, residual, err, nullptr, 0, stream);
 }
 
+// co-resident clusters of the walk kernel at cluster size CL (cached per
+// process; one device per process)
+constexpr int kWalkSmem = sdb::kWCap * (int)sizeof(float2);
+
+template <int CL, bool M, bool L>
+static int walk_max_clusters_of() {
+  static int cached = -1;
+  if (cached < 0) {
+    cudaFuncSetAttribute(sdb::stochastic_walk_kernel<CL, M, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kWalkSmem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * 1024);
+    cfg.blockDim = dim3(sdb::kWThreads);
+    cfg.dynamicSmemBytes = kWalkSmem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = CL;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, sdb::stochastic_walk_kernel<CL, M, L>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = sdb::num_sms() / CL;
+    }
+    cached = n;
+  }
+  return cached;
+}
+
+template <int CL>
+static int walk_max_clusters(bool lazy, bool masked) {
+  if (lazy) return masked ? walk_max_clusters_of<CL, true, true>() : walk_max_clusters_of<CL, false, true>();
+  return masked ? walk_max_clusters_of<CL, true, false>() : walk_max_clusters_of<CL, false, false>();
+}
+
 static int accept_stochastic_impl(const float *target_logits, const float *draft_logits, int batch, int r_max,
                                   int vocab, float temperature, float top_p, const int32_t *parent,
                                   const int32_t *n_rows, const int32_t *tokens, const double *uniforms,
@@ -1434,11 +1606,22 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
   const size_t smem = sizeof(sdb::StSmem);
   cudaFuncSetAttribute(sdb::row_stats_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(sdb::row_stats_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  // cluster size: enough CTAs to cover the SMs (8 = portable maximum)
-  const int ncl = batch * 8 <= 4 * sdb::num_sms() ? 8 : 4;
+  // cluster size: the widest (8 = portable maximum) whose clusters for the
+  // whole batch fit in two waves -- a wider cluster halves every CTA's
+  // full-slice passes, which costs more than a second wave of early-exiting
+  // clusters (C5, B 64: 0.94 ms at 8 wide vs 1.18 ms at 4 wide, one wave)
+  const int mc8 = walk_max_clusters<8>(lazy, allowed != nullptr);
+  const int mc4 = walk_max_clusters<4>(lazy, allowed != nullptr);
+  (void)walk_max_clusters<2>(lazy, allowed != nullptr);  // (sets the smem attribute)
+  int ncl = batch <= 2 * mc8 ? 8 : batch <= 2 * mc4 ? 4 : 2;
+  if (const char *e = getenv("SDB_WALK_CL")) {  // experiments
+    const int v = atoi(e);
+    if (v == 2 || v == 4 || v == 8) ncl = v;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(batch * ncl);
   cfg.blockDim = dim3(sdb::kWThreads);
+  cfg.dynamicSmemBytes = kWalkSmem;
   cfg.stream = s;
   // lazy mode: the walk's launches at the highest priority (a validation
   // scan may be streaming beside them at the lowest)
@@ -1474,9 +1657,11 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
                      next_token, uniforms_used, residual, err, allowed, allowed_words, lw, cur_rows)
   auto walk_launch = [&]() {
     if (lazy) {
+      if (ncl == 2) return allowed ? SDB_WALK(2, true, true) : SDB_WALK(2, false, true);
       if (ncl == 4) return allowed ? SDB_WALK(4, true, true) : SDB_WALK(4, false, true);
       return allowed ? SDB_WALK(8, true, true) : SDB_WALK(8, false, true);
     }
+    if (ncl == 2) return allowed ? SDB_WALK(2, true, false) : SDB_WALK(2, false, false);
     if (ncl == 4) return allowed ? SDB_WALK(4, true, false) : SDB_WALK(4, false, false);
     return allowed ? SDB_WALK(8, true, false) : SDB_WALK(8, false, false);
   };

@@ -387,7 +387,7 @@ class StochasticAcceptor:
     ``lazy``: only the rows the MSS walk visits are reduced, one tree level
     per launch pair, while a validation scan of every row (the reference's
     error behaviour) runs concurrently on a side stream; "auto" picks it from
-    48 sequences up.  ``levels`` (tree depth + 1) must be given when
+    28 sequences up.  ``levels`` (tree depth + 1) must be given when
     capturing a CUDA graph.  Results are identical either way."""
 
     def __init__(self, lazy="auto", levels=None):
@@ -431,11 +431,12 @@ class StochasticAcceptor:
                 o["uni"] = torch.empty((b, r), dtype=torch.float64, device=dev)
             uniforms = device_uniforms(seeds, steps, r, out=o["uni"], stream=stream)
         n_words = allowed.shape[-1] if allowed is not None else 0
-        # the lazy walk costs ~levels x 110 us of latency whatever the batch;
-        # reducing every row costs ~23 us per sequence (measured, V 128k):
-        # lazy wins from about 48 sequences (C5 B 64: 1.42 -> 1.15 ms; C3 B
-        # 32: eager 0.78 vs lazy 0.84 ms)
-        lazy = self.lazy if self.lazy != "auto" else (b >= 48)
+        # the lazy walk + concurrent validation scan costs ~440 us at B 8 and
+        # grows slowly; reducing every row costs ~20 us per sequence
+        # (tools/lazy_sweep.py, V 128k, tree64): lazy wins from about 28
+        # sequences (B 24: 566 eager / 637 lazy; B 32: 727 / 684; B 64:
+        # 1369 / 944 us)
+        lazy = self.lazy if self.lazy != "auto" else (b >= 28)
         levels = self.levels
         if lazy and levels is None and not torch.cuda.is_current_stream_capturing():
             levels = tree_levels(parent)

@@ -89,12 +89,19 @@ def _oracle_accept(aug, tl, dl, tokens, uniforms, temperature, top_p):
     return O.mss_verify(parent, tokens[1:], ndists, tdists, uniforms)
 
 
-@pytest.mark.parametrize("top_p,lazy", [(0.9, True), (0.9, False), (1.0, True)])
-def test_accept_stochastic_full_vocab_vs_oracle(top_p, lazy):
+@pytest.mark.parametrize("top_p,lazy,walk_cl", [(0.9, True, None), (0.9, False, None), (1.0, True, None),
+                                                 (0.9, True, "4"), (0.9, False, "2")])
+def test_accept_stochastic_full_vocab_vs_oracle(top_p, lazy, walk_cl, monkeypatch):
     """Llama-3 vocabulary (128,256), the 64-row EAGLE tree, uniforms drawn on
     the device from (seed, step): path, next token and uniforms_used must
-    equal the float64 oracle's (lazy walk and eager every-row reduction)."""
+    equal the float64 oracle's (lazy walk and eager every-row reduction).
+    walk_cl forces the walk's cluster width: 4 and 2 give vocabulary slices
+    too wide for the shared-memory bonus values, and at 2 the nucleus
+    overflows the shared-memory compaction list (full-row passes)."""
     from paper_2508_08192_b200.sampling import StochasticAcceptor
+
+    if walk_cl:
+        monkeypatch.setenv("SDB_WALK_CL", walk_cl)
 
     def accept_stochastic(*a, **k):
         return StochasticAcceptor(lazy=lazy)(*a, **k)

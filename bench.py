@@ -299,6 +299,37 @@ def run_reference(args, cfg, mode):
     print(json.dumps(line), flush=True)
 
 
+def graph_kernels(graph):
+    """(this library's kernels, all kernels) among the kernel nodes of a
+    captured step, by kernel name (namespace sdb), or None when the graph
+    cannot be inspected."""
+    try:
+        from cuda.bindings import driver as cu
+
+        g = cu.CUgraph(graph.raw_cuda_graph())
+        err, _, n = cu.cuGraphGetNodes(g, 0)
+        err, nodes, n = cu.cuGraphGetNodes(g, n)
+        ours = total = 0
+        others = []
+        for nd in nodes[:n]:
+            err, t = cu.cuGraphNodeGetType(nd)
+            if t != cu.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
+                continue
+            total += 1
+            err, prm = cu.cuGraphKernelNodeGetParams(nd)
+            err, name = cu.cuFuncGetName(prm.func)
+            if err == cu.CUresult.CUDA_SUCCESS and b"sdb" in bytes(name):
+                ours += 1
+            else:
+                others.append(bytes(name)[:60].decode(errors="replace"))
+        if others:
+            print(f"[bench] step graph: other kernels {others}", file=sys.stderr)
+        return ours, total
+    except Exception as e:  # noqa: BLE001 - diagnostic only
+        print(f"[bench] graph inspection failed: {e}", file=sys.stderr)
+        return None
+
+
 def graph_time(fn, iters, stream, use_graph=True):
     """Mean device time of fn(): captured into a CUDA graph and replayed
     `iters` times between two events (host launch gaps excluded); eager
@@ -596,7 +627,26 @@ def main():
     # library kernels per step: tree_build 1, attention 2 (persistent kernel +
     # LSE fix-up), acceptance 2 (greedy: keys + walk; stochastic: row stats +
     # walk, + 1 Philox), compaction 1
+    # our kernels per step: counted from the captured graph's kernel nodes;
+    # eager (gloo) runs fall back to the static count of the step's launches
     n_launch = (0 if accept_only else 4) + (2 if mode == "greedy" else 3)
+    counted = None
+    if graph is not None:
+        # a second, kept capture of the step only to count its kernel nodes
+        # (the timed graph is not kept: keep_graph=True measured +4 us at C2)
+        try:
+            kept = torch.cuda.CUDAGraph(keep_graph=True)
+            with torch.cuda.graph(kept):
+                step()
+            counted = graph_kernels(kept)
+            del kept
+        except Exception as e:  # noqa: BLE001 - diagnostic only
+            print(f"[bench] kernel count capture failed: {e}", file=sys.stderr)
+        torch.cuda.synchronize()
+    if counted is not None:
+        n_launch = counted[0]
+        if counted[1] != counted[0]:
+            print(f"[bench] step graph: {counted[0]} library kernels of {counted[1]}", file=sys.stderr)
     line = {
         "metric": METRIC, "value": ms * 1e3, "unit": "us/step", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",

@@ -55,6 +55,11 @@ int sdb_version(void);
 const char *sdb_strerror(int code);
 const char *sdb_last_cuda_error(void);
 
+/* Clear `bytes` (a multiple of 4, 4-byte aligned) of device memory on
+ * `stream` with a small kernel -- the per-call error words (the reference
+ * raises per call: sampling.py:43-49, engine.py:474-475). */
+int sdb_clear_async(void *ptr, int64_t bytes, void *stream);
+
 /* ---- K0: tree mask, depth and positions -------------------------------
  * Replaces TreeSpec.__post_init__ depth + validation (drafttree.py:26-35),
  * suffix_mask (drafttree.py:102-111) and the row positions

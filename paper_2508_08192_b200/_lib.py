@@ -83,6 +83,7 @@ _SIGNATURES = {
     "sdb_version": (I32, []),
     "sdb_strerror": (ctypes.c_char_p, [I32]),
     "sdb_last_cuda_error": (ctypes.c_char_p, []),
+    "sdb_clear_async": (I32, [P, I64, P]),
     "sdb_tree_build": (I32, [P, P, P, I32, I32, I32, P, P, P, P, P]),
     "sdb_attend_heads_f64": (I32, [P, P, P, P, I32, I32, I32, I32, F64, P, P, P]),
     "sdb_merge_partials_f64": (I32, [P, P, I32, I32, I32, I32, P, P, P, P]),
@@ -160,6 +161,11 @@ def check(rc: int, what: str):
 def ptr(t):
     """Device pointer of a torch tensor (or None -> NULL)."""
     return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def clear(t, stream=None):
+    """Zero a device tensor (4-byte words) on `stream` (sdb_clear_async)."""
+    check(lib().sdb_clear_async(ptr(t), t.numel() * t.element_size(), stream_ptr(stream)), "clear")
 
 
 def stream_ptr(stream=None):

@@ -1,4 +1,5 @@
 // Library-level C ABI: version, error strings, device facts.
+#include <algorithm>
 #include <stdio.h>
 #include <string.h>
 
@@ -27,6 +28,11 @@ int num_sms() {
   return cached[dev];
 }
 
+__global__ void clear_words_kernel(uint32_t *__restrict__ p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0u;
+}
+
 }  // namespace sdb
 
 extern "C" {
@@ -45,5 +51,18 @@ const char *sdb_strerror(int code) {
 }
 
 const char *sdb_last_cuda_error(void) { return sdb::g_last_cuda_error; }
+
+int sdb_clear_async(void *ptr, int64_t bytes, void *stream) {
+  if (!ptr || bytes < 0 || (bytes & 3) || ((uintptr_t)ptr & 3)) return SDB_E_INVALID;
+  if (bytes == 0) return SDB_OK;
+  // a kernel, not cudaMemsetAsync: a memset node in a captured step keeps
+  // the graph's forked acceptance branch from overlapping the attention
+  // (C3: 764 vs 670 us measured)
+  const int64_t n = bytes >> 2;
+  sdb::clear_words_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, sdb::as_stream(stream)>>>(
+      reinterpret_cast<uint32_t *>(ptr), n);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
 
 }  // extern "C"

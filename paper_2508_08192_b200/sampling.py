@@ -244,7 +244,7 @@ class GreedyAcceptor:
         else:
             raise SamplingError("logits must be [B, R, V] with unit vocab stride and uniform row stride")
         o = self._alloc(b, r, logits.device)
-        o["err"].zero_()
+        _lib.clear(o["err"], stream)
         rc = _lib.lib().sdb_accept_greedy(_lib.ptr(logits), dt, b, r, v, row_stride, _lib.ptr(parent),
                                           _lib.ptr(n_rows), _lib.ptr(tokens), _lib.ptr(o["keys"]),
                                           _lib.ptr(o["path"]), _lib.ptr(o["path_len"]), _lib.ptr(o["next_token"]),
@@ -260,7 +260,7 @@ class GreedyAcceptor:
         if logits.dtype != torch.float32 or logits.stride(2) != 1 or allowed.dtype != torch.int32:
             raise SamplingError("masked greedy acceptance takes fp32 logits and int32 allowed words")
         o = self._alloc(b, r, logits.device)
-        o["err"].zero_()
+        _lib.clear(o["err"], stream)
         rc = _lib.lib().sdb_accept_greedy_ex(_lib.ptr(logits), b, r, v, logits.stride(1), _lib.ptr(parent),
                                              _lib.ptr(n_rows), _lib.ptr(tokens), _lib.ptr(allowed), allowed.shape[-1],
                                              _lib.ptr(o["keys"]), _lib.ptr(o["path"]), _lib.ptr(o["path_len"]),
@@ -421,7 +421,7 @@ class StochasticAcceptor:
                 err=torch.zeros((1,), dtype=torch.int32, device=dev),
                 residual=torch.empty((b, v), dtype=torch.float32, device=dev) if want_residual else None))
         o = self._bufs[1]
-        o["err"].zero_()
+        _lib.clear(o["err"], stream)
         if uniforms is None:
             # (seeds, steps) on the device: the Philox rows are generated in
             # a launch on the same stream (no host transfer of uniforms)

@@ -235,7 +235,7 @@ def run_sharded_stochastic(ctxs, comm, top_p, levels, stream=None):
             _lib.check(lib.sdb_sharded_accept_phase(c.args, ph, level, sp), f"sharded_accept phase {ph}")
 
     for c in ctxs:
-        c.err.zero_()
+        _lib.clear(c.err, stream)
     phase(_lib.SH_PARTIALS)
     comm.all_gather([c.gathered for c in ctxs], [c.partials for c in ctxs])
     phase(_lib.SH_COMBINE)

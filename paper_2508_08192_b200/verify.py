@@ -134,8 +134,7 @@ class TreeVerifier:
                 and x.logits.dtype == torch.float32 and x.logits.stride(2) == 1
                 and (self.fuse_greedy == "always" or self._scan_hides(x, b, r, main.device))):
             keys, err = self.greedy.fused_keys(b, r, x.logits.device)
-            with torch.cuda.stream(main):
-                err.zero_()  # before tree_build: the attention is tree_build's programmatic dependent
+            _lib.clear(err, main)  # before tree_build: the attention is tree_build's programmatic dependent
             fused = (x.logits, keys, err, 0)
         fork = torch.cuda.Event()
         fork.record(main)

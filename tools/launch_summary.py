@@ -7,7 +7,8 @@ import csv
 import sys
 
 OURS = ("tree_", "argmax_keys", "greedy_walk", "row_stats", "stochastic_walk", "compact_kv", "paged_", "attend_",
-        "merge_", "philox", "target_dist", "mss_", "fixup", "accept", "draft_")
+        "merge_", "philox", "target_dist", "mss_", "fixup", "accept", "draft_", "stochastic_", "lazy_walk",
+        "clear_words", "tape_", "sharded_")
 
 
 def short(name):

@@ -417,14 +417,17 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   sp.w_unit = sp.w_pref + cdiv(p.r_max, kTileN);
   sp.total = (int64_t)sp.units * sp.w_unit;
   int n = ctas_override > 0 ? ctas_override : num_sms() / sp.cta_group;
-  // at least ~16 tiles per worker: small batches (bs 1) then leave SMs free
-  // for the acceptance branch running concurrently (verify.TreeVerifier.step)
-  // at no cost -- their time is set by the per-unit pipeline latency
-  // >= ~16 tiles per worker (small batches then leave SMs to the acceptance
-  // branch) but never fewer workers than units: a unit costs ~6 us of
-  // prologue / pipeline fill / epilogue, so units must not serialise
+  // >= ~9 tiles per worker (small batches then leave SMs to the acceptance
+  // branch running concurrently, verify.TreeVerifier.step) but never fewer
+  // workers than units: a unit costs ~6 us of prologue / pipeline fill /
+  // epilogue, so units must not serialise
   n = (int)std::max<int64_t>(
-      1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : std::max<int64_t>(sp.units, sp.total / 16)));
+      1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : std::max<int64_t>(sp.units, sp.total / 9)));
+  // several workers per unit: equal pieces (a multiple of the unit count)
+  // so no worker straddles two units (two prologues + epilogues) -- C2, 8
+  // units: 56 workers 33.0 us vs 52: 39.8 us; ~9 tiles per worker leaves
+  // a third of the SMs to the concurrent acceptance branch at bs 1
+  if (ctas_override <= 0 && n > sp.units && (n % sp.units) * 8 <= n) n -= n % sp.units;
   // a multiple of the row blocks per KV head keeps those blocks in step on
   // workers n / m_blocks apart (L2 serves the second read of each K/V tile);
   // a misaligned count reads K/V twice (C3, 63 pairs: +7 %)

@@ -315,26 +315,58 @@ __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params 
   }
   // pieces: worker k-1 (its first item iff its segment starts at the unit
   // start, else its last item), then the first item of every later worker
-  // whose segment starts inside u
+  // whose segment starts inside u.  Everything is fetched warp-parallel:
+  // the segment scan by ballot (seg is monotone), the piece LSEs one per
+  // lane, the partial rows four loads in flight -- a serial walk costs one
+  // dependent L2 round trip per piece (C2: 7 pieces per unit).
   const int first_slot = (k - 1) * 2 + (sp.seg[k - 1] == ustart ? 0 : 1);
   int kk_end = k;
-  while (kk_end < sp.n_workers && sp.seg[kk_end] < uend) ++kk_end;
-  float mx = sp.part_lse[(int64_t)first_slot * sp.rows_unit + local];
-  for (int kk = k; kk < kk_end; ++kk) mx = fmaxf(mx, sp.part_lse[(int64_t)(kk * 2) * sp.rows_unit + local]);
+  for (int base = k;; base += 32) {
+    const int kk = base + lane;
+    const bool inside = kk < sp.n_workers && sp.seg[kk] < uend;
+    const unsigned out = ~__ballot_sync(0xffffffffu, inside);
+    const int lead = out ? __ffs(out) - 1 : 32;
+    kk_end = base + lead;
+    if (lead < 32) break;
+  }
+  const int np = 1 + kk_end - k;  // piece j: slot first_slot (j = 0) or (k - 1 + j) * 2
+  auto slot_of = [&](int j) { return j == 0 ? first_slot : (k - 1 + j) * 2; };
+  float mx = -INFINITY;
+  for (int c0 = 0; c0 < np; c0 += 32) {
+    const int j = c0 + lane;
+    float l = j < np ? sp.part_lse[(int64_t)slot_of(j) * sp.rows_unit + local] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l = fmaxf(l, __shfl_xor_sync(0xffffffffu, l, o));
+    mx = fmaxf(mx, l);
+  }
   float wsum = 0.f;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int kk = k - 1; kk < kk_end; ++kk) {
-    const int sl = kk == k - 1 ? first_slot : kk * 2;
-    const float l = sp.part_lse[(int64_t)sl * sp.rows_unit + local];
-    if (l == -INFINITY) continue;
-    const float w = __expf(l - mx);
-    wsum += w;
-    const float4 o =
-        *reinterpret_cast<const float4 *>(sp.part_out + ((int64_t)sl * sp.rows_unit + local) * kHeadDim + lane * 4);
-    acc[0] = fmaf(w, o.x, acc[0]);
-    acc[1] = fmaf(w, o.y, acc[1]);
-    acc[2] = fmaf(w, o.z, acc[2]);
-    acc[3] = fmaf(w, o.w, acc[3]);
+  for (int c0 = 0; c0 < np; c0 += 32) {
+    const int j = c0 + lane;
+    const float l = j < np ? sp.part_lse[(int64_t)slot_of(j) * sp.rows_unit + local] : -INFINITY;
+    const float wl = l == -INFINITY ? 0.f : __expf(l - mx);
+    const int m = min(32, np - c0);
+    for (int t = 0; t < m; t += 4) {
+      float wt[4];
+      float4 o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        wt[u] = __shfl_sync(0xffffffffu, wl, (t + u) & 31);
+        o[u] = (t + u < m && wt[u] != 0.f)
+                   ? *reinterpret_cast<const float4 *>(
+                         sp.part_out + ((int64_t)slot_of(c0 + t + u) * sp.rows_unit + local) * kHeadDim + lane * 4)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (t + u >= m || wt[u] == 0.f) continue;
+        wsum += wt[u];
+        acc[0] = fmaf(wt[u], o[u].x, acc[0]);
+        acc[1] = fmaf(wt[u], o[u].y, acc[1]);
+        acc[2] = fmaf(wt[u], o[u].z, acc[2]);
+        acc[3] = fmaf(wt[u], o[u].w, acc[3]);
+      }
+    }
   }
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
   uint2 v;

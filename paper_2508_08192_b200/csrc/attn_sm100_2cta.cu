@@ -32,9 +32,19 @@ __device__ unsigned long long g_trace[16][256];
   do {                                                                                  \
     if (worker == 0 && (it) < 256) g_trace[ev][it] = clock64();                         \
   } while (0)
+// [event][worker] globaltimer stamps of every worker
+#define TRACE_G(ev)                                                                     \
+  do {                                                                                  \
+    unsigned long long t_;                                                              \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+    if (worker < 256) g_trace[ev][worker] = t_;                                         \
+  } while (0)
 #else
 #define TRACE(ev, it) \
   do {                \
+  } while (0)
+#define TRACE_G(ev) \
+  do {              \
   } while (0)
 #endif
 constexpr int kHalfBytes = kTileBytes / 2;    // 16 KB: K half [64 keys][128 d] or V half [128 keys][64 d]
@@ -273,6 +283,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const uint32_t rank = cta_rank();
   const int worker = blockIdx.x >> 1;
   griddep_launch_dependents();  // the fix-up grid may become resident (it waits for our completion)
+  if (threadIdx.x == 0 && rank == 0) TRACE(8, 0);
+  if (threadIdx.x == 0 && rank == 0) TRACE_G(13);
 
   if (threadIdx.x == 0) {
     if (rank == 0) {
@@ -306,6 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   cluster_sync();  // barriers of both CTAs initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  if (threadIdx.x == 0 && rank == 0) TRACE(9, 0);
 
   if (warp == 0 || warp == 2) {
     // ============ TMA producers (both CTAs): warp 0 Q + K ring, warp 2 V ring ============
@@ -712,12 +725,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         else
           mbar_arrive_leader(&sm.o_free);
       }
+      if (tr && wg == 0) TRACE(10, g_item);
       g_item += N;
     }
   }
+  if (threadIdx.x == 0 && rank == 0) TRACE(11, 0);
   tc_fence_before();
   __syncwarp();
   cluster_sync();  // the pair's MMAs, remote arrivals and TMEM reads are all done
+  if (threadIdx.x == 0 && rank == 0) TRACE(12, 0);
+  if (threadIdx.x == 0 && rank == 0) TRACE_G(14);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));

@@ -51,3 +51,19 @@ print("period mma: median", np.median(np.diff(b[1, 8:min(n, 200)])))
 print("softmax: S ready -> max pass done: median", np.median(b[6, it] - b[4, it]))
 print("softmax: max done -> chain ok: median", np.median(b[7, it] - b[6, it]))
 print("softmax: chain ok -> P arrived: median", np.median(b[5, it] - b[7, it]))
+# kernel-level phases of worker 0 (clock64 of its SM)
+e8 = int(buf[8, 0])
+if e8:
+    rel = lambda v: int(v) - e8
+    print("entry -> setup done (barriers, TMEM alloc, cluster sync):", rel(buf[9, 0]))
+    print("entry -> first S ready:", rel(buf[4, 0]) if buf[4, 0] else None)
+    ends = [(i, rel(buf[10, i])) for i in range(256) if buf[10, i]]
+    print("unit epilogues done (item index, cycles from entry):", ends[:8])
+    print("entry -> softmax loop exit (thread 0):", rel(buf[11, 0]), " -> final cluster sync:", rel(buf[12, 0]))
+# every worker (globaltimer ns): start / end spread
+st = buf[13][buf[13] > 0].astype(np.int64)
+en = buf[14][buf[14] > 0].astype(np.int64)
+if len(st):
+    t0 = st.min()
+    print("workers", len(st), "start spread ns", int(st.max() - t0), "end: min", int(en.min() - t0), "median",
+          int(np.median(en) - t0), "max", int(en.max() - t0))

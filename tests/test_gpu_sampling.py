@@ -123,6 +123,36 @@ def test_accept_stochastic_full_vocab_vs_oracle(top_p, lazy, walk_cl, monkeypatc
         assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used, b
 
 
+@pytest.mark.parametrize("lazy", [True, False])
+def test_accept_stochastic_wide_tree_vs_oracle(lazy):
+    """A 599-wide root (603 rows): the walk gathers a node's children a
+    512-row window at a time, so the decisions cross a window boundary.  The
+    first 550 root children carry a token outside the top-p nucleus (p = 0:
+    always rejected, the residual keeps shrinking by q), the rest are drawn
+    from the draft q; three children hang below draft node 0."""
+    from paper_2508_08192_b200.sampling import StochasticAcceptor
+
+    B, V, T, top_p = 2, 512, 1.0, 0.5
+    tree = [-1] * 599 + [0] * 3
+    aug, tl, dl, tokens, seeds, steps = _stochastic_case(B, V, tree, T, top_p, seed=31)
+    R = len(aug)
+    for b in range(B):
+        tokens[b, 1:551] = int(np.argmin(tl[b, 0]))  # lowest target logit: outside the nucleus
+    par = torch.tensor([aug] * B, dtype=torch.int32, device="cuda")
+    res = StochasticAcceptor(lazy=lazy)(torch.tensor(tl, device="cuda"), torch.tensor(dl, device="cuda"), T, top_p,
+                                        par, torch.full((B,), R, dtype=torch.int32, device="cuda"),
+                                        torch.tensor(tokens, device="cuda"), seeds=_i64(seeds), steps=_i64(steps))
+    torch.cuda.synchronize()
+    assert int(res.err[0]) == 0
+    for b in range(B):
+        uni = O.rank_sliced_uniforms(seeds[b], steps[b], 1, R)[0]
+        path, nxt, _res, used = _oracle_accept(aug, tl[b], dl[b], tokens[b], uni, T, top_p)
+        assert used > 551, used  # the decisions did cross the first window
+        plen = int(res.path_len[b])
+        assert res.path[b, :plen].cpu().tolist() == list(path), b
+        assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used, b
+
+
 # ---------------------------------------------------------------------------
 # vocab-sharded stochastic acceptance (SURVEY 8(e)): every rank's kernels run
 # in this process (VirtualComm); the protocol is the one torch.distributed runs

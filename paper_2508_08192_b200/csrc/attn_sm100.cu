@@ -288,16 +288,18 @@ __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params 
   // early, released when every attention CTA has finished and flushed
   griddep_wait();
   const TreeAttnParams &p = sp.p;
-  const int k = blockIdx.x + 1;
+  // blockIdx.x: a split unit from the host's list (its first interior
+  // boundary k), or every boundary when the list overflowed
+  const int k = sp.n_split >= 0 ? sp.split_k[blockIdx.x] : blockIdx.x + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int local = blockIdx.y * 4 + warp;
   if (local >= sp.rows_unit) return;
-  const int64_t ck = sp.seg[k];
+  const int64_t ck = seg_begin(sp, k);  // (arithmetic: the same values the main kernel wrote to sp.seg)
   const int W = sp.w_unit;
   const int unit = (int)(ck / W);
   const int64_t ustart = (int64_t)unit * W, uend = ustart + W;
-  if (ck == ustart) return;              // boundary between units: nothing split here
-  if (sp.seg[k - 1] > ustart) return;    // an earlier boundary inside u merges it
+  if (ck == ustart) return;                  // boundary between units: nothing split here
+  if (seg_begin(sp, k - 1) > ustart) return;  // an earlier boundary inside u merges it
   const int g = p.hq / p.hkv;
   const int bh = p.batch * p.hkv;
   const int b = (unit % bh) / p.hkv, kvh = unit % p.hkv;
@@ -319,11 +321,11 @@ __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params 
   // the segment scan by ballot (seg is monotone), the piece LSEs one per
   // lane, the partial rows four loads in flight -- a serial walk costs one
   // dependent L2 round trip per piece (C2: 7 pieces per unit).
-  const int first_slot = (k - 1) * 2 + (sp.seg[k - 1] == ustart ? 0 : 1);
+  const int first_slot = (k - 1) * 2 + (seg_begin(sp, k - 1) == ustart ? 0 : 1);
   int kk_end = k;
   for (int base = k;; base += 32) {
     const int kk = base + lane;
-    const bool inside = kk < sp.n_workers && sp.seg[kk] < uend;
+    const bool inside = kk < sp.n_workers && seg_begin(sp, kk) < uend;
     const unsigned out = ~__ballot_sync(0xffffffffu, inside);
     const int lead = out ? __ffs(out) - 1 : 32;
     kk_end = base + lead;
@@ -453,8 +455,13 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   // branch running concurrently, verify.TreeVerifier.step) but never fewer
   // workers than units: a unit costs ~6 us of prologue / pipeline fill /
   // epilogue, so units must not serialise
+  static int tpw = -1;
+  if (tpw < 0) {
+    const char *e = getenv("SDB_ATTN_TPW");  // testing knob: target tiles per worker
+    tpw = e ? std::max(1, atoi(e)) : 9;
+  }
   n = (int)std::max<int64_t>(
-      1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : std::max<int64_t>(sp.units, sp.total / 9)));
+      1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : std::max<int64_t>(sp.units, sp.total / tpw)));
   // several workers per unit: equal pieces (a multiple of the unit count)
   // so no worker straddles two units (two prologues + epilogues) -- C2, 8
   // units: 56 workers 33.0 us vs 52: 39.8 us; ~9 tiles per worker leaves
@@ -564,9 +571,18 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *wor
 #undef SDB_LAUNCH_TC
     SDB_CHECK_LAUNCH();
   }
-  if (sp.n_workers > 1) {
+  // split units (a worker boundary strictly inside): one fix-up block row
+  // each; no launch at all when every unit is whole
+  sp.n_split = 0;
+  for (int k = 1; k < sp.n_workers && sp.n_split >= 0; ++k) {
+    const int64_t ck = seg_begin(sp, k), ustart = ck / sp.w_unit * sp.w_unit;
+    if (ck == ustart || seg_begin(sp, k - 1) > ustart) continue;
+    if (sp.n_split == kMaxSplit) sp.n_split = -1;
+    else sp.split_k[sp.n_split++] = k;
+  }
+  if (sp.n_workers > 1 && sp.n_split != 0) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(sp.n_workers - 1, cdiv(sp.rows_unit, 4));
+    cfg.gridDim = dim3(sp.n_split > 0 ? sp.n_split : sp.n_workers - 1, cdiv(sp.rows_unit, 4));
     cfg.blockDim = dim3(128);
     cfg.stream = stream;
     cudaLaunchAttribute attr;

@@ -268,6 +268,8 @@ __host__ __device__ constexpr uint32_t make_idesc(bool b_mn_major) {
          | ((uint32_t)(kTileN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
 }
 
+constexpr int kMaxSplit = 192;  // split units listed for the fix-up grid
+
 struct Sm100Params {
   TreeAttnParams p;
   int cta_group;   // 1: one CTA per unit (M = 128 MMAs); 2: CTA pair (M = 256, cta_group::2)
@@ -282,6 +284,8 @@ struct Sm100Params {
   float *part_out; // [n_workers * 2][rows_unit][128] partial outputs of split units
   float *part_lse; // [n_workers * 2][rows_unit]
   int64_t *seg;    // [n_workers + 1] segment starts, written by the main kernel for the fix-up
+  int n_split;     // split units to merge (-1: more than kMaxSplit, the fix-up scans every boundary)
+  int split_k[kMaxSplit];  // per split unit: its first interior worker boundary k
 };
 
 __host__ __device__ __forceinline__ int64_t seg_begin(const Sm100Params &sp, int k) {

@@ -558,6 +558,25 @@ def test_tcgen05_small_batch_stream_k(ctas):
     assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
 
 
+def test_tcgen05_fixup_more_split_units_than_listed():
+    """250 CTA-pair workers over 256 units (B 16, 64q/8kv: two 256-row blocks
+    per KV head): ~250 split units, more than the host list holds, so the
+    fix-up falls back to one block row per worker boundary."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    c = _rand_paged_case(16, 64, 8, 128, 512, 64, TREE64, seed=5, ragged=True)
+    out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                     c["nr"], 128 ** -0.5, num_splits=250, kernel=1)
+    torch.cuda.synchronize()
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(c["q"]), f64(c["kp"]), f64(c["vp"]), c["table_np"],
+                                                   c["ctx_np"], f64(c["tk"]), f64(c["tv"]), [c["aug"]] * 16,
+                                                   128 ** -0.5)
+    err = np.abs(out.float().cpu().numpy() - want_o)
+    assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+    assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
+
+
 @pytest.mark.parametrize("group", ["1", "2"])
 def test_tcgen05_single_cta_and_pair_kernels_agree(group, monkeypatch):
     """Force the 1-CTA (M=128) or the CTA-pair (cta_group::2, M=256) kernel on

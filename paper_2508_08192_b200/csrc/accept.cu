@@ -1550,10 +1550,14 @@ constexpr int kWalkSmem = sdb::kWCap * (int)sizeof(float2);
 
 template <int CL, bool M, bool L>
 static int walk_max_clusters_of() {
-  static int cached = -1;
-  if (cached < 0) {
-    cudaFuncSetAttribute(sdb::stochastic_walk_kernel<CL, M, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kWalkSmem);
+  // the smem opt-in is per device: set on every call (cheap); the occupancy
+  // query is cached per device
+  cudaFuncSetAttribute(sdb::stochastic_walk_kernel<CL, M, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWalkSmem);
+  static int cached_per_dev[64] = {0};  // 0: not queried yet (stored + 1)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int &cached = cached_per_dev[dev & 63];
+  if (cached == 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL * 1024);
     cfg.blockDim = dim3(sdb::kWThreads);
@@ -1570,9 +1574,9 @@ static int walk_max_clusters_of() {
       cudaGetLastError();
       n = sdb::num_sms() / CL;
     }
-    cached = n;
+    cached = n + 1;
   }
-  return cached;
+  return cached - 1;
 }
 
 template <int CL>

@@ -613,10 +613,18 @@ def main():
     else:
         t_attn_ms = parts["tree_attn"]
         achieved_tf = attn_flops / (t_attn_ms * 1e-3) / 1e12
-        roof = {"kernel": "tree_attn", "bound": "tensor", "achieved": achieved_tf, "peak": tc_peak,
-                "unit": "TFLOP/s", "frac": achieved_tf / tc_peak, "traffic": traffic, "peak_source": peak_src,
-                "flops_per_launch": attn_flops, "hbm_gbs": attn_bytes / (t_attn_ms * 1e-3) / 1e9,
-                "accept_hbm_gbs": accept_gbs, "accept_hbm_frac": accept_gbs / hbm_peak}
+        attn_gbs = attn_bytes / (t_attn_ms * 1e-3) / 1e9
+        # the binding bound of the attention: tensor at C3/C4, HBM at bs 1 (C2)
+        if attn_bytes / (hbm_peak * 1e9) > attn_flops / (tc_peak * 1e12):
+            roof = {"kernel": "tree_attn", "bound": "hbm", "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": attn_gbs / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                    "bytes_per_launch": attn_bytes, "tflops": achieved_tf,
+                    "accept_hbm_gbs": accept_gbs, "accept_hbm_frac": accept_gbs / hbm_peak}
+        else:
+            roof = {"kernel": "tree_attn", "bound": "tensor", "achieved": achieved_tf, "peak": tc_peak,
+                    "unit": "TFLOP/s", "frac": achieved_tf / tc_peak, "traffic": traffic, "peak_source": peak_src,
+                    "flops_per_launch": attn_flops, "hbm_gbs": attn_gbs,
+                    "accept_hbm_gbs": accept_gbs, "accept_hbm_frac": accept_gbs / hbm_peak}
     # step-level roofline: the attention's binding bound (tensor at C3/C4)
     # plus the acceptance's HBM bound, executed back to back
     t_attn_star = 0.0 if accept_only else max(attn_flops / (tc_peak * 1e12), attn_bytes / (hbm_peak * 1e9))

@@ -182,7 +182,7 @@ class TreeVerifier:
         """SMs to leave to a greedy acceptance running beside a full-occupancy
         attention: k such that the scan on k SMs (~80 GB/s each, measured)
         takes as long as the attention on n_sms - k (~1.1 PFLOP/s on all
-        SMs, measured).  C3: k ~= 22 (step 690 -> 635 us).  Stochastic
+        SMs, measured).  C3: k = 20 (64 CTA pairs; step 690 -> ~640 us).  Stochastic
         acceptance is instruction-bound on every SM: no reserve."""
         import torch
 
@@ -191,7 +191,10 @@ class TreeVerifier:
         hq, d = x.q.shape[2], x.q.shape[3]
         ctx = self.max_ctx if self.max_ctx else x.block_table.shape[1] * x.k_pool.shape[2]
         t_att = 4.0 * d * hq * b * r * ctx / 1.1e15
-        acc_sm_s = b * r * x.logits.shape[2] * 4 / 80.0e9  # scan time on one SM
+        # scan time on one SM: 90 GB/s per SM (the C3 step measures best at
+        # 64 pairs / 20 SMs left, 629-649 us, vs 641-665 at 62 / 22 on the
+        # same boxes; the 80 GB/s measured alone under-states the rate)
+        acc_sm_s = b * r * x.logits.shape[2] * 4 / 90.0e9
         # acc_sm_s / k = t_att * n / (n - k)  ->  k = acc_sm_s * n / (t_att * n + acc_sm_s)
         k = acc_sm_s * n_sms / (t_att * n_sms + acc_sm_s)
         k = int(round(k))

@@ -123,6 +123,29 @@ def test_accept_stochastic_full_vocab_vs_oracle(top_p, lazy, walk_cl, monkeypatc
         assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used, b
 
 
+@pytest.mark.parametrize("top_p,lazy", [(0.9, True), (0.9, False), (1.0, True)])
+def test_accept_stochastic_odd_vocab_vs_oracle(top_p, lazy):
+    """V = 4099 (rows not 16-byte aligned): the scalar paths of the row
+    stats, the walk's nucleus compaction and the bonus pass."""
+    from paper_2508_08192_b200.sampling import StochasticAcceptor
+
+    B, V, T = 3, 4099, 0.9
+    aug, tl, dl, tokens, seeds, steps = _stochastic_case(B, V, TREE64, T, top_p, seed=41)
+    R = len(aug)
+    par = torch.tensor([aug] * B, dtype=torch.int32, device="cuda")
+    res = StochasticAcceptor(lazy=lazy)(torch.tensor(tl, device="cuda"), torch.tensor(dl, device="cuda"), T, top_p,
+                                        par, torch.full((B,), R, dtype=torch.int32, device="cuda"),
+                                        torch.tensor(tokens, device="cuda"), seeds=_i64(seeds), steps=_i64(steps))
+    torch.cuda.synchronize()
+    assert int(res.err[0]) == 0
+    for b in range(B):
+        uni = O.rank_sliced_uniforms(seeds[b], steps[b], 1, R)[0]
+        path, nxt, _res, used = _oracle_accept(aug, tl[b], dl[b], tokens[b], uni, T, top_p)
+        plen = int(res.path_len[b])
+        assert res.path[b, :plen].cpu().tolist() == list(path), b
+        assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used, b
+
+
 @pytest.mark.parametrize("lazy", [True, False])
 def test_accept_stochastic_wide_tree_vs_oracle(lazy):
     """A 599-wide root (603 rows): the walk gathers a node's children a

@@ -57,6 +57,14 @@ def _augment(parent):
     return [-1] + [0 if p == -1 else p + 1 for p in parent]
 
 
+def _ancestor_pairs(aug):
+    """Number of (row, key) pairs of the ancestor-or-self tree mask."""
+    depth = []
+    for p in aug:
+        depth.append(1 if p < 0 else depth[p] + 1)
+    return sum(depth)
+
+
 def _tree_levels(aug):
     depth = []
     for p in aug:
@@ -410,10 +418,8 @@ def main():
     _lib.load()
     shard = shard_for(rank, world, cfg["Hq"], cfg["Hkv"], cfg["V"])
     x, R = make_inputs(cfg, shard, dev, mode=mode)
-    from oracle import specdec_oracle as O  # checker only (mask popcount for the FLOP count)
-
     aug = tuple(_augment(TREE))
-    anc_pairs = int(O.suffix_mask(aug).sum())
+    anc_pairs = _ancestor_pairs(aug)  # visible (row, tree key) pairs: the suffix part of the FLOP count
     n_parent_rows = len(set(p for p in aug[1:]))
     temperature = 0.0 if mode == "greedy" else TEMPERATURE
     ver = TreeVerifier(scale=cfg["d"] ** -0.5, temperature=temperature, top_p=TOP_P if mode != "greedy" else 1.0,

@@ -462,11 +462,35 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   }
   n = (int)std::max<int64_t>(
       1, std::min<int64_t>(n, ctas_override > 0 ? sp.total : std::max<int64_t>(sp.units, sp.total / tpw)));
-  // several workers per unit: equal pieces (a multiple of the unit count)
-  // so no worker straddles two units (two prologues + epilogues) -- C2, 8
-  // units: 56 workers 33.0 us vs 52: 39.8 us; ~9 tiles per worker leaves
-  // a third of the SMs to the concurrent acceptance branch at bs 1
-  if (ctas_override <= 0 && n > sp.units && (n % sp.units) * 8 <= n) n -= n % sp.units;
+  // worker count by a cost model in tiles per worker: whole units per
+  // worker (no split, no fix-up), equal pieces of every unit (+ a merge), or
+  // pieces straddling unit boundaries (+ a second prologue / epilogue), each
+  // overhead ~11 tiles (calibrated on C3 per-GPU shards: G 8, 64 units: 64
+  // pairs 71.6 us vs 74: 86.6; G 4, 128 units: 137.4 vs 146.6; G 1, 512
+  // units: 533 vs 516; C2, 8 units: 56 workers 33.0 us vs 52: 39.8); the
+  // search stays within 3/4 of the SM-limited count (CTA-pair kernel)
+  static int cost_plan = -1;
+  if (cost_plan < 0) {
+    const char *e = getenv("SDB_ATTN_COST_PLAN");  // testing knob: 0 disables
+    cost_plan = e ? atoi(e) != 0 : 1;
+  }
+  if (ctas_override <= 0 && n > 1 && cost_plan && sp.cta_group == 2) {
+    constexpr int64_t kSplit = 11;
+    auto cost = [&](int m) -> int64_t {
+      if (sp.units % m == 0) return (int64_t)(sp.units / m) * sp.w_unit;
+      if (m % sp.units == 0) return sp.total / m + kSplit;
+      return (sp.total + m - 1) / m + 2 * kSplit;
+    };
+    int best = n;
+    for (int m = n - 1; m * 4 >= n * 3; --m)
+      if (cost(m) < cost(best)) best = m;
+    n = best;
+  } else if (ctas_override <= 0 && n > sp.units && (n % sp.units) * 8 <= n) {
+    // single-CTA kernel: equal pieces per unit when that costs <= 1/8 of the
+    // workers (its split overhead is small: whole-unit plans measured slower
+    // on the draft depth steps, 276 vs 215 us)
+    n -= n % sp.units;
+  }
   // a multiple of the row blocks per KV head keeps those blocks in step on
   // workers n / m_blocks apart (L2 serves the second read of each K/V tile);
   // a misaligned count reads K/V twice (C3, 63 pairs: +7 %)

@@ -214,13 +214,19 @@ __global__ void __launch_bounds__(kArgmaxThreads) argmax_keys_masked_kernel(
 
 // One warp per sequence: the argmax walk in the augmented frame (row 0 =
 // root; children of row r = rows j > r with parent[j] == r, index order).
+constexpr int kWalkStage = 256;  // tree rows staged in shared memory per sequence (12 KB per 4 warps)
+
 __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int32_t *__restrict__ parent,
                                    const int32_t *__restrict__ n_rows, const int32_t *__restrict__ tokens,
                                    int batch, int r_max, int32_t *__restrict__ path, int32_t *__restrict__ path_len,
                                    int64_t *__restrict__ next_token, int32_t *__restrict__ uniforms_used,
                                    int split) {
+  // small trees: the sequence's parents, tokens and per-row argmax are
+  // staged into shared memory with coalesced loads first, so the walk's
+  // level-by-level decisions cost no dependent global round trips
+  __shared__ int32_t s_par[4][kWalkStage], s_tok[4][kWalkStage], s_amax[4][kWalkStage];
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = (threadIdx.x >> 5) & 3;
   if (b >= batch) return;
   const int n = min(n_rows[b], r_max);
   const int32_t *par = parent + (int64_t)b * r_max;
@@ -231,14 +237,26 @@ __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int
     for (int s = 1; s < split; ++s) k = max(k, key[(int64_t)r * split + s]);
     return k;
   };
+  const bool staged = n <= kWalkStage;
+  if (staged) {
+    for (int r = lane; r < n; r += 32) {
+      s_par[wib][r] = par[r];
+      s_tok[wib][r] = tok[r];
+      s_amax[wib][r] = (int)key_index(row_key(r));
+    }
+    __syncwarp();
+  }
+  auto P = [&](int j) { return staged ? s_par[wib][j] : par[j]; };
+  auto T = [&](int j) { return staged ? s_tok[wib][j] : tok[j]; };
+  auto A = [&](int r) { return staged ? s_amax[wib][r] : (int)key_index(row_key(r)); };
   int cur = 0, used = 0, len = 0;
   while (true) {
-    const int want = (int)key_index(row_key(cur));
+    const int want = A(cur);
     int accepted = -1, examined = 0;
     for (int j0 = cur + 1; j0 < n; j0 += 32) {
       const int j = j0 + lane;
-      const bool child = j < n && par[j] == cur;
-      const bool hit = child && tok[j] == want;
+      const bool child = j < n && P(j) == cur;
+      const bool hit = child && T(j) == want;
       const unsigned cm = __ballot_sync(SDB_FULL_MASK, child);
       const unsigned hm = __ballot_sync(SDB_FULL_MASK, hit);
       if (hm) {
@@ -257,7 +275,7 @@ __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int
   }
   if (lane == 0) {
     path_len[b] = len;
-    next_token[b] = (int64_t)key_index(row_key(cur));
+    next_token[b] = (int64_t)A(cur);
     uniforms_used[b] = used + 1;
   }
 }

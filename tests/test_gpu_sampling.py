@@ -146,6 +146,36 @@ def test_accept_stochastic_odd_vocab_vs_oracle(top_p, lazy):
         assert int(res.next_token[b]) == nxt and int(res.uniforms_used[b]) == used, b
 
 
+def test_lazy_walk_repeatable_at_full_occupancy():
+    """64 sequences (8-CTA clusters in two waves, the validation scan on a
+    second stream): 25 repeated calls give identical results (the cluster
+    CTAs share the lazy state; a race shows up as a mismatch or a fault)."""
+    from paper_2508_08192_b200.sampling import StochasticAcceptor, tree_levels
+
+    B, V = 64, 32768
+    g = torch.Generator(device="cuda").manual_seed(5)
+    aug = O.augment(tuple(TREE64))
+    R = len(aug)
+    tl = torch.randn((B, R, V), generator=g, device="cuda") * 2.0
+    dl = tl + 0.5 * torch.randn((B, R, V), generator=g, device="cuda")
+    tok = torch.randint(0, V, (B, R), generator=g, device="cuda", dtype=torch.int32)
+    par = torch.tensor([aug] * B, dtype=torch.int32, device="cuda")
+    nr = torch.full((B,), R, dtype=torch.int32, device="cuda")
+    seeds = torch.arange(B, dtype=torch.int64, device="cuda") + 77
+    steps = torch.full((B,), 6, dtype=torch.int64, device="cuda")
+    acc = StochasticAcceptor(lazy=True, levels=tree_levels(par))
+
+    def run():
+        r = acc(tl, dl, 1.0, 0.9, par, nr, tok, seeds=seeds, steps=steps)
+        return [t.clone() for t in (r.path, r.path_len, r.next_token, r.uniforms_used, r.err)]
+
+    ref = run()
+    for _ in range(25):
+        got = run()
+        assert all(torch.equal(a, b) for a, b in zip(ref, got))
+    assert int(ref[4][0]) == 0
+
+
 @pytest.mark.parametrize("lazy", [True, False])
 def test_accept_stochastic_wide_tree_vs_oracle(lazy):
     """A 599-wide root (603 rows): the walk gathers a node's children a

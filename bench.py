@@ -260,6 +260,55 @@ def cpu_sample(cfg, seed=0, mode="greedy"):
     return ta, tacc, B * Hkv, B
 
 
+def parity_sample(cfg, x, out, lse, acc, mode, aug):
+    """Check one sampled sequence of the measured run against the CPU oracle
+    (the cpu_baseline leg's restatement): accepted path / bonus token /
+    uniforms used, and out / LSE of one (sequence, KV head) slice in float64
+    (bf16 tolerances of tests/test_gpu_benched_configs.py)."""
+    import numpy as np
+
+    from oracle import specdec_oracle as O
+
+    b = cfg["B"] // 2
+    R = len(aug)
+    raw = tuple(p - 1 if p > 0 else -1 for p in aug[1:])
+    tokens = x.tokens[b].cpu().numpy()
+    if mode == "greedy":
+        want = O.greedy_walk(raw, tokens[1:], np.argmax(x.logits[b].cpu().numpy(), axis=-1))
+    else:
+        qmemo = {}
+
+        def qdist(c):
+            row = aug[1 + c]
+            if row not in qmemo:
+                qmemo[row] = O.target_dist(x.draft_logits[b, row].double().cpu().numpy(), TEMPERATURE, 1.0)
+            return qmemo[row]
+
+        uni = O.rank_sliced_uniforms(int(x.seeds[b]), int(x.steps[b]), 1, R)[0]
+        w = O.mss_verify(raw, tokens[1:], qdist,
+                         lambda i: O.target_dist(x.logits[b, i].double().cpu().numpy(), TEMPERATURE, TOP_P), uni)
+        want = (w[0], w[1], w[3])
+    plen = int(acc.path_len[b])
+    got = ([int(a) for a in acc.path[b, :plen].cpu()], int(acc.next_token[b]), int(acc.uniforms_used[b]))
+    res = {"sequence": b, "accept_exact": got == (list(want[0]), int(want[1]), int(want[2]))}
+    if out is not None:
+        g = cfg["Hq"] // cfg["Hkv"]
+        f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+        c = int(x.ctx_len[b])
+        n_pages = -(-c // x.k_pool.shape[2])
+        pages = x.block_table[b, :n_pages].long()
+        wo, wl = O.tree_verify_attention_batch(f64(x.q[b:b + 1, :, :g]), f64(x.k_pool[pages][:, :1]),
+                                               f64(x.v_pool[pages][:, :1]), np.arange(n_pages)[None],
+                                               np.array([c]), f64(x.tree_k[b:b + 1, :, :1]),
+                                               f64(x.tree_v[b:b + 1, :, :1]), [aug], cfg["d"] ** -0.5)
+        err_o = np.abs(out[b, :, :g].float().cpu().numpy() - wo[0])
+        err_l = float(np.abs(lse[b, :g].cpu().numpy() - wl[0]).max())
+        res.update(kv_head=0, out_max_abs=float(err_o.max()), out_mean_abs=float(err_o.mean()), lse_max_abs=err_l,
+                   attn_ok=bool(err_o.max() < 2e-2 and err_o.mean() < 2e-3 and err_l < 2e-3))
+    res["ok"] = bool(res["accept_exact"] and res.get("attn_ok", True))
+    return res
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -678,7 +727,13 @@ def main():
         "gpu_launches": n_launch * args.steps,
         "e2e": e2e,
     }
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the oracle leg: one sampled sequence of the measured outputs checked ...
+        parity = parity_sample(cfg, x, None if accept_only else o["out"], None if accept_only else o["lse"], acc,
+                               mode, aug)
+        line["parity"] = parity
+        # ... and the reference algorithm timed on a bounded sample
         cpu_sample(cfg, mode=mode)
         ta, tacc, fa, facc = cpu_sample(cfg, seed=1, mode=mode)
         us = (ta * fa + tacc * facc) * 1e6
@@ -688,6 +743,9 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        print(f"[bench] PARITY FAILURE vs the oracle: {parity}", file=sys.stderr)
+        sys.exit(1)
 
 
 if __name__ == "__main__":

@@ -46,6 +46,7 @@ extern "C" {
 #define SDB_ERR_ALL_MASKED 16     /* AttentionError: row masked in every part (attention.py:117) */
 #define SDB_ERR_NO_ALLOWED 32     /* SamplingError: no token allowed (sampling.py:96-97)       */
 #define SDB_ERR_CACHE 64          /* CacheError: block pool exhausted / tape or table overflow */
+#define SDB_ERR_PLAN 128          /* SamplingError: tree deeper / wider than the host-planned walk */
 
 #define SDB_DTYPE_BF16 0
 #define SDB_DTYPE_F32 1
@@ -344,23 +345,27 @@ int sdb_mss_verify_f64(const int32_t *parent, const int32_t *tokens, int n_nodes
  * (PagedKvCache.write / compact_accepted, kvstore.py:217-233).
  * tree_k/v: bf16 [n_layers][B][r_max][hkv][head_dim]; caches: per layer
  * pool, layer stride layer_stride elements.  n_keep int32 [B] may be NULL
- * (-> path_len + 1). */
+ * (-> path_len + 1).  A position past the sequence's mapped blocks (table
+ * entry < 0 or beyond max_blocks: the reference's CacheError "write past
+ * allocated blocks", kvstore.py:220-221) is not written and sets SDB_ERR_CACHE in
+ * err[0] (err may be NULL). */
 int sdb_compact_kv(const void *tree_k, const void *tree_v, void *k_cache, void *v_cache,
                    int64_t cache_layer_stride, const int32_t *block_table, int max_blocks,
                    const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
                    const int32_t *n_keep, int n_layers, int batch, int r_max, int hkv,
-                   int head_dim, int block_size, int elem_bytes, void *stream);
+                   int head_dim, int block_size, int elem_bytes, int32_t *err, void *stream);
 
 /* ---- bookkeeping either side of the step ----------
  * Draft-cache write-back (engine.py:524-531): rows path[:n_keep-1] of the
  * draft's carried suffix K/V suffix_k/v [n_layers][B][n_src][hkv][head_dim]
  * (realized draft nodes in node order, no root row) written at positions
- * ctx_len[b] + 1 .. (L; the alignment token already sits at L - 1). */
+ * ctx_len[b] + 1 .. (L; the alignment token already sits at L - 1).  Unmapped
+ * positions are skipped with SDB_ERR_CACHE, as in sdb_compact_kv. */
 int sdb_compact_draft_kv(const void *suffix_k, const void *suffix_v, void *k_cache, void *v_cache,
                          int64_t cache_layer_stride, const int32_t *block_table, int max_blocks,
                          const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
                          const int32_t *n_keep, int n_layers, int batch, int r_max, int n_src, int hkv,
-                         int head_dim, int block_size, int elem_bytes, void *stream);
+                         int head_dim, int block_size, int elem_bytes, int32_t *err, void *stream);
 
 /* Hidden tape append (engine.py:532-533 -> HiddenTape.append_rows,
  * kvstore.py:405-409): rows [0] + [1 + a for a in path[:n_keep-1]] of hidden

@@ -382,20 +382,36 @@ def mss_verify(parent, node_tokens, node_dists, target_dists, uniforms):
 
     parent: NON-augmented draft tree; node_dists[c] is the draft q that
     proposed node c; target_dists[0] is the root context, [1+i] node i's.
-    Returns (accepted_path, next_token, residual, uniforms_used)."""
-    if len(target_dists) != len(parent) + 1:
-        raise OracleError("need one target dist per node parent incl. root")
-    dists = [check_dist(d) for d in target_dists]
+    Returns (accepted_path, next_token, residual, uniforms_used).
+
+    Test-size shortcut: node_dists / target_dists may also be callables
+    (index -> dist), evaluated and checked only for the rows the walk reads
+    (the reference checks every row first; the walk itself is identical).
+    Used at the full Llama-3 vocabulary for batches of 64 sequences, where
+    the top-p sort of every row would take minutes."""
+    if callable(target_dists):
+        memo = {}
+
+        def tdist(i):
+            if i not in memo:
+                memo[i] = check_dist(target_dists(i))
+            return memo[i]
+    else:
+        if len(target_dists) != len(parent) + 1:
+            raise OracleError("need one target dist per node parent incl. root")
+        dists = [check_dist(d) for d in target_dists]
+        tdist = dists.__getitem__
+    qdist = node_dists if callable(node_dists) else node_dists.__getitem__
     used = 0
     cur = ROOT
-    p = dists[0]
+    p = tdist(0)
     anchor = p
     path = []
     while True:
         descended = False
         for c in children(parent, cur):
             t = node_tokens[c]
-            q = node_dists[c]
+            q = qdist(c)
             if used >= len(uniforms):
                 raise OracleError("uniform stream exhausted mid-walk")
             u = uniforms[used]
@@ -404,7 +420,7 @@ def mss_verify(parent, node_tokens, node_dists, target_dists, uniforms):
             accept = (pt > 0.0) if qt <= 0.0 else (u < min(1.0, pt / qt))
             if accept:
                 path.append(c)
-                p = dists[1 + c]
+                p = tdist(1 + c)
                 anchor = p
                 cur = c
                 descended = True

@@ -22,6 +22,7 @@ SDB_ERR_UNIFORMS = 8
 SDB_ERR_ALL_MASKED = 16
 SDB_ERR_NO_ALLOWED = 32
 SDB_ERR_CACHE = 64
+SDB_ERR_PLAN = 128
 
 ATTN_FLAG_PDL = 1
 
@@ -107,8 +108,8 @@ _SIGNATURES = {
     "sdb_philox_uniforms": (I32, [P, P, I32, I64, I32, P, P]),
     "sdb_target_dist_f64": (I32, [P, P, I64, I32, F64, F64, P, P, P]),
     "sdb_mss_verify_f64": (I32, [P, P, I32, I32, P, P, P, I32, P, P, P, P, P]),
-    "sdb_compact_kv": (I32, [P, P, P, P, I64, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, P]),
-    "sdb_compact_draft_kv": (I32, [P, P, P, P, I64, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, P]),
+    "sdb_compact_kv": (I32, [P, P, P, P, I64, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, P, P]),
+    "sdb_compact_draft_kv": (I32, [P, P, P, P, I64, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, P, P]),
     "sdb_tape_append": (I32, [P, P, I64, P, P, P, P, I32, I32, I32, P, P]),
     "sdb_paged_alloc": (I32, [P, I32, P, P, I32, I32, P, P, P, P]),
     "sdb_paged_rewind": (I32, [P, I32, P, P, I32, I32, P, P, P]),

@@ -75,13 +75,22 @@ def _join_heads(x):
     return np.ascontiguousarray(x.transpose(1, 0, 2)).reshape(rows, heads * dh)
 
 
+def _bias_kind(bias):
+    """Bias class by name, so the reference's own CausalPrefix / LocalChunk /
+    TreeSuffix objects (attention.py:24-47) work when this module replaces
+    the reference's ``attend`` in place (shim.install_reference)."""
+    kind = type(bias).__name__
+    return kind if kind in ("CausalPrefix", "LocalChunk", "TreeSuffix") else None
+
+
 def _bias_mask(bias, n_q, n_k):
     """Visibility matrix for a bias object (attention.py:76-90)."""
-    if isinstance(bias, CausalPrefix):
+    kind = _bias_kind(bias)
+    if kind == "CausalPrefix":
         if bias.context_len != n_k:
             raise AttentionError("CausalPrefix context_len must match key count")
         return None
-    if isinstance(bias, LocalChunk):
+    if kind == "LocalChunk":
         if bias.chunk_len < 1:
             raise AttentionError("LocalChunk chunk_len must be >= 1")
         qp = np.asarray(bias.q_positions)
@@ -90,7 +99,7 @@ def _bias_mask(bias, n_q, n_k):
             raise AttentionError("LocalChunk positions must match q/k lengths")
         same = qp[:, None] // bias.chunk_len == kp[None, :] // bias.chunk_len
         return same & (kp[None, :] <= qp[:, None])
-    if isinstance(bias, TreeSuffix):
+    if kind == "TreeSuffix":
         if bias.mask.shape != (n_q, n_k):
             raise AttentionError(f"TreeSuffix mask {bias.mask.shape} vs ({n_q}, {n_k})")
         return np.asarray(bias.mask, dtype=bool)

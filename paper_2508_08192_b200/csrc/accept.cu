@@ -1354,6 +1354,20 @@ __global__ void __launch_bounds__(kWThreads, 2) stochastic_walk_kernel(
   }
 }
 
+// lazy walk end: a sequence still walking after the planned levels had a
+// deeper tree than the host plan (TreeVerifier(tree_levels=) / a captured
+// graph): flag it instead of leaving stale outputs
+__global__ void lazy_walk_finish_kernel(const LazyWalk *__restrict__ lw, int batch, int32_t *__restrict__ path_len,
+                                        int64_t *__restrict__ next_token, int32_t *__restrict__ uniforms_used,
+                                        int32_t *__restrict__ err) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch || lw[b].done) return;
+  path_len[b] = 0;
+  next_token[b] = -1;
+  uniforms_used[b] = 0;
+  atomicOr(err, SDB_ERR_PLAN);
+}
+
 // lazy walk start: every sequence at its root row
 __global__ void lazy_walk_init_kernel(const int32_t *__restrict__ n_rows, int batch, LazyWalk *__restrict__ lw,
                                       int32_t *__restrict__ cur_rows) {
@@ -1706,6 +1720,9 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
     if (le != cudaSuccess) return sdb::record_cuda_error(le);
     SDB_CHECK_LAUNCH();
   }
+  sdb::lazy_walk_finish_kernel<<<(batch + 127) / 128, 128, 0, s>>>(lw, batch, path_len, next_token, uniforms_used,
+                                                                   err);
+  SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
 

@@ -504,7 +504,11 @@ __global__ void __launch_bounds__(kShThreads) sh_walk_kernel(ShParams p) {
         const double u = uni[used++];
         const int64_t jdx = (int64_t)b * p.r_max + j;
         const double P = p.pq[jdx * 2], Q = p.pq[jdx * 2 + 1];
-        const double2 cm = p.s.chain[((int64_t)b * p.r_max + cur) * (p.levels + 1) + min(k, p.levels)];
+        if (k > p.levels) {  // more siblings than the planned chain (max_children): no clamped guess
+          failed = 3;
+          break;
+        }
+        const double2 cm = p.s.chain[((int64_t)b * p.r_max + cur) * (p.levels + 1) + k];
         const double pt = fmax(P - cm.x * Q, 0.0) / cm.y;
         const bool acc = Q <= 0.0 ? pt > 0.0 : u < fmin(1.0, pt / Q);
         if (acc) {
@@ -519,6 +523,7 @@ __global__ void __launch_bounds__(kShThreads) sh_walk_kernel(ShParams p) {
       if (failed || !descended) break;
     }
     if (!failed && used >= p.n_uniforms) failed = 1;
+    if (!failed && k > p.levels) failed = 3;
     ShWalk w;
     const double2 cm = p.s.chain[((int64_t)b * p.r_max + cur) * (p.levels + 1) + min(k, p.levels)];
     w.c = cm.x;
@@ -531,7 +536,7 @@ __global__ void __launch_bounds__(kShThreads) sh_walk_kernel(ShParams p) {
     w.used = failed ? used : used + 1;
     s_w = w;
     p.s.walk[b] = w;
-    if (failed) atomicOr(p.err, SDB_ERR_UNIFORMS);
+    if (failed) atomicOr(p.err, failed == 3 ? SDB_ERR_PLAN : SDB_ERR_UNIFORMS);
   }
   __syncthreads();
   const ShWalk w = s_w;
@@ -629,8 +634,8 @@ __global__ void __launch_bounds__(kShThreads) sh_pick_kernel(ShParams p) {
   }
   if (threadIdx.x == 0) {
     p.bonus_token[b] = tok;
-    p.path_len[b] = w.failed == 2 ? 0 : w.len;
-    p.uniforms_used[b] = w.failed == 2 ? 0 : w.used;
+    p.path_len[b] = w.failed >= 2 ? 0 : w.len;
+    p.uniforms_used[b] = w.failed >= 2 ? 0 : w.used;
   }
 }
 

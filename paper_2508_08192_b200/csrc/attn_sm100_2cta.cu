@@ -150,14 +150,40 @@ struct alignas(1024) Smem2 {
   float mref[3][128];  // running reference max after each item (log2 units), by slot
   float lsum[3][128];  // per-warpgroup partial row sums at the end of a unit
   float msum[3][128];  // ... and the reference max they are relative to
+  uint32_t bad[128];   // fixed reference exceeded in this row of the unit (exact recompute)
   alignas(128) float lg[kLgStages][kLgChunk];  // fused greedy scan: logits chunk ring (warp 3; 16-B aligned for TMA)
   uint64_t lg_full[kLgStages];
 };
 
 constexpr int kSoftmaxWG = 3;                       // softmax warpgroups (one per S slot)
+// register split (65536 per SM, one CTA per SM): the TMA / MMA / scan
+// warpgroup keeps 56 per thread, the softmax warpgroups get 152
+// measured (C3, attention alone): no reallocation 525 us; 56 / 152 536 us
+// (and an intermittent hang); 32 / 160 569 us (the control warps spill) --
+// the 128-register budget with its few softmax spills is the fastest
+#ifndef SDB_REGS_CTL
+#define SDB_REGS_CTL 0
+#endif
+#ifndef SDB_REGS_SOFTMAX
+#define SDB_REGS_SOFTMAX 152
+#endif
+constexpr int kRegsCtl = SDB_REGS_CTL;  // 0: no register reallocation
+constexpr int kRegsSoftmax = SDB_REGS_SOFTMAX;
+static_assert(kRegsCtl == 0 || kRegsCtl * 128 + kRegsSoftmax * 128 * kSoftmaxWG <= 65536, "register file");
 constexpr int kPairThreads = 128 + kSoftmaxWG * 128;
 constexpr int kSBase = 128;                          // TMEM: O [0,128), S slot s at 128 + 128 s
 constexpr int kBarUnit = 1 + 4 * kSoftmaxWG;         // named barrier: unit end, all softmax warps
+#ifndef SDB_ATTN_FIXREF
+#define SDB_ATTN_FIXREF 1
+#endif
+// Fixed reference max: after the first item of a unit piece, P = exp2(s -
+// m_ref) against that item's row max, with no max pass and no max hand-off
+// (P, O and the row sum are all relative to one reference, so nothing is
+// ever rescaled).  fp32 / bf16 hold 2^127, so exactness only needs the scores
+// to stay below m_ref + kOverflowLog2; a row that exceeds it (a score ~67
+// nats above every score of the piece's first tile) is recomputed exactly.
+constexpr bool kFixRef = SDB_ATTN_FIXREF != 0;
+constexpr float kOverflowLog2 = 96.f;
 
 // 32 S values of one row (fp32 bits in r[0..31]) -> P = exp2(s * sl2 - m),
 // packed bf16 into r[0..15]; returns the sum of the 32 probabilities.
@@ -273,7 +299,7 @@ template <int EMU8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     tree_attn_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_tk,
-                                  const __grid_constant__ CUtensorMap tm_tv, const Sm100Params sp) {
+                                  const __grid_constant__ CUtensorMap tm_tv, const __grid_constant__ Sm100Params sp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem2 &sm = *reinterpret_cast<Smem2 *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const TreeAttnParams &p = sp.p;
@@ -310,6 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     for (int s = 0; s < kLgStages; ++s) mbar_init(&sm.lg_full[s], 1);
     fence_barrier_init();
   }
+  if (threadIdx.x < 128) sm.bad[threadIdx.x] = 0u;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -319,7 +346,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   if (threadIdx.x == 0 && rank == 0) TRACE(9, 0);
-
+  // (each role's code must be dominated by its setmaxnreg: ptxas allocates
+  // a region reached from both budgets with the smaller one)
+  if (warp < 4) {
+  if (kRegsCtl) regs_dec<kRegsCtl ? kRegsCtl : 128>();
   if (warp == 0 || warp == 2) {
     // ============ TMA producers (both CTAs): warp 0 Q + K ring, warp 2 V ring ============
     // Each CTA loads its own half of every tile; completion bytes land on the
@@ -564,7 +594,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  }
+  if (kRegsCtl) regs_inc<128>();  // back to the launch budget for the common tail (waits for the softmax warpgroups)
+  } else {
+    if (kRegsCtl) regs_inc<kRegsCtl ? kRegsSoftmax : 128>();
     // programmatic dependent launch: the mask words come from the kernel
     // launched just before (tree_build); everything else in flight above
     // (TMEM alloc, TMA of Q/K/V, first QK^T) already overlaps its tail
@@ -592,8 +625,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const int node = min(geo.q0 + rho / g, max(geo.n_nodes - 1, 0));
       const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
       const int N = geo.n_tiles;
-      float m_w = -INFINITY, l_w = 0.f;
-      bool seen = false;
+      float m_w = -INFINITY, l_w = 0.f, m_fix = -INFINITY;
+      bool seen = false, bad = false;
       for (int n = (int)((wg + 3 - g_item % 3) % 3); n < N; n += 3) {
         const uint32_t gi = g_item + n;
         const int slot = wg;
@@ -611,84 +644,115 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
           for (int c = 0; c < 4; ++c) vm[c] = vis_word(pref, kvalid, mrow, key0, p.n_words, row_ok, 32 * c);
         }
-        // pass 1: row max over four 32-column chunks, each load overlapped
-        // with the max of the previous chunk (chunk 3 stays in registers)
-        uint32_t r[32], r2[32];
-        SDB_TMEM_LD32(t_s + 0, r2);
-        SDB_TMEM_WAIT_LD_REGS(r2);
-        SDB_TMEM_LD32(t_s + 32, r);
-        if (!full) apply_mask32(r2, vm[0]);
-        float mx = max32(r2);
-        SDB_TMEM_WAIT_LD_REGS(r);
-        SDB_TMEM_LD32(t_s + 64, r2);
-        if (!full) apply_mask32(r, vm[1]);
-        mx = fmaxf(mx, max32(r));
-        SDB_TMEM_WAIT_LD_REGS(r2);
-        SDB_TMEM_LD32(t_s + 96, r);
-        if (!full) apply_mask32(r2, vm[2]);
-        mx = fmaxf(mx, max32(r2));
-        SDB_TMEM_WAIT_LD_REGS(r);
-        if (!full) apply_mask32(r, vm[3]);
-        mx = fmaxf(mx, max32(r));
-        mx *= sl2;
-        if (tr) TRACE(6, gi);
-        // reference max chain (lazy: moves only when the max grows by > 2^8)
-        float m_prev = -INFINITY;
-        if (gi > 0) {
-          asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
-          m_prev = sm.mref[(gi + 2) % 3][i];
-        }
-        if (tr) TRACE(7, gi);
-        const float m_ref = (n == 0 || mx > m_prev + kRescaleThreshold) ? mx : m_prev;
-        sm.mref[slot][i] = m_ref;
-        asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
-        const bool resc = n > 0 && m_ref != m_prev;
-        if (__any_sync(0xffffffffu, resc)) {
-          // O holds items < n relative to m_prev: wait for PV(n - 1), rescale in place
-          const float corr = resc ? ex2(m_prev - m_ref) : 1.f;
-          mbar_wait(&sm.o_done[(gi + 2) % 3], ((gi - 1) / 3) & 1);
-          tc_fence_after();
+        if (kFixRef && n > 0) {
+          // fixed reference: no max pass; the first item of this warpgroup
+          // in the unit takes the reference from the chain
+          if (n <= 2) {
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+            m_fix = sm.mref[(gi + 2) % 3][i];
+            if (n == 1 && N > 2) {
+              sm.mref[slot][i] = m_fix;
+              asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
+            }
+          }
+        } else {
+          // pass 1: row max over four 32-column chunks, each load overlapped
+          // with the max of the previous chunk
+          uint32_t r[32], r2[32];
+          SDB_TMEM_LD32(t_s + 0, r2);
+          SDB_TMEM_WAIT_LD_REGS(r2);
+          SDB_TMEM_LD32(t_s + 32, r);
+          if (!full) apply_mask32(r2, vm[0]);
+          float mx = max32(r2);
+          SDB_TMEM_WAIT_LD_REGS(r);
+          SDB_TMEM_LD32(t_s + 64, r2);
+          if (!full) apply_mask32(r, vm[1]);
+          mx = fmaxf(mx, max32(r));
+          SDB_TMEM_WAIT_LD_REGS(r2);
+          SDB_TMEM_LD32(t_s + 96, r);
+          if (!full) apply_mask32(r2, vm[2]);
+          mx = fmaxf(mx, max32(r2));
+          SDB_TMEM_WAIT_LD_REGS(r);
+          if (!full) apply_mask32(r, vm[3]);
+          mx = fmaxf(mx, max32(r));
+          mx *= sl2;
+          // reference max chain (lazy: moves only when the max grows by > 2^8);
+          // with the fixed reference only the unit's first item gets here and
+          // hands its max to the second
+          float m_prev = -INFINITY;
+          if (!kFixRef && gi > 0) {
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+            m_prev = sm.mref[(gi + 2) % 3][i];
+          }
+          const float m_ref = (n == 0 || mx > m_prev + kRescaleThreshold) ? mx : m_prev;
+          m_fix = m_ref;
+          if (!kFixRef || N > 1) {
+            sm.mref[slot][i] = m_ref;
+            asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
+          }
+          const bool resc = !kFixRef && n > 0 && m_ref != m_prev;
+          if (!kFixRef && __any_sync(0xffffffffu, resc)) {
+            // O holds items < n relative to m_prev: wait for PV(n - 1), rescale in place
+            const float corr = resc ? ex2(m_prev - m_ref) : 1.f;
+            mbar_wait(&sm.o_done[(gi + 2) % 3], ((gi - 1) / 3) & 1);
+            tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            SDB_TMEM_LD32(tmem + lane_off + c * 32, o);
-            tmem_wait_ld();
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              SDB_TMEM_LD32(tmem + lane_off + c * 32, o);
+              tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-            SDB_TMEM_ST32(tmem + lane_off + c * 32, o);
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+              SDB_TMEM_ST32(tmem + lane_off + c * 32, o);
+            }
           }
         }
+        if (tr) TRACE(6, gi);
         if (!seen) {
-          m_w = m_ref;
+          m_w = m_fix;
           seen = true;
-        } else if (m_ref != m_w) {
-          l_w *= ex2(m_w - m_ref);
-          m_w = m_ref;
+        } else if (m_fix != m_w) {
+          l_w *= ex2(m_w - m_fix);
+          m_w = m_fix;
         }
-        const float neg_mu = (m_ref == -INFINITY) ? 0.f : -m_ref;
-        const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
-        // pass 2: P of chunk c (keys 32c .. 32c+31) packed into columns
-        // [32c, 32c + 16) of the slot -- inside the chunk's own, already
-        // consumed S columns.  Chunk 3 first (still in registers); each
-        // reload is overlapped with the exps of the previous chunk.
-        SDB_TMEM_LD32(t_s + 0, r2);
-        float rs = exp_pack32<EMU8>(r, sc2, nm2);
-        SDB_TMEM_ST16(t_s + 96, r);
-        SDB_TMEM_WAIT_LD_REGS(r2);
-        SDB_TMEM_LD32(t_s + 32, r);
-        if (!full) apply_mask32(r2, vm[0]);
-        rs += exp_pack32<EMU8>(r2, sc2, nm2);
-        SDB_TMEM_ST16(t_s + 0, r2);
-        SDB_TMEM_WAIT_LD_REGS(r);
-        SDB_TMEM_LD32(t_s + 64, r2);
-        if (!full) apply_mask32(r, vm[1]);
-        rs += exp_pack32<EMU8>(r, sc2, nm2);
-        SDB_TMEM_ST16(t_s + 32, r);
-        SDB_TMEM_WAIT_LD_REGS(r2);
-        if (!full) apply_mask32(r2, vm[2]);
-        rs += exp_pack32<EMU8>(r2, sc2, nm2);
-        SDB_TMEM_ST16(t_s + 64, r2);
-        l_w += rs;
+        {
+          // exp pass: P of chunk c (keys 32c .. 32c+31) packed into columns
+          // [32c, 32c + 16) of the slot -- inside the chunk's own, already
+          // loaded S columns; each load overlapped with the previous
+          // chunk's exps.  The row max of the item is tracked on the side:
+          // with the fixed reference, a score above m_ref + kOverflowLog2
+          // (or a visible key in a row whose reference is -inf) flags the
+          // row for the exact recompute.
+          const float neg_mu = (m_fix == -INFINITY) ? 0.f : -m_fix;
+          const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
+          uint32_t r[32], r2[32];
+          SDB_TMEM_LD32(t_s + 0, r2);
+          SDB_TMEM_WAIT_LD_REGS(r2);
+          SDB_TMEM_LD32(t_s + 32, r);
+          if (!full) apply_mask32(r2, vm[0]);
+          float mo = kFixRef ? max32(r2) : 0.f;
+          float rs = exp_pack32<EMU8>(r2, sc2, nm2);
+          SDB_TMEM_ST16(t_s + 0, r2);
+          SDB_TMEM_WAIT_LD_REGS(r);
+          SDB_TMEM_LD32(t_s + 64, r2);
+          if (!full) apply_mask32(r, vm[1]);
+          if (kFixRef) mo = fmaxf(mo, max32(r));
+          rs += exp_pack32<EMU8>(r, sc2, nm2);
+          SDB_TMEM_ST16(t_s + 32, r);
+          SDB_TMEM_WAIT_LD_REGS(r2);
+          SDB_TMEM_LD32(t_s + 96, r);
+          if (!full) apply_mask32(r2, vm[2]);
+          if (kFixRef) mo = fmaxf(mo, max32(r2));
+          rs += exp_pack32<EMU8>(r2, sc2, nm2);
+          SDB_TMEM_ST16(t_s + 64, r2);
+          SDB_TMEM_WAIT_LD_REGS(r);
+          if (!full) apply_mask32(r, vm[3]);
+          if (kFixRef) mo = fmaxf(mo, max32(r));
+          rs += exp_pack32<EMU8>(r, sc2, nm2);
+          SDB_TMEM_ST16(t_s + 96, r);
+          l_w += rs;
+          if (kFixRef) bad |= mo * sl2 > m_fix + kOverflowLog2;
+        }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -703,15 +767,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       // ---- unit end: combine the partial row sums, normalise, store ----
       sm.lsum[wg][i] = l_w;
       sm.msum[wg][i] = seen ? m_w : -INFINITY;
-      asm volatile("bar.sync %0, %1;" ::"r"(kBarUnit), "r"(kSoftmaxWG * 128) : "memory");
+      if (bad) sm.bad[i] = 1u;
+      // unit-end barrier of the softmax warps, OR-reducing "a row needs the exact recompute"
+      uint32_t any_bad;
+      asm volatile(
+          "{\n.reg .pred pi, po;\nsetp.ne.u32 pi, %1, 0;\nbar.red.or.pred po, %2, %3, pi;\n"
+          "selp.u32 %0, 1, 0, po;\n}"
+          : "=r"(any_bad)
+          : "r"(bad ? 1u : 0u), "r"(kBarUnit), "r"(kSoftmaxWG * 128)
+          : "memory");
       const uint32_t gl = g_item + N - 1;  // the unit's last item
-      const float m_fin = sm.mref[gl % 3][i];
+      // the final reference is the largest one any warpgroup used (the
+      // running max only grows; with the fixed reference they are all equal)
+      float m_fin = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kSoftmaxWG; ++w) m_fin = fmaxf(m_fin, sm.msum[w][i]);
       float l_full = 0.f;
 #pragma unroll
       for (int w = 0; w < kSoftmaxWG; ++w) {
         const float mw = sm.msum[w][i];
         if (mw != -INFINITY) l_full += sm.lsum[w][i] * ex2(mw - m_fin);
       }
+      bool row_bad = false;
+      if (any_bad && wg == 0) {
+        row_bad = sm.bad[i] != 0u;
+        sm.bad[i] = 0u;
+      }
+      bad = false;
       asm volatile("bar.sync %0, %1;" ::"r"(kBarUnit), "r"(kSoftmaxWG * 128) : "memory");
       mbar_wait(&sm.o_done[gl % 3], (gl / 3) & 1);
       tc_fence_after();
@@ -725,9 +807,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         else
           mbar_arrive_leader(&sm.o_free);
       }
+      if (any_bad) {
+        // every warpgroup's epilogue stores are done; overwrite the flagged rows exactly
+        asm volatile("bar.sync %0, %1;" ::"r"(kBarUnit), "r"(kSoftmaxWG * 128) : "memory");
+        if (row_bad) exact_row(sp, item, geo, g, local);
+      }
       if (tr && wg == 0) TRACE(10, g_item);
       g_item += N;
     }
+    if (kRegsCtl) regs_dec<128>();
   }
   if (threadIdx.x == 0 && rank == 0) TRACE(11, 0);
   tc_fence_before();

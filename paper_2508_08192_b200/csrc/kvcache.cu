@@ -11,6 +11,14 @@
 
 namespace sdb {
 
+// Page of position pos of sequence b, or -1 when the position lies past the
+// sequence's mapped blocks (unmapped table entry or beyond max_blocks).
+__device__ __forceinline__ int mapped_page(const int32_t *__restrict__ block_table, int b, int max_blocks,
+                                           int64_t pos, int block_size) {
+  if (pos < 0 || pos / block_size >= max_blocks) return -1;
+  return block_table[(int64_t)b * max_blocks + pos / block_size];
+}
+
 // One CTA per (row slot, sequence, layer); threads stride over hkv*head_dim
 // in 16-byte chunks, K and V in the same pass.
 __global__ void compact_kv_kernel(const uint8_t *__restrict__ tree_k, const uint8_t *__restrict__ tree_v,
@@ -19,7 +27,7 @@ __global__ void compact_kv_kernel(const uint8_t *__restrict__ tree_k, const uint
                                   int max_blocks, const int32_t *__restrict__ ctx_len,
                                   const int32_t *__restrict__ path, const int32_t *__restrict__ path_len,
                                   const int32_t *__restrict__ n_keep, int batch, int r_max, int hkv,
-                                  int row_bytes, int block_size) {
+                                  int row_bytes, int block_size, int32_t *__restrict__ err) {
   const int slot = blockIdx.x, b = blockIdx.y, layer = blockIdx.z;
   int len = path_len[b];
   int keep = n_keep ? n_keep[b] : len + 1;
@@ -27,7 +35,11 @@ __global__ void compact_kv_kernel(const uint8_t *__restrict__ tree_k, const uint
   if (slot >= n_write) return;
   int row = slot == 0 ? 0 : 1 + path[(int64_t)b * r_max + slot - 1];
   int64_t pos = (int64_t)ctx_len[b] + slot;
-  int page = block_table[(int64_t)b * max_blocks + pos / block_size];
+  int page = mapped_page(block_table, b, max_blocks, pos, block_size);
+  if (page < 0) {  // CacheError "write past allocated blocks" (kvstore.py:220-221)
+    if (threadIdx.x == 0 && layer == 0 && err) atomicOr(err, SDB_ERR_CACHE);
+    return;
+  }
   int off = (int)(pos % block_size);
   const int64_t src_row = (((int64_t)layer * batch + b) * r_max + row) * hkv;  // in units of head rows
   const int chunks = row_bytes / 16;
@@ -70,7 +82,7 @@ extern "C" int sdb_compact_kv(const void *tree_k, const void *tree_v, void *k_ca
                               int64_t cache_layer_stride, const int32_t *block_table, int max_blocks,
                               const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
                               const int32_t *n_keep, int n_layers, int batch, int r_max, int hkv,
-                              int head_dim, int block_size, int elem_bytes, void *stream) {
+                              int head_dim, int block_size, int elem_bytes, int32_t *err, void *stream) {
   if (!tree_k || !tree_v || !k_cache || !v_cache || !block_table || !ctx_len || !path || !path_len)
     return SDB_E_INVALID;
   if (n_layers < 1 || batch < 0 || r_max < 1 || hkv < 1 || head_dim < 1 || block_size < 1)
@@ -84,7 +96,7 @@ extern "C" int sdb_compact_kv(const void *tree_k, const void *tree_v, void *k_ca
   sdb::compact_kv_kernel<<<grid, threads, 0, sdb::as_stream(stream)>>>(
       (const uint8_t *)tree_k, (const uint8_t *)tree_v, (uint8_t *)k_cache, (uint8_t *)v_cache,
       cache_layer_stride * elem_bytes, block_table, max_blocks, ctx_len, path, path_len, n_keep, batch, r_max,
-      hkv, row_bytes, block_size);
+      hkv, row_bytes, block_size, err);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
@@ -137,14 +149,18 @@ __global__ void compact_draft_kv_kernel(const uint8_t *__restrict__ suf_k, const
                                         int max_blocks, const int32_t *__restrict__ ctx_len,
                                         const int32_t *__restrict__ path, const int32_t *__restrict__ path_len,
                                         const int32_t *__restrict__ n_keep, int batch, int r_max, int n_src,
-                                        int hkv, int row_bytes, int block_size) {
+                                        int hkv, int row_bytes, int block_size, int32_t *__restrict__ err) {
   const int slot = blockIdx.x, b = blockIdx.y, layer = blockIdx.z;
   const int len = path_len[b];
   const int keep = n_keep ? n_keep[b] : len + 1;
   if (slot >= min(keep - 1, len)) return;
   const int row = path[(int64_t)b * r_max + slot];
   const int64_t pos = (int64_t)ctx_len[b] + 1 + slot;
-  const int page = block_table[(int64_t)b * max_blocks + pos / block_size];
+  const int page = mapped_page(block_table, b, max_blocks, pos, block_size);
+  if (page < 0) {
+    if (threadIdx.x == 0 && layer == 0 && err) atomicOr(err, SDB_ERR_CACHE);
+    return;
+  }
   const int off = (int)(pos % block_size);
   const int64_t src_row = (((int64_t)layer * batch + b) * n_src + row) * hkv;
   const int chunks = row_bytes / 16;
@@ -242,7 +258,7 @@ extern "C" int sdb_compact_draft_kv(const void *suffix_k, const void *suffix_v, 
                                     int64_t cache_layer_stride, const int32_t *block_table, int max_blocks,
                                     const int32_t *ctx_len, const int32_t *path, const int32_t *path_len,
                                     const int32_t *n_keep, int n_layers, int batch, int r_max, int n_src, int hkv,
-                                    int head_dim, int block_size, int elem_bytes, void *stream) {
+                                    int head_dim, int block_size, int elem_bytes, int32_t *err, void *stream) {
   if (!suffix_k || !suffix_v || !k_cache || !v_cache || !block_table || !ctx_len || !path || !path_len ||
       n_layers < 1 || batch < 0 || r_max < 1 || n_src < 1 || hkv < 1 || block_size < 1 || max_blocks < 1)
     return SDB_E_INVALID;
@@ -253,7 +269,7 @@ extern "C" int sdb_compact_draft_kv(const void *suffix_k, const void *suffix_v, 
   sdb::compact_draft_kv_kernel<<<grid, 128, 0, sdb::as_stream(stream)>>>(
       (const uint8_t *)suffix_k, (const uint8_t *)suffix_v, (uint8_t *)k_cache, (uint8_t *)v_cache,
       cache_layer_stride * elem_bytes, block_table, max_blocks, ctx_len, path, path_len, n_keep, batch, r_max, n_src,
-      hkv, row_bytes, block_size);
+      hkv, row_bytes, block_size, err);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

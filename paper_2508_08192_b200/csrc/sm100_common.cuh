@@ -186,6 +186,17 @@ __device__ __forceinline__ float max_nan3(float a, float b, float c) {
 // wait for the upstream kernel's completion + memory flush (no-op when the
 // kernel was launched without the programmatic-serialization attribute)
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Warp-specialised register budgets (whole warpgroup, warp-uniform): the
+// producer / MMA warpgroup hands registers to the softmax warpgroups.
+template <int N>
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
 // let the downstream PDL kernel start launching (its CTAs run their
 // prologue until their own griddep_wait)
 __device__ __forceinline__ void griddep_launch_dependents() {
@@ -674,6 +685,87 @@ __device__ __forceinline__ void inactive_row(const Sm100Params &sp, const Item &
                        (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim;
     for (int c = 0; c < kHeadDim; c += 8) *reinterpret_cast<uint4 *>(o + c) = make_uint4(0, 0, 0, 0);
     if (p.lse) p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = -INFINITY;
+  }
+}
+
+// Exact fallback for one query row of an item, on the CUDA cores: two fp32
+// passes (max, then exp-sum and P.V) over exactly the keys the item covers
+// (its prefix tiles through the block table, its tree tiles under the
+// ancestor mask), writing what the epilogue writes (bf16 out + LSE of a whole
+// unit, the fp32 partial of a split one).  Runs only when the fixed-reference
+// softmax saw a score far above its reference (kOverflowLog2) -- never for
+// attention scores within ~60 nats of the piece's first tile.
+static __device__ __noinline__ void exact_row(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,
+                                       int local) {
+  const TreeAttnParams &p = sp.p;
+  const int rho = geo.row0 + local;
+  if (rho >= geo.rows_total || geo.q0 * g + rho >= p.r_max * g) return;  // padding rows keep the epilogue's zeros
+  const int node = geo.q0 + rho / g;
+  const int hq_idx = geo.kvh * g + (rho % g);
+  const __nv_bfloat16 *q = reinterpret_cast<const __nv_bfloat16 *>(p.q) +
+                           (((int64_t)geo.b * p.r_max + node) * p.hq + hq_idx) * kHeadDim;
+  const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
+  const int32_t *bt = p.block_table + (int64_t)geo.b * p.max_blocks;
+  const int kp0 = geo.k0 + geo.pa * kTileN, kp1 = min(geo.k0 + (geo.pa + geo.n_pref) * kTileN, geo.C);
+  const int ks0 = geo.sa * kTileN, ks1 = min((geo.sa + geo.n_suf) * kTileN, geo.n_nodes);
+  auto key_row = [&](int j, bool pref, bool v) -> const __nv_bfloat16 * {
+    if (pref) {
+      const int page = bt[j / p.block_size];
+      const int64_t off = (((int64_t)page * p.hkv + geo.kvh) * p.block_size + j % p.block_size) * kHeadDim;
+      return reinterpret_cast<const __nv_bfloat16 *>(v ? p.v_cache : p.k_cache) + off;
+    }
+    return reinterpret_cast<const __nv_bfloat16 *>(v ? p.tree_v : p.tree_k) +
+           (((int64_t)geo.b * p.r_max + j) * p.hkv + geo.kvh) * kHeadDim;
+  };
+  auto score = [&](const __nv_bfloat16 *k) {
+    float s = 0.f;
+#pragma unroll 8
+    for (int e = 0; e < kHeadDim; ++e) s += __bfloat162float(q[e]) * __bfloat162float(k[e]);
+    return s * p.scale;
+  };
+  auto visible = [&](int j) { return j < geo.n_nodes && ((mrow[j >> 5] >> (j & 31)) & 1u); };
+  float m = -INFINITY;
+  for (int j = kp0; j < kp1; ++j) m = fmaxf(m, score(key_row(j, true, false)));
+  for (int j = ks0; j < ks1; ++j)
+    if (visible(j)) m = fmaxf(m, score(key_row(j, false, false)));
+  // P.V in four 32-column chunks (scores recomputed per chunk: a small
+  // register footprint for a path that essentially never runs)
+  float l = 0.f;
+  for (int c = 0; c < kHeadDim / 32; ++c) {
+    float o[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) o[e] = 0.f;
+    float lc = 0.f;
+    auto accum = [&](int j, bool pref) {
+      const float w = __expf(score(key_row(j, pref, false)) - m);
+      const __nv_bfloat16 *v = key_row(j, pref, true) + 32 * c;
+      lc += w;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] += w * __bfloat162float(v[e]);
+    };
+    if (m != -INFINITY) {
+      for (int j = kp0; j < kp1; ++j) accum(j, true);
+      for (int j = ks0; j < ks1; ++j)
+        if (visible(j)) accum(j, false);
+    }
+    if (c == 0) l = lc;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    if (item.whole) {
+      __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) +
+                           (((int64_t)geo.b * p.r_max + node) * p.hq + hq_idx) * kHeadDim + 32 * c;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) out[e] = __float2bfloat16(o[e] * inv);
+    } else {
+      float *out = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim + 32 * c;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) out[e] = o[e] * inv;
+    }
+  }
+  const float lse_n = l > 0.f ? m + __logf(l) : -INFINITY;
+  if (item.whole) {
+    if (p.lse) p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node] = lse_n;
+  } else {
+    sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = lse_n;
   }
 }
 

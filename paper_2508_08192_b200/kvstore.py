@@ -207,9 +207,12 @@ class PagedKvCache:
 # batched device write-back
 # ---------------------------------------------------------------------------
 
-def compact_kv(tree_k, tree_v, k_pools, v_pools, block_table, ctx_len, path, path_len, n_keep=None, stream=None):
+def compact_kv(tree_k, tree_v, k_pools, v_pools, block_table, ctx_len, path, path_len, n_keep=None, stream=None,
+               err=None):
     """Write rows [0] + [1 + a for a in path[:n_keep-1]] of every sequence's
     tree K/V into its pages at positions ctx_len.. for every layer.
+    Positions past a sequence's mapped blocks are not written; they set
+    SDB_ERR_CACHE in ``err`` (int32 [1], e.g. the acceptance's error word).
 
     tree_k/v [L, B, R, Hkv, d]; k_pools/v_pools [L, num_blocks, Hkv, bs, d];
     block_table int32 [B, max_blocks]; ctx_len / path_len / n_keep int32 [B];
@@ -222,7 +225,7 @@ def compact_kv(tree_k, tree_v, k_pools, v_pools, block_table, ctx_len, path, pat
     rc = _lib.lib().sdb_compact_kv(_lib.ptr(tree_k), _lib.ptr(tree_v), _lib.ptr(k_pools), _lib.ptr(v_pools),
                                    layer_stride, _lib.ptr(block_table), block_table.shape[1], _lib.ptr(ctx_len),
                                    _lib.ptr(path), _lib.ptr(path_len), _lib.ptr(n_keep), n_layers, b, r, hkv, d, bs,
-                                   tree_k.element_size(), _lib.stream_ptr(stream))
+                                   tree_k.element_size(), _lib.ptr(err), _lib.stream_ptr(stream))
     _lib.check(rc, "compact_kv")
 
 
@@ -231,7 +234,7 @@ def compact_kv(tree_k, tree_v, k_pools, v_pools, block_table, ctx_len, path, pat
 # ---------------------------------------------------------------------------
 
 def compact_draft_kv(suffix_k, suffix_v, k_pools, v_pools, block_table, ctx_len, path, path_len, n_keep=None,
-                     stream=None):
+                     stream=None, err=None):
     """Draft-cache write-back (engine.py:524-531): rows path[:n_keep-1] of the
     draft's carried suffix K/V [L, B, n_src, Hkv, d] (realized draft nodes, no
     root row) into the draft pages at positions ctx_len + 1 .. (= L)."""
@@ -243,7 +246,7 @@ def compact_draft_kv(suffix_k, suffix_v, k_pools, v_pools, block_table, ctx_len,
                                          _lib.ptr(v_pools), k_pools.stride(0), _lib.ptr(block_table),
                                          block_table.shape[1], _lib.ptr(ctx_len), _lib.ptr(path), _lib.ptr(path_len),
                                          _lib.ptr(n_keep), n_layers, b, path.shape[1], n_src, hkv, d, bs,
-                                         suffix_k.element_size(), _lib.stream_ptr(stream))
+                                         suffix_k.element_size(), _lib.ptr(err), _lib.stream_ptr(stream))
     _lib.check(rc, "compact_draft_kv")
 
 

@@ -67,6 +67,12 @@ def _raise_err(code, what):
         raise SamplingError("distribution entries must be >= 0 and sum to 1")
     if code & _lib.SDB_ERR_UNIFORMS:
         raise SamplingError("uniform stream exhausted")
+    if code & _lib.SDB_ERR_PLAN:
+        raise SamplingError("tree deeper / wider than the planned walk levels")
+    if code & _lib.SDB_ERR_CACHE:
+        from .kvstore import CacheError
+
+        raise CacheError("write past allocated blocks")
 
 
 def target_dists(logits, temperature, top_p, allowed=None):
@@ -203,6 +209,13 @@ class AcceptResult:
     uniforms_used: "object"  # int32 [B]
     err: "object"            # int32 [1] device error bits
     residual: "object" = None
+
+    def raise_if_error(self, what="acceptance"):
+        """Host sync: map the device error bits to the reference exceptions
+        (ValueError for NaN, SamplingError, CacheError for a compaction
+        past the mapped blocks)."""
+        if self.err is not None:
+            _raise_err(int(self.err.reshape(-1)[0].item()), what)
 
 
 class GreedyAcceptor:
@@ -404,6 +417,13 @@ class StochasticAcceptor:
         b, r, v = target_logits.shape
         if target_logits.dtype != torch.float32 or draft_logits.dtype != torch.float32:
             raise SamplingError("stochastic acceptance takes fp32 logits")
+        # every stochastic kernel indexes rows as (b * r_max + r) * vocab
+        if (not target_logits.is_contiguous() or not draft_logits.is_contiguous()
+                or draft_logits.shape != target_logits.shape):
+            raise SamplingError("stochastic acceptance takes contiguous [B, R, V] target and draft logits")
+        if uniforms is not None and (uniforms.dtype != torch.float64 or uniforms.dim() != 2
+                                     or uniforms.shape[0] != b or not uniforms.is_contiguous()):
+            raise SamplingError("uniforms must be a contiguous float64 [B, n_uniforms] tensor")
         if not (temperature > 0):
             raise SamplingError("stochastic acceptance needs temperature > 0 (use accept_greedy)")
         dev = target_logits.device

@@ -91,13 +91,30 @@ class ShardedGreedyAcceptor:
         self.group = group
 
     def __call__(self, logits_shard, parent, n_rows, tokens, stream=None):
-        from .sampling import argmax_keys, greedy_walk
+        """The rank's error word rides in the same all-reduce as the keys (one
+        extra int64 after the B*R keys), so a NaN in any shard raises on every
+        rank (softmax_lse, numcore.py:47-48) instead of only on its owner."""
+        import torch
+
+        from . import _lib
+        from .sampling import greedy_walk
 
         b, r, v = logits_shard.shape
-        keys, err = argmax_keys(logits_shard.reshape(b * r, v), vocab_offset=self.shard.v_lo, stream=stream)
-        combine_argmax_keys(keys, self.group)
-        res = greedy_walk(keys.reshape(b, r), parent, n_rows, tokens, stream=stream)
-        res.err = err
+        if logits_shard.stride(2) != 1 or (b > 1 and logits_shard.stride(0) != r * logits_shard.stride(1)):
+            raise ValueError("logits shard must be [B, R, V_local] with unit vocab stride and uniform row stride")
+        rows = b * r
+        dev = logits_shard.device
+        keys = torch.empty((rows + 1,), dtype=torch.int64, device=dev)
+        err = torch.zeros((1,), dtype=torch.int32, device=dev)
+        dt = _lib.DTYPE_F32 if logits_shard.dtype == torch.float32 else _lib.DTYPE_BF16
+        rc = _lib.lib().sdb_argmax_keys(_lib.ptr(logits_shard), dt, rows, v, logits_shard.stride(1),
+                                        int(self.shard.v_lo), _lib.ptr(keys), _lib.ptr(err), _lib.stream_ptr(stream))
+        _lib.check(rc, "argmax_keys")
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream(dev)):
+            keys[rows:].copy_(err)  # error bits (MAX over ranks: nonzero anywhere -> nonzero everywhere)
+            combine_argmax_keys(keys, self.group)
+            res = greedy_walk(keys[:rows].reshape(b, r), parent, n_rows, tokens, stream=stream)
+            res.err = keys[rows:].to(torch.int32)
         return res
 
 

@@ -149,7 +149,7 @@ class TreeVerifier:
             if compact:
                 compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0),
                            x.v_pool.unsqueeze(0), x.block_table, x.ctx_len, acc.path, acc.path_len, None,
-                           stream=main)
+                           stream=main, err=acc.err)
             return o["out"], o["lse"], acc, o["tree_err"]
         # overlap only when the attention's persistent grid leaves SMs free
         # (small batches); at full occupancy the acceptance CTAs would delay
@@ -173,7 +173,7 @@ class TreeVerifier:
                 # attention reads (prefix keys < ctx_len are the only unmasked ones)
                 compact_kv(x.tree_k.unsqueeze(0), x.tree_v.unsqueeze(0), x.k_pool.unsqueeze(0),
                            x.v_pool.unsqueeze(0), x.block_table, x.ctx_len, acc.path, acc.path_len, None,
-                           stream=side)
+                           stream=side, err=acc.err)
         if side is not main:
             main.wait_stream(side)
         return o["out"], o["lse"], acc, o["tree_err"]
@@ -210,14 +210,6 @@ class TreeVerifier:
         attn_s = 4.0 * d * hq * b * r * ctx / 1.0e15
         scan_s = (b * r / _num_sms(device)) * x.logits.shape[2] * 4 / 10.0e9
         return scan_s < 0.8 * attn_s
-
-    # kernel launches per step (for the bench's gpu_launches claim)
-    def launches_per_step(self, x: StepInputs):
-        n_attn = 1
-        a = self.attn
-        return 1 + n_attn + (1 if self._needs_combine else 0) + 2 + 1
-
-    _needs_combine = True
 
     def capture(self, x: StepInputs, warmup=2):
         """Capture one step into a CUDA graph; replay with ``replay()``."""

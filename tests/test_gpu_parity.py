@@ -919,3 +919,35 @@ def test_tcgen05_r65_variant_vs_oracle():
     err = np.abs(out.float().cpu().numpy() - want_o)
     assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
     assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
+
+
+@pytest.mark.parametrize("ctas", [0, 148])
+def test_tcgen05_fixed_reference_overflow_exact(ctas):
+    """The pair kernel's softmax takes each unit piece's first-tile row max as
+    a fixed reference (no max pass, no rescale afterwards).  A key whose score
+    lies ~170 nats above everything in the first tile (exp2 would overflow
+    against that reference) sends the affected rows through the exact
+    recompute; whole units (ctas 0) and stream-K pieces merged by the fix-up
+    (ctas 148 at B = 1) must both match the float64 oracle."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    B = 2 if ctas == 0 else 1
+    c = _rand_paged_case(B, 64, 8, 128, 3000, 64, TREE64, seed=91, ragged=False)
+    kvh, g, j = 3, 8, 2500  # late prefix key of sequence 0 / KV head 3
+    page = int(c["table_np"][0, j // 64])
+    c["kp"][page, kvh, j % 64, :] = 4.0
+    c["q"][0, :, kvh * g:(kvh + 1) * g, :] = 4.0
+    out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                     c["nr"], 128 ** -0.5, num_splits=ctas, kernel=1)
+    torch.cuda.synchronize()
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(c["q"]), f64(c["kp"]), f64(c["vp"]), c["table_np"],
+                                                   c["ctx_np"], f64(c["tk"]), f64(c["tv"]), [c["aug"]] * B,
+                                                   128 ** -0.5)
+    got_o = out.float().cpu().numpy()
+    assert np.isfinite(got_o).all()
+    err = np.abs(got_o - want_o)
+    assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+    assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
+    # the flagged rows really are dominated by the planted key (LSE ~ 181 nats)
+    assert want_l[0, kvh * g:(kvh + 1) * g].min() > 150

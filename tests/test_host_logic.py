@@ -45,3 +45,30 @@ def test_unpack_mask_words():
     words = np.array([[1, 0], [3, 0], [0x80000001, 1]], dtype=np.uint32).astype(np.int32)
     m = D.unpack_mask_words(words, 33)
     assert m[0, 0] and not m[0, 1] and m[1, 1] and m[2, 31] and m[2, 32]
+
+
+def test_shim_patch_targets_exist():
+    """Every early-bound name the reference shim rebinds exists in the
+    installed reference package (baseline/_ref), so install_reference
+    covers the whole verification path (model.py:21, engine.py:31-33,
+    verify.py:19)."""
+    import importlib
+    import os
+    import sys
+    import tempfile
+
+    import pytest
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "specdec")):
+        pytest.skip("reference package not installed in baseline/_ref")
+    os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_"))
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from paper_2508_08192_b200.shim import _PATCHES
+
+    for mod_name, attr, new in _PATCHES:
+        mod = importlib.import_module(f"specdec.{mod_name}")
+        old = getattr(mod, attr)
+        assert callable(old) and callable(new)
+        assert old.__name__ == new.__name__, (mod_name, attr)

@@ -117,6 +117,11 @@ def test_stochastic_mss_matches_reference(golden):
         assert nxt == int(g[p + "next"])
         assert used == int(g[p + "used"])
         np.testing.assert_allclose(resid, g[p + "residual"], atol=1e-15)
+        # the lazy accessor form (rows computed on demand) walks identically
+        lz = O.mss_verify(parent, g[p + "tokens"], lambda c: qd[c],
+                          lambda i: O.target_dist(logits[i], temp, top_p), g[p + "uniforms"])
+        assert lz[0] == path and lz[1] == nxt and lz[3] == used
+        np.testing.assert_array_equal(lz[2], resid)
 
 
 def test_sampling_known_answers(golden):

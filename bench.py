@@ -50,6 +50,10 @@ CONFIGS = {
                ctx=0, bs=64, V=128256, accept_only=True, mode="stochastic"),
 }
 TEMPERATURE, TOP_P = 1.0, 0.9
+# HBM-bound contrast trees of SURVEY.md 8(d) at the C3 shapes: chain-3
+# (build_chain(3), drafttree.py:60-63; R = 4, R*g = 32) and the reference's
+# N8 tree (R = 9, R*g = 72)
+TREES = {"64": TREE64, "65": TREE64 + [0], "chain3": [-1, 0, 1], "n8": [-1, -1, 0, 0, 1, 2, 2, 5]}
 TREE = TREE64  # set from --tree
 
 
@@ -309,6 +313,78 @@ def parity_sample(cfg, x, out, lse, acc, mode, aug):
     return res
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_reference():
+    """The unmodified reference package installed in baseline/_ref (pip
+    --target, gitignored, shipped with the snapshot), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "specdec")):
+        return None
+    import tempfile
+
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "sdb_numba_cache"))
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import specdec
+    import specdec.attention
+    import specdec.engine
+    import specdec.kernels
+    import specdec.sampling
+
+    return specdec
+
+
+def reference_sample(ref, cfg, seed=0, mode="greedy"):
+    """The STOCK reference path on a bounded sample of the workload: one
+    sequence x one KV-head group of the attention through
+    specdec.attention.tree_attention (kernels.attend_heads under the numba and
+    the numpy backends; GQA by repeating the KV head), and one
+    sequence of acceptance: specdec.sampling.target_dist for every row (+ the
+    draft q of every parent row) and mss_verify (sampling.py:87-202).
+    Returns {"attn_numba": s, "attn_numpy": s, "accept": s}."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    B, Hq, Hkv, d, C, V = (cfg[k] for k in ("B", "Hq", "Hkv", "d", "ctx", "V"))
+    g = Hq // Hkv
+    tree = ref.drafttree.TreeSpec(tuple(TREE))
+    aug = ref.engine._augment(tree)
+    R = aug.n_nodes
+    out = {}
+    if not cfg.get("accept_only"):
+        def bf(x):
+            return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+        q = bf(rng.normal(size=(R, g * d)))
+        ck = np.repeat(bf(rng.normal(size=(C, 1, d))), g, axis=1).reshape(C, g * d)
+        cv = np.repeat(bf(rng.normal(size=(C, 1, d))), g, axis=1).reshape(C, g * d)
+        tk = np.repeat(bf(rng.normal(size=(R, 1, d))), g, axis=1).reshape(R, g * d)
+        tv = np.repeat(bf(rng.normal(size=(R, 1, d))), g, axis=1).reshape(R, g * d)
+        for backend in ("numba", "numpy"):
+            prev = ref.kernels.set_backend(backend)
+            try:
+                t0 = time.perf_counter()
+                ref.attention.tree_attention(q, ck, cv, tk, tv, aug, d ** -0.5, n_heads=g)
+                out["attn_" + backend] = time.perf_counter() - t0
+            finally:
+                ref.kernels.set_backend(prev)
+    logits = (2.0 * rng.normal(size=(R, V))).astype(np.float32).astype(np.float64)
+    draft = logits + 0.5 * rng.normal(size=(R, V))
+    T, top_p = (0.0, 1.0) if mode == "greedy" else (TEMPERATURE, TOP_P)
+    t1 = time.perf_counter()
+    tdists = [ref.sampling.target_dist(logits[i], T, top_p) for i in range(R)]
+    qrow = {p_: ref.sampling.target_dist(draft[p_], T, 1.0) for p_ in set(aug.parent[1:])}
+    node_dists = tuple(qrow[aug.parent[1 + c]] for c in range(tree.n_nodes))
+    tokens = tuple(int(rng.integers(V)) for _ in range(tree.n_nodes))
+    res = ref.sampling.mss_verify(ref.sampling.DraftResult(tree, tokens, node_dists), tdists,
+                                  ref.sampling.rank_sliced_uniforms(seed, 16, 1, R + 1)[0],
+                                  "greedy_children" if mode == "greedy" else "stochastic")
+    out["accept"] = time.perf_counter() - t1
+    out["accepted"] = len(res.accepted_path)
+    return out
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -328,6 +404,13 @@ def _sample_desc(cfg, mode, cores):
 
 
 def run_reference(args, cfg, mode):
+    """--impl reference: the reference's own CPU implementation of the path
+    (stock specdec from baseline/_ref when installed, else the numpy port),
+    rank 0 only, all host cores.  Each step is a bounded sample -- one
+    sequence x one KV-head group of the attention, one sequence of acceptance
+    -- extrapolated exactly to the batch (the reference loops sequences one
+    after another, engine.py:581-582; attention is per KV head).  The measured
+    sample seconds and the extrapolation factors are reported separately."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -338,21 +421,58 @@ def run_reference(args, cfg, mode):
         threadpool_limits(os.cpu_count() or 1)
     except Exception:  # noqa: BLE001 - threadpoolctl is optional
         pass
-    samples = []
-    for i in range(args.warmup + args.steps):
-        ta, tacc, fa, facc = cpu_sample(cfg, seed=i, mode=mode)
-        if i >= args.warmup:
-            samples.append(ta * fa + tacc * facc)
-    per_step = statistics.mean(samples)
-    us = per_step * 1e6
     cores = blas_threads()
+    f_attn = 0 if cfg.get("accept_only") else cfg["B"] * cfg["Hkv"]
+    f_acc = cfg["B"]
+    ref = load_reference()
+    port = None
+    if ref is not None:
+        reference_sample(ref, cfg, seed=10_000, mode=mode)  # numba JIT compile + warm caches
+        per_step, samples = [], []
+        for i in range(args.warmup + args.steps):
+            smp = reference_sample(ref, cfg, seed=i, mode=mode)
+            if i >= args.warmup:
+                samples.append(smp)
+        attn_best = {k: statistics.mean(x[k] for x in samples) for k in ("attn_numba", "attn_numpy")
+                     if k in samples[0]}
+        acc_s = statistics.mean(x["accept"] for x in samples)
+        # the faster stock backend is the reference's best CPU number
+        best_key = min(attn_best, key=attn_best.get) if attn_best else None
+        attn_s = attn_best[best_key] if best_key else 0.0
+        best_backend = best_key[len("attn_"):] if best_key else None
+        step_s = attn_s * f_attn + acc_s * f_acc
+        kind = "reference"
+        sample = (f"stock specdec (baseline/_ref): tree_attention of 1 sequence x 1 KV-head group "
+                  f"({cfg['Hq'] // cfg['Hkv']} q heads, {best_backend} backend, x{f_attn}) + target_dist/mss_verify "
+                  f"of 1 sequence (x{f_acc}); {cores} host threads; extrapolated"
+                  if f_attn else f"stock specdec (baseline/_ref): target_dist + mss_verify of 1 sequence (x{f_acc}); "
+                                 f"{cores} host threads; extrapolated")
+        extra = {"sample_seconds": {**{k: v for k, v in attn_best.items()}, "accept": acc_s},
+                 "extrapolation": {"attention": f_attn, "accept": f_acc},
+                 "attn_backends_us_per_step": {k: v * f_attn * 1e6 + acc_s * f_acc * 1e6
+                                               for k, v in attn_best.items()}}
+        # the numpy port (oracle restatement) as a secondary figure
+        ta, tacc, fa, facc = cpu_sample(cfg, seed=1, mode=mode)
+        port = (ta * fa + tacc * facc) * 1e6
+    else:
+        samples = []
+        for i in range(args.warmup + args.steps):
+            ta, tacc, fa, facc = cpu_sample(cfg, seed=i, mode=mode)
+            if i >= args.warmup:
+                samples.append(ta * fa + tacc * facc)
+        step_s = statistics.mean(samples)
+        kind = "port"
+        sample = _sample_desc(cfg, mode, cores)
+        extra = {}
+    us = step_s * 1e6
     line = {"impl": "reference", "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "global_batch": cfg["B"], "seq_len": cfg["ctx"], "mode": mode},
-            "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": "port",
-                             "sample": _sample_desc(cfg, mode, cores)},
+            "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": kind, "sample": sample, **extra},
             "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if port is not None:
+        line["cpu_baseline"]["port_us_per_step"] = port
     print(json.dumps(line), flush=True)
 
 
@@ -424,15 +544,19 @@ def main():
     ap.add_argument("--mode", default=None, choices=["greedy", "stochastic"],
                     help="acceptance mode (default: greedy, c5: stochastic)")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 tcgen05, 2 SIMT")
-    ap.add_argument("--tree", type=int, default=64, choices=[64, 65], help="R = tree rows (63 or 64 drafts + root)")
+    ap.add_argument("--tree", default="64", choices=sorted(TREES),
+                    help="64 / 65: R = 64 / 65 tree rows (63 / 64 drafts + root); chain3 / n8: the HBM-bound "
+                         "contrast trees (R = 4 / 9)")
     ap.add_argument("--splits", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     global TREE
-    TREE = TREE64 + [0] if args.tree == 65 else TREE64
+    TREE = TREES[args.tree]
     cfg = dict(CONFIGS[args.config])
+    if args.tree != "64":
+        cfg["workload"] = cfg["workload"].replace("tree64", {"65": "tree65"}.get(args.tree, f"tree-{args.tree}"))
     mode = args.mode or cfg.get("mode", "greedy")
     accept_only = bool(cfg.get("accept_only"))
     if mode != "greedy" and not accept_only:

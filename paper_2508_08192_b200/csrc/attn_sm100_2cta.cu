@@ -655,6 +655,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
             }
           }
+          if (tr) TRACE(6, gi);
+          if (tr) TRACE(7, gi);
         } else {
           // pass 1: row max over four 32-column chunks, each load overlapped
           // with the max of the previous chunk
@@ -684,6 +686,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
             m_prev = sm.mref[(gi + 2) % 3][i];
           }
+          if (tr) TRACE(6, gi);
+          if (tr) TRACE(7, gi);
           const float m_ref = (n == 0 || mx > m_prev + kRescaleThreshold) ? mx : m_prev;
           m_fix = m_ref;
           if (!kFixRef || N > 1) {
@@ -707,7 +711,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             }
           }
         }
-        if (tr) TRACE(6, gi);
         if (!seen) {
           m_w = m_fix;
           seen = true;

@@ -76,10 +76,11 @@ def _check_greedy_paths(x, acc, raw_parent):
     return float(plen.mean())
 
 
-def _run_bench_step(config, mode="greedy"):
+def _run_bench_step(config, mode="greedy", tree="64"):
     from paper_2508_08192_b200.sharding import shard_for
     from paper_2508_08192_b200.verify import TreeVerifier
 
+    bench.TREE = bench.TREES[tree]
     cfg = bench.CONFIGS[config]
     dev = torch.device("cuda", 0)
     shard = shard_for(0, 1, cfg["Hq"], cfg["Hkv"], cfg["V"])
@@ -119,6 +120,19 @@ def test_c3_bench_step_vs_oracle():
     assert ver._auto_reserve(x, cfg["B"], R, _num_sms(x.q.device)) >= 8
     _check_greedy_paths(x, acc, tuple(bench.TREE))
     _check_slices(cfg, x, aug, out, lse, [(0, 0), (13, 5), (31, 7)])
+
+
+@pytest.mark.parametrize("tree", ["chain3", "n8", "65"])
+def test_c3_other_trees_bench_step_vs_oracle(tree):
+    """The bench's other C3 trees: the HBM-bound contrast trees chain-3
+    (R = 4, R*g = 32 rows per KV head: one part-filled 128-row MMA tile) and
+    N8 (R = 9, R*g = 72), and the R = 65 variant (520 rows per KV head)."""
+    try:
+        cfg, x, R, aug, out, lse, acc = _run_bench_step("c3", tree=tree)
+        _check_greedy_paths(x, acc, tuple(bench.TREE))
+        _check_slices(cfg, x, aug, out, lse, [(0, 0), (17, 6), (31, 7)])
+    finally:
+        bench.TREE = bench.TREE64
 
 
 def test_c4_bench_step_vs_oracle():

@@ -19,7 +19,10 @@
 namespace sdb {
 namespace sm100 {
 
-constexpr int kStagesK = 6;  // K ring: S(n) is issued ~3 items before its PV, so K needs the deeper ring
+#ifndef SDB_STAGES_K
+#define SDB_STAGES_K 6
+#endif
+constexpr int kStagesK = SDB_STAGES_K;  // K ring: S(n) is issued ~3 items before its PV, so K needs the deeper ring
 #ifndef SDB_STAGES_V
 #define SDB_STAGES_V 3
 #endif
@@ -135,7 +138,7 @@ __host__ __device__ constexpr uint32_t make_idesc2(bool b_mn_major) {
          ((uint32_t)(256 >> 4) << 24);
 }
 
-constexpr int kLgStages = kStagesV == 3 ? 5 : 3;  // fused argmax: 8 KB bulk-copy ring in the SMEM left over
+constexpr int kLgStages = kStagesK + kStagesV <= 9 ? 5 : 3;  // fused argmax: 8 KB bulk-copy ring in the SMEM left over
 constexpr int kLgChunk = 2048;   // floats per chunk
 
 struct alignas(1024) Smem2 {
@@ -144,7 +147,8 @@ struct alignas(1024) Smem2 {
   uint8_t v[kStagesV][kHalfBytes];
   uint64_t q_full, q_empty;
   uint64_t k_full[kStagesK], k_empty[kStagesK], v_full[kStagesV], v_empty[kStagesV];
-  uint64_t s_full[3], p_full[3], o_done[3];  // per TMEM S slot
+  uint64_t s_full[3], p_full[3], o_done[3];  // per TMEM S slot (o_done: running-max mode only)
+  uint64_t o_last;  // the unit's last PV done (epilogue may read O)
   uint64_t o_free;
   uint32_t tmem_base;
   float mref[3][128];  // running reference max after each item (log2 units), by slot
@@ -332,6 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       mbar_init(&sm.p_full[s], 2 * 4);  // the 4 warps of the slot's warpgroup in both CTAs
       mbar_init(&sm.o_done[s], 1);
     }
+    mbar_init(&sm.o_last, 1);
     mbar_init(&sm.o_free, 2 * 4 * kSoftmaxWG);
     for (int s = 0; s < kLgStages; ++s) mbar_init(&sm.lg_full[s], 1);
     fence_barrier_init();
@@ -489,7 +494,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             for (int k = 0; k < kTileN / 16; ++k)
               mma2_ts(tm, a + 32 * (k >> 1) + 8 * (k & 1), vd + (uint64_t)((k * 2048) >> 4), idesc_o,
                       (n > 0 || k > 0) ? 1u : 0u);
-            tc_commit2(&sm.o_done[slot]);
+            // O progress is only waited on by a rescale (running-max mode)
+            // and by the unit's epilogue (its last PV)
+            if (!kFixRef) tc_commit2(&sm.o_done[slot]);
+            if (n == N - 1) tc_commit2(&sm.o_last);
             tc_commit2(&sm.v_empty[st]);
           }
           __syncwarp();
@@ -611,7 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const int bar_in = 1 + wg * 4 + lg;                          // max handoff into this warpgroup
     const int bar_out = 1 + ((wg + 1) % kSoftmaxWG) * 4 + lg;   // ... and out of it
     const bool tr = rank == 0 && lg == 0 && lane == 0;
-    uint32_t g_item = 0;
+    uint32_t g_item = 0, g_unit = 0;
     ItemIter iter(sp, worker);
     Item item;
     while (iter.next(sp, item)) {
@@ -779,7 +787,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           : "=r"(any_bad)
           : "r"(bad ? 1u : 0u), "r"(kBarUnit), "r"(kSoftmaxWG * 128)
           : "memory");
-      const uint32_t gl = g_item + N - 1;  // the unit's last item
       // the final reference is the largest one any warpgroup used (the
       // running max only grows; with the fixed reference they are all equal)
       float m_fin = -INFINITY;
@@ -798,7 +805,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
       bad = false;
       asm volatile("bar.sync %0, %1;" ::"r"(kBarUnit), "r"(kSoftmaxWG * 128) : "memory");
-      mbar_wait(&sm.o_done[gl % 3], (gl / 3) & 1);
+      mbar_wait(&sm.o_last, g_unit & 1);
+      ++g_unit;
       tc_fence_after();
       for (int c = wg; c < 4; c += kSoftmaxWG)
         epilogue_chunk(sp, item, geo, g, local, c, tmem + lane_off, m_fin, l_full);

@@ -19,12 +19,15 @@
 namespace sdb {
 namespace sm100 {
 
+// ring depths: C3 attention alone 534 us (K 6 / V 3), 520 (6 / 4), 518 (5 / 5):
+// with the fixed-reference softmax the MMA issuer waited ~580 cycles per
+// item for V with three stages
 #ifndef SDB_STAGES_K
-#define SDB_STAGES_K 6
+#define SDB_STAGES_K 5
 #endif
 constexpr int kStagesK = SDB_STAGES_K;  // K ring: S(n) is issued ~3 items before its PV, so K needs the deeper ring
 #ifndef SDB_STAGES_V
-#define SDB_STAGES_V 3
+#define SDB_STAGES_V 5
 #endif
 constexpr int kStagesV = SDB_STAGES_V;  // (3 suffice: V(n) is consumed by PV(n), ~3 items after its load is issued)
 
@@ -184,10 +187,11 @@ constexpr int kBarUnit = 1 + 4 * kSoftmaxWG;         // named barrier: unit end,
 // m_ref) against that item's row max, with no max pass and no max hand-off
 // (P, O and the row sum are all relative to one reference, so nothing is
 // ever rescaled).  fp32 / bf16 hold 2^127, so exactness only needs the scores
-// to stay below m_ref + kOverflowLog2; a row that exceeds it (a score ~67
-// nats above every score of the piece's first tile) is recomputed exactly.
+// to stay below m_ref + ~89 (log2 units); a row that exceeds it (a score ~60
+// nats above the first 32 scores of the piece's first tile) is recomputed
+// exactly.
 constexpr bool kFixRef = SDB_ATTN_FIXREF != 0;
-constexpr float kOverflowLog2 = 96.f;
+constexpr float kOverflowSum = 0x1p96f;  // an item's row sum above this flags the row (2^89 x 128 terms)
 
 // 32 S values of one row (fp32 bits in r[0..31]) -> P = exp2(s * sl2 - m),
 // packed bf16 into r[0..15]; returns the sum of the 32 probabilities.
@@ -242,9 +246,10 @@ __device__ __forceinline__ float max32(const uint32_t *r) {
   return fmax3(c0, c1, fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31])));
 }
 
-// Epilogue: O columns [32 c, 32 c + 32) of this row normalised by the row sum
+// Epilogue: O columns [16 c, 16 c + 16) of this row normalised by the row sum
 // (bf16 output of a whole unit, fp32 partial of a split one); chunk 0 writes
-// the LSE.
+// the LSE.  Eight 16-column chunks spread 3 / 3 / 2 over the softmax
+// warpgroups (the unit-end drain is on the critical path of the next unit).
 __device__ __forceinline__ void epilogue_chunk(const Sm100Params &sp, const Item &item, const ItemGeo &geo, int g,
                                                int local, int c, uint32_t t_o, float m, float l_full) {
   const TreeAttnParams &p = sp.p;
@@ -255,16 +260,16 @@ __device__ __forceinline__ void epilogue_chunk(const Sm100Params &sp, const Item
   const int hq_idx = geo.kvh * g + (rho % g);
   const float inv = l_full > 0.f ? 1.f / l_full : 0.f;
   const float lse_n = l_full > 0.f ? (m + __log2f(l_full)) * 0.6931471805599453f : -INFINITY;
-  uint32_t r[32];
-  SDB_TMEM_LD32(t_o + 32 * c, r);
+  uint32_t r[16];
+  SDB_TMEM_LD16(t_o + 16 * c, r);
   tmem_wait_ld();
-  const int col0 = 32 * c;
+  const int col0 = 16 * c;
   if (item.whole) {
     if (in_range) {
       __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(p.out) +
                          (((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim + col0;
 #pragma unroll
-      for (int e = 0; e < 32; e += 8) {
+      for (int e = 0; e < 16; e += 8) {
         uint4 v;
         if (row_ok) {
           v.x = pack_bf16(__uint_as_float(r[e + 0]) * inv, __uint_as_float(r[e + 1]) * inv);
@@ -282,7 +287,7 @@ __device__ __forceinline__ void epilogue_chunk(const Sm100Params &sp, const Item
   } else {
     float *o = sp.part_out + ((int64_t)item.slot * sp.rows_unit + local) * kHeadDim + col0;
 #pragma unroll
-    for (int e = 0; e < 32; e += 4)
+    for (int e = 0; e < 16; e += 4)
       *reinterpret_cast<float4 *>(o + e) = make_float4(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv,
                                                        __uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
     if (c == 0) sp.part_lse[(int64_t)item.slot * sp.rows_unit + local] = row_ok ? lse_n : -INFINITY;
@@ -469,6 +474,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                       kd + (uint64_t)(((k >> 2) * kKChunk + (k & 3) * 32) >> 4), idesc_s, k > 0);
             tc_commit2(&sm.s_full[slot]);
             tc_commit2(&sm.k_empty[st]);
+            // the unit's last S: Q is free once it completes, so the next
+            // unit's Q load overlaps this unit's last three items
+            if (n == N - 1) tc_commit2(&sm.q_empty);
           }
           __syncwarp();
         };
@@ -504,8 +512,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (n + 3 < N) issue_s(n + 3);
           TRACE(2, gi);
         }
-        if (elect_one()) tc_commit2(&sm.q_empty);
-        __syncwarp();
         g_tile += N;
         g_item += N;
         ++g_q;
@@ -647,6 +653,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         tc_fence_after();
         if (tr) TRACE(4, gi);
         const uint32_t t_s = tmem + lane_off + kSBase + slot * 128;
+        // a warp whose 32 rows are all padding (the short last row block of
+        // R = 65: 520 rows per KV head) skips the softmax: its P rows only
+        // feed O rows that are never stored.  It still waits for S (one phase
+        // per item) and arrives on p_full, and its chain partners (same lane
+        // group, other warpgroups) skip the hand-off alike.
+        const bool pad_warp = geo.row0 + (int)rank * kTileM + lg * 32 >= geo.rows_total;
+        if (!pad_warp) {
         uint32_t vm[4] = {~0u, ~0u, ~0u, ~0u};
         if (!full) {
 #pragma unroll
@@ -671,9 +684,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           uint32_t r[32], r2[32];
           SDB_TMEM_LD32(t_s + 0, r2);
           SDB_TMEM_WAIT_LD_REGS(r2);
-          SDB_TMEM_LD32(t_s + 32, r);
+          if (!kFixRef) SDB_TMEM_LD32(t_s + 32, r);
           if (!full) apply_mask32(r2, vm[0]);
           float mx = max32(r2);
+          if (kFixRef) {
+            // fixed reference: the row max of the first 32 keys of the
+            // piece's first tile is enough (anything above it by less than
+            // ~89 log2 units stays exact), so the hand-off leaves right away
+            mx *= sl2;
+          } else {
           SDB_TMEM_WAIT_LD_REGS(r);
           SDB_TMEM_LD32(t_s + 64, r2);
           if (!full) apply_mask32(r, vm[1]);
@@ -686,11 +705,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (!full) apply_mask32(r, vm[3]);
           mx = fmaxf(mx, max32(r));
           mx *= sl2;
+          }
           // reference max chain (lazy: moves only when the max grows by > 2^8);
           // with the fixed reference only the unit's first item gets here and
           // hands its max to the second
           float m_prev = -INFINITY;
-          if (!kFixRef && gi > 0) {
+          if (!kFixRef && n > 0) {
             asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
             m_prev = sm.mref[(gi + 2) % 3][i];
           }
@@ -698,7 +718,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (tr) TRACE(7, gi);
           const float m_ref = (n == 0 || mx > m_prev + kRescaleThreshold) ? mx : m_prev;
           m_fix = m_ref;
-          if (!kFixRef || N > 1) {
+          if (n + 1 < N) {  // hand-offs pair up within the unit
             sm.mref[slot][i] = m_ref;
             asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
           }
@@ -731,7 +751,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           // [32c, 32c + 16) of the slot -- inside the chunk's own, already
           // loaded S columns; each load overlapped with the previous
           // chunk's exps.  The row max of the item is tracked on the side:
-          // with the fixed reference, a score above m_ref + kOverflowLog2
+          // with the fixed reference, a score ~89 log2 units above m_ref
           // (or a visible key in a row whose reference is -inf) flags the
           // row for the exact recompute.
           const float neg_mu = (m_fix == -INFINITY) ? 0.f : -m_fix;
@@ -741,29 +761,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           SDB_TMEM_WAIT_LD_REGS(r2);
           SDB_TMEM_LD32(t_s + 32, r);
           if (!full) apply_mask32(r2, vm[0]);
-          float mo = kFixRef ? max32(r2) : 0.f;
           float rs = exp_pack32<EMU8>(r2, sc2, nm2);
           SDB_TMEM_ST16(t_s + 0, r2);
           SDB_TMEM_WAIT_LD_REGS(r);
           SDB_TMEM_LD32(t_s + 64, r2);
           if (!full) apply_mask32(r, vm[1]);
-          if (kFixRef) mo = fmaxf(mo, max32(r));
           rs += exp_pack32<EMU8>(r, sc2, nm2);
           SDB_TMEM_ST16(t_s + 32, r);
           SDB_TMEM_WAIT_LD_REGS(r2);
           SDB_TMEM_LD32(t_s + 96, r);
           if (!full) apply_mask32(r2, vm[2]);
-          if (kFixRef) mo = fmaxf(mo, max32(r2));
           rs += exp_pack32<EMU8>(r2, sc2, nm2);
           SDB_TMEM_ST16(t_s + 64, r2);
           SDB_TMEM_WAIT_LD_REGS(r);
           if (!full) apply_mask32(r, vm[3]);
-          if (kFixRef) mo = fmaxf(mo, max32(r));
           rs += exp_pack32<EMU8>(r, sc2, nm2);
           SDB_TMEM_ST16(t_s + 96, r);
           l_w += rs;
-          if (kFixRef) bad |= mo * sl2 > m_fix + kOverflowLog2;
+          // a score ~89 log2 units above the reference shows in the item's sum
+          // (an exp2 that overflowed is +inf; 128 terms cannot reach 2^96
+          // otherwise unless one of them is within 7 of the limit), and a
+          // visible key in a row whose reference is -inf gives a positive sum
+          if (kFixRef) bad |= rs > kOverflowSum || (m_fix == -INFINITY && rs > 0.f);
         }
+        }  // !pad_warp
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -808,7 +829,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       mbar_wait(&sm.o_last, g_unit & 1);
       ++g_unit;
       tc_fence_after();
-      for (int c = wg; c < 4; c += kSoftmaxWG)
+      for (int c = wg; c < 8; c += kSoftmaxWG)
         epilogue_chunk(sp, item, geo, g, local, c, tmem + lane_off, m_fin, l_full);
       tc_fence_before();
       __syncwarp();

@@ -148,6 +148,8 @@ def make_inputs(cfg, shard, device, seed=0, mode="greedy"):
     nb = B * pages + 8
     # identical page permutation on every rank (same block table)
     perm = torch.randperm(nb, generator=torch.Generator().manual_seed(seed + 1)).to(torch.int32)
+    if os.environ.get("SDB_BENCH_PAGES") == "seq":  # A/B: each sequence's pages contiguous in the pool
+        perm = torch.arange(nb, dtype=torch.int32)
     table = perm[:B * pages].reshape(B, pages).to(device)
 
     def randn(*shape, dtype=torch.bfloat16, std=1.0, gen=g):

@@ -88,12 +88,17 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
 
   if (warp == 0) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
-      tma_prefetch(&tm_q);
-      tma_prefetch(&tm_k);
-      tma_prefetch(&tm_v);
-      tma_prefetch(&tm_tk);
-      tma_prefetch(&tm_tv);
+    // Whole warp walks the schedule; block-table entries of the next 32 pages
+    // come from one coalesced load by the 32 lanes (shuffled to the issuing
+    // lane), so no TMA issue waits for a dependent global load.
+    {
+      if (lane == 0) {
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+        tma_prefetch(&tm_tk);
+        tma_prefetch(&tm_tv);
+      }
       const int bs = p.block_size;
       const int seg_rows = bs < 64 ? bs : 64;  // pool TMA box rows
       uint32_t g_tile = 0, g_q = 0;
@@ -104,16 +109,27 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
         if (!geo.active) continue;
         // Q tiles of this unit once the previous unit's S MMAs are done
         mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
-        mbar_expect_tx(&sm.q_full, NT * kTileBytes);
-        for (int t = 0; t < NT; ++t) {
-          const int node0 = geo.q0 + (geo.row0 + t * kTileM) / g;
-          for (int c = 0; c < 2; ++c)
-            tma_load_4d(sm.q[t] + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, 0, geo.kvh,
-                        geo.b * p.r_max + node0);
+        if (lane == 0) {
+          mbar_expect_tx(&sm.q_full, NT * kTileBytes);
+          for (int t = 0; t < NT; ++t) {
+            const int node0 = geo.q0 + (geo.row0 + t * kTileM) / g;
+            for (int c = 0; c < 2; ++c)
+              tma_load_4d(sm.q[t] + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, 0, geo.kvh,
+                          geo.b * p.r_max + node0);
+          }
         }
         ++g_q;
         const int n_valid_pages = (geo.C + bs - 1) / bs;
         const int32_t *bt = p.block_table + (int64_t)geo.b * p.max_blocks;
+        int pc_base = -64, pc_val = 0;  // lane l holds the page of logical block pc_base + l
+        auto page_of = [&](int lp) {
+          if (lp < pc_base || lp >= pc_base + 32) {  // warp-uniform
+            pc_base = lp & ~31;
+            const int e = pc_base + lane;
+            pc_val = e < n_valid_pages ? __ldg(bt + e) : p.num_blocks;  // OOB page -> zero fill
+          }
+          return __shfl_sync(0xffffffffu, pc_val, lp - pc_base);
+        };
         for (int it = 0; it < geo.n_tiles; ++it, ++g_tile) {
           const int s = g_tile & 1;
           const uint32_t ph = (g_tile >> 1) & 1;
@@ -124,17 +140,17 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
             uint64_t *ful = kv ? &sm.v_full[s] : &sm.k_full[s];
             uint8_t *dst = kv ? sm.v[s] : sm.k[s];
             mbar_wait(emp, ph ^ 1);
-            mbar_expect_tx(ful, kTileBytes);
+            if (lane == 0) mbar_expect_tx(ful, kTileBytes);
             if (pref) {
               const CUtensorMap *m = kv ? &tm_v : &tm_k;
               for (int r0 = 0; r0 < kTileN; r0 += seg_rows) {
                 const int key = geo.k0 + tile * kTileN + r0;
-                const int lp = key / bs;
-                const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;  // OOB page -> zero fill
+                const int page = page_of(key / bs);
                 const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
-                for (int c = 0; c < 2; ++c) tma_load_2d(dst + c * kChunkBytes + r0 * 128, m, ful, c * 64, rowc);
+                if (lane == 0)
+                  for (int c = 0; c < 2; ++c) tma_load_2d(dst + c * kChunkBytes + r0 * 128, m, ful, c * 64, rowc);
               }
-            } else {
+            } else if (lane == 0) {
               const CUtensorMap *m = kv ? &tm_tv : &tm_tk;
               for (int c = 0; c < 2; ++c)
                 tma_load_3d(dst + c * kChunkBytes, m, ful, c * 64, geo.kvh, geo.b * p.r_max + tile * kTileN);

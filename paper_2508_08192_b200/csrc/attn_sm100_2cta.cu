@@ -33,7 +33,7 @@ constexpr int kStagesV = SDB_STAGES_V;  // (3 suffice: V(n) is consumed by PV(n)
 
 #ifdef SDB_TRACE
 // [event][iteration] clock64 stamps of worker 0 (debug builds only)
-__device__ unsigned long long g_trace[16][256];
+__device__ unsigned long long g_trace[24][256];
 #define TRACE(ev, it)                                                                   \
   do {                                                                                  \
     if (worker == 0 && (it) < 256) g_trace[ev][it] = clock64();                         \
@@ -364,16 +364,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // ============ TMA producers (both CTAs): warp 0 Q + K ring, warp 2 V ring ============
     // Each CTA loads its own half of every tile; completion bytes land on the
     // leader's barriers.  Separate K and V producers so a K load never waits
-    // behind a V slot (and vice versa).
-    if (lane == 0) {
+    // behind a V slot (and vice versa).  The whole warp walks the schedule:
+    // the block-table entries of the next 32 pages are fetched by the 32 lanes
+    // in one coalesced load and handed to the issuing lane by shuffles, so a
+    // tile's TMA issue never waits for a dependent global load (with one
+    // block-table load per page on the issuing lane, the V producer's two
+    // serial loads per tile took longer than the tile's tensor work).
+    {
       const bool kprod = warp == 0;
-      if (kprod) {
-        tma_prefetch(&tm_q);
-        tma_prefetch(&tm_k);
-        tma_prefetch(&tm_tk);
-      } else {
-        tma_prefetch(&tm_v);
-        tma_prefetch(&tm_tv);
+      if (lane == 0) {
+        if (kprod) {
+          tma_prefetch(&tm_q);
+          tma_prefetch(&tm_k);
+          tma_prefetch(&tm_tk);
+        } else {
+          tma_prefetch(&tm_v);
+          tma_prefetch(&tm_tv);
+        }
       }
       const int bs = p.block_size;
       const int seg_rows = bs < 64 ? bs : 64;
@@ -386,14 +393,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         if (!geo.active) continue;
         if (kprod) {
           mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
-          if (rank == 0) mbar_expect_tx(&sm.q_full, 2 * kTileBytes);
-          const int node0 = geo.q0 + (geo.row0 + (int)rank * kTileM) / g;
-          for (int c = 0; c < 2; ++c)
-            tma2_4d(sm.q + c * kChunkBytes, &tm_q, l_qfull, c * 64, 0, geo.kvh, geo.b * p.r_max + node0);
+          if (lane == 0) {
+            if (rank == 0) mbar_expect_tx(&sm.q_full, 2 * kTileBytes);
+            const int node0 = geo.q0 + (geo.row0 + (int)rank * kTileM) / g;
+            for (int c = 0; c < 2; ++c)
+              tma2_4d(sm.q + c * kChunkBytes, &tm_q, l_qfull, c * 64, 0, geo.kvh, geo.b * p.r_max + node0);
+          }
         }
         ++g_q;
         const int n_valid_pages = (geo.C + bs - 1) / bs;
         const int32_t *bt = p.block_table + (int64_t)geo.b * p.max_blocks;
+        int pc_base = -64, pc_val = 0;  // lane l holds the page of logical block pc_base + l
+        auto page_of = [&](int lp) {
+          if (lp < pc_base || lp >= pc_base + 32) {  // warp-uniform
+            pc_base = lp & ~31;
+            const int e = pc_base + lane;
+            pc_val = e < n_valid_pages ? __ldg(bt + e) : p.num_blocks;  // OOB page -> zero fill
+          }
+          return __shfl_sync(0xffffffffu, pc_val, lp - pc_base);
+        };
         for (int it = 0; it < geo.n_tiles; ++it, ++g_tile) {
           const bool pref = it < geo.n_pref;
           const int tile = pref ? geo.pa + it : geo.sa + (it - geo.n_pref);
@@ -401,17 +419,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             // K half: keys [tile*128 + rank*64, +64), all 128 head-dim columns
             const int s = g_tile % kStagesK;
             mbar_wait(&sm.k_empty[s], ((g_tile / kStagesK) & 1) ^ 1);
-            if (rank == 0) mbar_expect_tx(&sm.k_full[s], 2 * kHalfBytes);
+            if (rank == 0 && lane == 0) TRACE(17, g_tile);
             const uint32_t l_kfull = leader_addr(&sm.k_full[s]);
+            if (lane == 0 && rank == 0) mbar_expect_tx(&sm.k_full[s], 2 * kHalfBytes);
             if (pref) {
               for (int r0 = 0; r0 < 64; r0 += seg_rows) {
                 const int key = geo.k0 + tile * kTileN + (int)rank * 64 + r0;
-                const int lp = key / bs;
-                const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;  // OOB page -> zero fill
+                const int page = page_of(key / bs);
                 const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
-                for (int c = 0; c < 2; ++c) tma2_2d(sm.k[s] + c * kKChunk + r0 * 128, &tm_k, l_kfull, c * 64, rowc);
+                if (lane == 0)
+                  for (int c = 0; c < 2; ++c) tma2_2d(sm.k[s] + c * kKChunk + r0 * 128, &tm_k, l_kfull, c * 64, rowc);
               }
-            } else {
+            } else if (lane == 0) {
               for (int c = 0; c < 2; ++c)
                 tma2_3d(sm.k[s] + c * kKChunk, &tm_tk, l_kfull, c * 64, geo.kvh,
                         geo.b * p.r_max + tile * kTileN + (int)rank * 64);
@@ -420,17 +439,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             // V half: all 128 keys, head-dim columns [rank*64, +64)
             const int s = g_tile % kStagesV;
             mbar_wait(&sm.v_empty[s], ((g_tile / kStagesV) & 1) ^ 1);
-            if (rank == 0) mbar_expect_tx(&sm.v_full[s], 2 * kHalfBytes);
+            if (rank == 0 && lane == 0) TRACE(16, g_tile);
             const uint32_t l_vfull = leader_addr(&sm.v_full[s]);
+            if (lane == 0 && rank == 0) mbar_expect_tx(&sm.v_full[s], 2 * kHalfBytes);
             if (pref) {
               for (int r0 = 0; r0 < kTileN; r0 += seg_rows) {
                 const int key = geo.k0 + tile * kTileN + r0;
-                const int lp = key / bs;
-                const int page = lp < n_valid_pages ? bt[lp] : p.num_blocks;
+                const int page = page_of(key / bs);
                 const int rowc = (page * p.hkv + geo.kvh) * bs + key % bs;
-                tma2_2d(sm.v[s] + r0 * 128, &tm_v, l_vfull, (int)rank * 64, rowc);
+                if (lane == 0) tma2_2d(sm.v[s] + r0 * 128, &tm_v, l_vfull, (int)rank * 64, rowc);
               }
-            } else {
+            } else if (lane == 0) {
               tma2_3d(sm.v[s], &tm_tv, l_vfull, (int)rank * 64, geo.kvh, geo.b * p.r_max + tile * kTileN);
             }
           }
@@ -488,6 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int st = gt % kStagesV;
           const uint32_t gi = g_item + n;
           const int slot = gi % 3;
+          TRACE(18, gi);
           mbar_wait(&sm.v_full[st], (gt / kStagesV) & 1);
           TRACE(0, gi);
           mbar_wait_cluster(&sm.p_full[slot], (gi / 3) & 1);
@@ -524,6 +544,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // the TMA engine streams each row through a 3 x 8 KB shared ring while
     // the tensor pipe runs the attention, so the HBM-bound acceptance scan
     // uses the attention's spare memory bandwidth instead of its own launch.
+#ifdef SDB_TRACE
+    // trace builds: watch the tensor pipe of worker 0 (completion of S(n) via
+    // s_full, of PV(n) via v_empty) from this otherwise idle warp; completion
+    // order inside the first unit: S0 S1 S2 PV0 S3 PV1 S4 ...
+    if (!p.fa_logits && worker == 0 && rank == 0 && lane == 0) {
+      for (int gi = 0; gi < 3; ++gi) {
+        mbar_wait(&sm.s_full[gi % 3], (gi / 3) & 1);
+        TRACE(19, gi);
+      }
+      for (int n = 0; n + 3 < 60; ++n) {
+        mbar_wait(&sm.v_empty[n % kStagesV], (n / kStagesV) & 1);
+        TRACE(20, n);
+        mbar_wait(&sm.s_full[(n + 3) % 3], ((n + 3) / 3) & 1);
+        TRACE(19, n + 3);
+      }
+    }
+#endif
     if (p.fa_logits) {
       griddep_wait();  // logits may come from the kernel launched just before
       const int nrows = p.batch * p.r_max;

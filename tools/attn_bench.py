@@ -39,6 +39,8 @@ for _ in range(3):
     call()
 torch.cuda.synchronize()
 times = []
+clk = bench.ClockSampler(0)
+clk.__enter__()
 for _ in range(args.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -47,6 +49,7 @@ for _ in range(args.reps):
     e1.record()
     torch.cuda.synchronize()
     times.append(e0.elapsed_time(e1) / args.iters)
+clk.__exit__()
 ms = statistics.median(times)
 from oracle import specdec_oracle as O  # noqa: E402  (mask popcount only)
 
@@ -54,4 +57,4 @@ anc = int(O.suffix_mask(tuple(bench._augment(bench.TREE64))).sum())
 _, _, flops = bench.step_bytes_flops(cfg, shard, R, anc)
 print(json.dumps({"config": args.config, "gpus": args.gpus, "kernel": args.kernel, "ctas": args.ctas,
                   "emu": os.environ.get("SDB_ATTN_EMU", "default"), "ms": ms, "tflops": flops / ms / 1e9,
-                  "spread": [min(times), max(times)]}))
+                  "spread": [min(times), max(times)], "clocks": clk.summary()}))

@@ -106,6 +106,95 @@ __global__ void k_f16path(float *out, long long *cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+
+// F2FP: cvt.rn.bf16x2.f32 alone (8 independent chains)
+__global__ void k_cvt(float *out, long long *cyc) {
+  float a[8];
+  uint32_t pk = 0;
+  for (int i = 0; i < 8; ++i) a[i] = -0.001f * (threadIdx.x + i);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t r;
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[i]), "f"(a[(i + 1) & 7]));
+      pk ^= r;
+      a[i] = __uint_as_float(__float_as_uint(a[i]) ^ (r & 1u));
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a[0] + pk;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+// the softmax mix per element pair: FFMA2 scale, 2 x MUFU.EX2, F2FP pack, FADD2 sum
+__global__ void k_mix(float *out, long long *cyc) {
+  float a[16];
+  for (int i = 0; i < 16; ++i) a[i] = -0.001f * (threadIdx.x + i);
+  uint64_t acc = 0;
+  uint32_t pk = 0;
+  const uint64_t sc = (uint64_t)__float_as_uint(0.125f) | ((uint64_t)__float_as_uint(0.125f) << 32);
+  const uint64_t nm = (uint64_t)__float_as_uint(-1.f) | ((uint64_t)__float_as_uint(-1.f) << 32);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 2; ++it) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      uint64_t x;
+      asm volatile("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a[2 * e]), "f"(a[2 * e + 1]));
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x) : "l"(sc), "l"(nm));
+      float x0, x1, p0, p1;
+      asm volatile("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(x));
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(x0));
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(x1));
+      uint32_t r;
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(p1), "f"(p0));
+      pk ^= r;
+      uint64_t pp;
+      asm volatile("mov.b64 %0, {%1, %2};" : "=l"(pp) : "f"(p0), "f"(p1));
+      asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pp));
+      a[2 * e] = p0;
+      a[2 * e + 1] = p1;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __uint_as_float((uint32_t)acc) + pk;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+// same mix without the F2FP pack
+__global__ void k_mix_nocvt(float *out, long long *cyc) {
+  float a[16];
+  for (int i = 0; i < 16; ++i) a[i] = -0.001f * (threadIdx.x + i);
+  uint64_t acc = 0;
+  const uint64_t sc = (uint64_t)__float_as_uint(0.125f) | ((uint64_t)__float_as_uint(0.125f) << 32);
+  const uint64_t nm = (uint64_t)__float_as_uint(-1.f) | ((uint64_t)__float_as_uint(-1.f) << 32);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 2; ++it) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      uint64_t x;
+      asm volatile("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a[2 * e]), "f"(a[2 * e + 1]));
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x) : "l"(sc), "l"(nm));
+      float x0, x1, p0, p1;
+      asm volatile("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(x));
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(x0));
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(x1));
+      uint64_t pp;
+      asm volatile("mov.b64 %0, {%1, %2};" : "=l"(pp) : "f"(p0), "f"(p1));
+      asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pp));
+      a[2 * e] = p0;
+      a[2 * e + 1] = p1;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __uint_as_float((uint32_t)acc);
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 template <typename K>
 void run(const char *name, K kern, double results_per_thread_iter, int threads) {
   float *out;
@@ -133,6 +222,9 @@ int main() {
     run("ex2.bf16x2", k_bf16x2, 16, t);
     run("ffma2", k_ffma2, 16, t);
     run("f16path", k_f16path, 16, t);
+    run("cvt.bf16x2", k_cvt, 8, t);
+    run("mix", k_mix, 8, t);
+    run("mix-nocvt", k_mix_nocvt, 8, t);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

@@ -15,7 +15,9 @@ from paper_2508_08192_b200.attention import TreeVerifyAttention  # noqa: E402
 from paper_2508_08192_b200.drafttree import tree_build  # noqa: E402
 from paper_2508_08192_b200.sharding import shard_for  # noqa: E402
 
-cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"]
+cfg = dict(bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"])
+if os.environ.get("TRACE_B"):
+    cfg["B"] = int(os.environ["TRACE_B"])
 lib = _lib.load()
 dev = torch.device("cuda", 0)
 shard = shard_for(0, 1, cfg["Hq"], cfg["Hkv"], cfg["V"])
@@ -24,9 +26,9 @@ mask, _, _, _ = tree_build(x.parent, x.n_rows, x.ctx_len)
 attn = TreeVerifyAttention()
 for _ in range(3):
     attn(x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, mask, x.n_rows, cfg["d"] ** -0.5,
-         max_ctx=cfg["ctx"], kernel=1)
+         max_ctx=cfg["ctx"], kernel=1, num_splits=int(os.environ.get("TRACE_CTAS", "0")))
 torch.cuda.synchronize()
-buf = np.zeros((16, 256), dtype=np.uint64)
+buf = np.zeros((24, 256), dtype=np.uint64)
 fn = lib.sdb_debug_trace
 fn.argtypes = [ctypes.c_void_p]
 assert fn(buf.ctypes.data) == 0
@@ -47,10 +49,35 @@ print("mma PV+S issue (pok->issued): median", np.median(b[2, it] - b[1, it]))
 print("P arrive -> mma sees it: median", np.median(b[1, it] - b[5, it]))
 print("mma issued(n) -> pwait(n+1) (V wait + loop): median", np.median(b[0, it + 1] - b[2, it]))
 per = b[:, it]
+if buf[19, 5]:
+    k = np.arange(8, 50)
+    print("tensor pipe: PV(n) done -> S(n+3) done: median", np.median(b[19, k + 3] - b[20, k]))
+    print("tensor pipe: S(n+3) done -> PV(n+1) done: median", np.median(b[20, k + 1] - b[19, k + 3]))
+    print("tensor pipe: PV(n) issue start (P seen) -> PV(n) done: median", np.median(b[20, k] - b[1, k]))
+    print("tensor pipe: S(n+3) issued -> S(n+3) done: median", np.median(b[19, k + 3] - b[2, k]))
+    print("tensor pipe: S(n) done -> softmax sees it: median", np.median(b[4, k] - b[19, k]))
+    k5 = np.arange(8, 50)
+    print("V(n+5) TMA issue - PV(n) done (slot reuse gate): median", np.median(b[16, k5 + 5] - b[20, k5]))
+    print("V(n) TMA issue -> PV(n) issue start: median", np.median(b[1, k5] - b[16, k5]))
+if os.environ.get("TRACE_ROWS"):
+    print("item: Vwait(18->0) Pwait(0->1) issue(1->2) loop(2->18') | sm: swait sok->done | S(n+3) lat")
+    for k in range(8, 40):
+        print(k, b[0, k] - b[18, k], b[1, k] - b[0, k], b[2, k] - b[1, k], b[18, k + 1] - b[2, k], "|",
+              b[4, k] - b[3, k], b[5, k] - b[4, k], "|", b[4, k + 3] - b[2, k])
+it3 = np.arange(8, min(n, 200) - 3)
+print("S(n+3) issued (after PV(n)) -> softmax sees S(n+3): median", np.median(b[4, it3 + 3] - b[2, it3]))
+print("P(n) arrived -> softmax sees S(n+3): median", np.median(b[4, it3 + 3] - b[5, it3]))
+if buf[16, 8]:
+    print("V TMA issued -> MMA sees v_full: median", np.median(b[0, it] - b[16, it]))
+    print("V TMA issued ahead of the MMA's V wait: median", np.median(b[18, it] - b[16, it]))
+    print("MMA V wait (v_full): median", np.median(b[0, it] - b[18, it]))
+    print("K TMA issue period: median", np.median(np.diff(b[17, 8:min(n, 200)])))
+    print("V TMA issue period: median", np.median(np.diff(b[16, 8:min(n, 200)])))
 print("period mma: median", np.median(np.diff(b[1, 8:min(n, 200)])))
-print("softmax: S ready -> max pass done: median", np.median(b[6, it] - b[4, it]))
-print("softmax: max done -> chain ok: median", np.median(b[7, it] - b[6, it]))
-print("softmax: chain ok -> P arrived: median", np.median(b[5, it] - b[7, it]))
+print("softmax: S ready -> first chunk loaded: median", np.median(b[6, it] - b[4, it]))
+print("softmax: chunk 0 loaded -> chunks 0, 1 exp'd: median", np.median(b[7, it] - b[6, it]))
+print("softmax: chunks 2, 3 exp'd: median", np.median(b[15, it] - b[7, it]))
+print("softmax: last store -> P arrived (wait::st, fence, arrive): median", np.median(b[5, it] - b[15, it]))
 # kernel-level phases of worker 0 (clock64 of its SM)
 e8 = int(buf[8, 0])
 if e8:

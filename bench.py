@@ -781,7 +781,7 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
-            traffic = json.load(f).get(f"{args.config}:{mode}:g{world}")
+            traffic = json.load(f).get(f"{args.config}:{mode}:g{world}" + ("" if args.tree == "64" else f":{args.tree}"))
     except Exception:
         pass
     gbs = step_bytes_all / (ms * 1e-3) / 1e9

@@ -34,9 +34,12 @@ constexpr int kStagesV = SDB_STAGES_V;  // (3 suffice: V(n) is consumed by PV(n)
 #ifdef SDB_TRACE
 // [event][iteration] clock64 stamps of worker 0 (debug builds only)
 __device__ unsigned long long g_trace[24][256];
+#ifndef SDB_TRACE_WORKER
+#define SDB_TRACE_WORKER 0
+#endif
 #define TRACE(ev, it)                                                                   \
   do {                                                                                  \
-    if (worker == 0 && (it) < 256) g_trace[ev][it] = clock64();                         \
+    if (worker == SDB_TRACE_WORKER && (it) < 256) g_trace[ev][it] = clock64();          \
   } while (0)
 // [event][worker] globaltimer stamps of every worker
 #define TRACE_G(ev)                                                                     \
@@ -548,7 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // trace builds: watch the tensor pipe of worker 0 (completion of S(n) via
     // s_full, of PV(n) via v_empty) from this otherwise idle warp; completion
     // order inside the first unit: S0 S1 S2 PV0 S3 PV1 S4 ...
-    if (!p.fa_logits && worker == 0 && rank == 0 && lane == 0) {
+    if (!p.fa_logits && worker == SDB_TRACE_WORKER && rank == 0 && lane == 0) {
       for (int gi = 0; gi < 3; ++gi) {
         mbar_wait(&sm.s_full[gi % 3], (gi / 3) & 1);
         TRACE(19, gi);

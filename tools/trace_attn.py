@@ -16,6 +16,8 @@ from paper_2508_08192_b200.drafttree import tree_build  # noqa: E402
 from paper_2508_08192_b200.sharding import shard_for  # noqa: E402
 
 cfg = dict(bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"])
+if os.environ.get("TRACE_TREE"):
+    bench.TREE = bench.TREES[os.environ["TRACE_TREE"]]
 if os.environ.get("TRACE_B"):
     cfg["B"] = int(os.environ["TRACE_B"])
 lib = _lib.load()

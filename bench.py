@@ -405,58 +405,139 @@ def _sample_desc(cfg, mode, cores):
     return f"{att}{acc} for 1 sequence x{cfg['B']}; numpy float64 oracle port, {cores} BLAS threads, extrapolated"
 
 
-def run_reference(args, cfg, mode):
-    """--impl reference: the reference's own CPU implementation of the path
-    (stock specdec from baseline/_ref when installed, else the numpy port),
-    rank 0 only, all host cores.  Each step is a bounded sample -- one
-    sequence x one KV-head group of the attention, one sequence of acceptance
-    -- extrapolated exactly to the batch (the reference loops sequences one
-    after another, engine.py:581-582; attention is per KV head).  The measured
-    sample seconds and the extrapolation factors are reported separately."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    # all host cores for the numpy/BLAS reference (torchrun exports OMP_NUM_THREADS=1)
+_REF = {}
+
+
+def _ref_worker_init(cfg, mode, tree, seed):
+    """Pool worker: one BLAS thread, the stock reference imported, one unit's
+    inputs drawn once (the reference's cost does not depend on the values)."""
+    import numpy as np
+
     try:
         from threadpoolctl import threadpool_limits
 
-        threadpool_limits(os.cpu_count() or 1)
+        threadpool_limits(1)
     except Exception:  # noqa: BLE001 - threadpoolctl is optional
         pass
-    cores = blas_threads()
+    global TREE
+    TREE = tree
+    ref = load_reference()
+    ref.kernels.set_backend(_REF.get("backend", "numpy"))
+    rng = np.random.default_rng(seed)
+    Hq, Hkv, d, C, V = (cfg[k] for k in ("Hq", "Hkv", "d", "ctx", "V"))
+    g = Hq // Hkv
+    spec = ref.drafttree.TreeSpec(tuple(tree))
+    aug = ref.engine._augment(spec)
+    R = aug.n_nodes
+    st = {"ref": ref, "aug": aug, "spec": spec, "g": g, "d": d, "mode": mode, "seed": seed}
+    if not cfg.get("accept_only"):
+        def bf(x):
+            return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+        st["q"] = bf(rng.normal(size=(R, g * d)))
+        st["ck"] = np.repeat(bf(rng.normal(size=(C, 1, d))), g, axis=1).reshape(C, g * d)
+        st["cv"] = np.repeat(bf(rng.normal(size=(C, 1, d))), g, axis=1).reshape(C, g * d)
+        st["tk"] = np.repeat(bf(rng.normal(size=(R, 1, d))), g, axis=1).reshape(R, g * d)
+        st["tv"] = np.repeat(bf(rng.normal(size=(R, 1, d))), g, axis=1).reshape(R, g * d)
+    st["logits"] = (2.0 * rng.normal(size=(R, V))).astype(np.float32).astype(np.float64)
+    st["draft"] = st["logits"] + 0.5 * rng.normal(size=(R, V))
+    st["tokens"] = tuple(int(t) for t in rng.integers(V, size=spec.n_nodes))
+    _REF.update(st)
+
+
+def _ref_attn_unit(_i):
+    """One (sequence, KV head) unit of the stock tree attention
+    (specdec.attention.tree_attention, attention.py:131-151)."""
+    s = _REF
+    s["ref"].attention.tree_attention(s["q"], s["ck"], s["cv"], s["tk"], s["tv"], s["aug"], s["d"] ** -0.5,
+                                      n_heads=s["g"])
+    return 0
+
+
+def _ref_accept_seq(_i):
+    """One sequence of stock acceptance: target_dist of every row, the draft
+    q of every parent row, mss_verify (sampling.py:87-202)."""
+    s = _REF
+    ref, aug, spec = s["ref"], s["aug"], s["spec"]
+    T, top_p = (0.0, 1.0) if s["mode"] == "greedy" else (TEMPERATURE, TOP_P)
+    tdists = [ref.sampling.target_dist(s["logits"][i], T, top_p) for i in range(aug.n_nodes)]
+    qrow = {p_: ref.sampling.target_dist(s["draft"][p_], T, 1.0) for p_ in set(aug.parent[1:])}
+    node_dists = tuple(qrow[aug.parent[1 + c]] for c in range(spec.n_nodes))
+    res = ref.sampling.mss_verify(ref.sampling.DraftResult(spec, s["tokens"], node_dists), tdists,
+                                  ref.sampling.rank_sliced_uniforms(s["seed"], 16, 1, aug.n_nodes + 1)[0],
+                                  "greedy_children" if s["mode"] == "greedy" else "stochastic")
+    return len(res.accepted_path)
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, mode):
+    """--impl reference: the reference's own CPU implementation of the path
+    (stock specdec from baseline/_ref; the numpy oracle port when it is not
+    installed), rank 0 only, every host core: a pool of one-BLAS-thread
+    processes runs the step's (sequence, KV head) attention units and its
+    sequences' acceptance -- the reference loops them independently
+    (engine.py:581-582; attention per KV head), so the pool's wall time is
+    the reference's best multi-core step.  A step is the whole workload
+    unless that would exceed ~3 s of wall time; then a fixed share of the
+    units per step, scaled to the whole batch (reported as sample_fraction)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = _host_cores()
     f_attn = 0 if cfg.get("accept_only") else cfg["B"] * cfg["Hkv"]
     f_acc = cfg["B"]
     ref = load_reference()
     port = None
     if ref is not None:
-        reference_sample(ref, cfg, seed=10_000, mode=mode)  # numba JIT compile + warm caches
-        per_step, samples = [], []
-        for i in range(args.warmup + args.steps):
-            smp = reference_sample(ref, cfg, seed=i, mode=mode)
-            if i >= args.warmup:
-                samples.append(smp)
-        attn_best = {k: statistics.mean(x[k] for x in samples) for k in ("attn_numba", "attn_numpy")
-                     if k in samples[0]}
-        acc_s = statistics.mean(x["accept"] for x in samples)
-        # the faster stock backend is the reference's best CPU number
-        best_key = min(attn_best, key=attn_best.get) if attn_best else None
-        attn_s = attn_best[best_key] if best_key else 0.0
-        best_backend = best_key[len("attn_"):] if best_key else None
-        step_s = attn_s * f_attn + acc_s * f_acc
+        import multiprocessing as mp
+
+        # both stock attention backends timed once on one unit (numba JIT warmed first); the faster runs
+        one = reference_sample(ref, cfg, seed=10_000, mode=mode)
+        one = reference_sample(ref, cfg, seed=10_001, mode=mode)
+        backends = {k[len("attn_"):]: v for k, v in one.items() if k.startswith("attn_")}
+        backend = min(backends, key=backends.get) if backends else "numpy"
+        _REF["backend"] = backend
+        t_unit = backends.get(backend, 0.0)
+        budget = 3.0  # seconds of pool wall time per step
+        n_attn = f_attn if t_unit * f_attn <= budget * cores else max(cores, int(budget * cores / max(t_unit, 1e-9)))
+        n_acc = f_acc if one["accept"] * f_acc <= budget * cores else max(cores, int(budget * cores / one["accept"]))
+        n_attn, n_acc = min(n_attn, f_attn), min(n_acc, f_acc)
+        ctx = mp.get_context("fork")
+        times = []
+        with ctx.Pool(cores, initializer=_ref_worker_init, initargs=(cfg, mode, list(TREE), 0)) as pool:
+            for i in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                if n_attn:
+                    pool.map(_ref_attn_unit, range(n_attn), chunksize=1)
+                t1 = time.perf_counter()
+                pool.map(_ref_accept_seq, range(n_acc), chunksize=1)
+                t2 = time.perf_counter()
+                if i >= args.warmup:
+                    times.append(((t1 - t0) * (f_attn / n_attn if n_attn else 0.0), (t2 - t1) * f_acc / n_acc))
+        attn_s = statistics.mean(t[0] for t in times)
+        acc_s = statistics.mean(t[1] for t in times)
+        step_s = attn_s + acc_s
         kind = "reference"
-        sample = (f"stock specdec (baseline/_ref): tree_attention of 1 sequence x 1 KV-head group "
-                  f"({cfg['Hq'] // cfg['Hkv']} q heads, {best_backend} backend, x{f_attn}) + target_dist/mss_verify "
-                  f"of 1 sequence (x{f_acc}); {cores} host threads; extrapolated"
-                  if f_attn else f"stock specdec (baseline/_ref): target_dist + mss_verify of 1 sequence (x{f_acc}); "
-                                 f"{cores} host threads; extrapolated")
-        extra = {"sample_seconds": {**{k: v for k, v in attn_best.items()}, "accept": acc_s},
-                 "extrapolation": {"attention": f_attn, "accept": f_acc},
-                 "attn_backends_us_per_step": {k: v * f_attn * 1e6 + acc_s * f_acc * 1e6
-                                               for k, v in attn_best.items()}}
+        full = n_attn == f_attn and n_acc == f_acc
+        sample = (f"stock specdec (baseline/_ref), {backend} attention backend: "
+                  + (f"{n_attn} of {f_attn} (sequence, KV-head) tree_attention units + " if f_attn else "")
+                  + f"target_dist/mss_verify of {n_acc} of {f_acc} sequences per step on a pool of {cores} "
+                  f"one-BLAS-thread processes" + ("" if full else ", scaled to the whole batch"))
+        extra = {"sample_fraction": {"attention": (n_attn / f_attn) if f_attn else None, "accept": n_acc / f_acc},
+                 "pool_seconds_per_step": {"attention": attn_s * (n_attn / f_attn) if f_attn else 0.0,
+                                           "accept": acc_s * n_acc / f_acc},
+                 "one_unit_seconds": {**{"attn_" + k: v for k, v in backends.items()}, "accept": one["accept"]}}
         # the numpy port (oracle restatement) as a secondary figure
         ta, tacc, fa, facc = cpu_sample(cfg, seed=1, mode=mode)
         port = (ta * fa + tacc * facc) * 1e6
     else:
+        cores = blas_threads()
         samples = []
         for i in range(args.warmup + args.steps):
             ta, tacc, fa, facc = cpu_sample(cfg, seed=i, mode=mode)

@@ -216,7 +216,9 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
             tc_fence_after();
             if (elect_one()) {
               issue_pv(t, st, it > 0);
-              tc_commit(&sm.o_done[t]);
+              // O is read only by the unit's epilogue (a rescale relies on the
+              // in-order pipe: S(n + 1), committed after PV(n), gates it)
+              if (it == n_tiles - 1) tc_commit(&sm.o_done[t]);
             }
             __syncwarp();
             if (it + 1 < n_tiles) {
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
     const uint32_t t_s = tmem + lane_off + t * 128;
     const uint32_t t_o = tmem + lane_off + 256 + t * 128;
     const int local = t * kTileM + i;  // row within the unit
-    uint32_t g_tile = 0;
+    uint32_t g_tile = 0, g_unit = 0;
     ItemIter iter(sp, blockIdx.x);
     Item item;
     while (iter.next(sp, item)) {
@@ -278,7 +280,8 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
         softmax_tile<EMU>(t_s, t_o, sl2, it == 0, pref, kvalid, mrow, key0, p.n_words, row_ok, m, l);
         mbar_arrive(&sm.p_full[t]);
       }
-      mbar_wait(&sm.o_done[t], (g_tile + geo.n_tiles - 1) & 1);
+      mbar_wait(&sm.o_done[t], g_unit & 1);  // the unit's last PV
+      ++g_unit;
       tc_fence_after();
       epilogue_row(sp, item, geo, g, local, t_o, m, l);
       tc_fence_before();

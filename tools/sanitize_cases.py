@@ -1,6 +1,6 @@
 """Small launches of the pair attention kernel and the stochastic cluster
 walk for compute-sanitizer (racecheck / synccheck / memcheck):
-python tools/sanitize_cases.py attn|stoch"""
+python tools/sanitize_cases.py attn|attn1|stoch"""
 import os
 import sys
 
@@ -24,6 +24,16 @@ if what == "attn":
         out, lse, acc, terr = ver.step(x)
         torch.cuda.synchronize()
     print("attn ok", float(out.float().abs().mean()))
+elif what == "attn1":
+    # 1-CTA kernel (<= 128 query rows per KV head): the chain-3 tree, whole units + stream-K pieces + fix-up
+    bench.TREE = bench.TREES["chain3"]
+    cfg = dict(bench.CONFIGS["c3"], B=4, ctx=1024, V=2048)
+    x, R = bench.make_inputs(cfg, shard_for(0, 1, cfg["Hq"], cfg["Hkv"], cfg["V"]), dev)
+    for splits in (0, 40):
+        ver = TreeVerifier(scale=cfg["d"] ** -0.5, max_ctx=cfg["ctx"], num_splits=splits, kernel=1)
+        out, lse, acc, terr = ver.step(x)
+        torch.cuda.synchronize()
+    print("attn1 ok", float(out.float().abs().mean()))
 else:
     # stochastic acceptance, lazy walk (8-CTA clusters) + validation scan, and eager
     cfg = dict(bench.CONFIGS["c5"], B=4, V=32768)

@@ -505,8 +505,11 @@ def run_reference(args, cfg, mode):
         _REF["backend"] = backend
         t_unit = backends.get(backend, 0.0)
         budget = 3.0  # seconds of pool wall time per step
-        n_attn = f_attn if t_unit * f_attn <= budget * cores else max(cores, int(budget * cores / max(t_unit, 1e-9)))
-        n_acc = f_acc if one["accept"] * f_acc <= budget * cores else max(cores, int(budget * cores / one["accept"]))
+        # the whole step when it fits twice the budget, else a fixed share
+        n_attn = (f_attn if t_unit * f_attn <= 2 * budget * cores
+                  else max(cores, int(budget * cores / max(t_unit, 1e-9))))
+        n_acc = (f_acc if one["accept"] * f_acc <= 2 * budget * cores
+                 else max(cores, int(budget * cores / max(one["accept"], 1e-9))))
         n_attn, n_acc = min(n_attn, f_attn), min(n_acc, f_acc)
         ctx = mp.get_context("fork")
         times = []

@@ -499,6 +499,19 @@ __device__ double exact_cut(StSmem &sm, int count, double mass_above, double tau
 // one pass that sums the exact (f64) mass above the bins straddling the cut
 // and collects their few elements, which are sorted exactly by (key desc,
 // index asc) -- the reference's top_p_mask order (sampling.py:57-72).
+#ifdef SDB_TRACE
+// [launch][phase] clock64 stamps of the target row of sequence 0 (trace builds)
+__device__ unsigned long long g_st_trace[16][8];
+__device__ unsigned int g_st_launch;
+#define ST_TRACE(ph)                                                                          \
+  do {                                                                                        \
+    if (st_tr && threadIdx.x == 0) g_st_trace[st_launch & 15][ph] = clock64();                \
+  } while (0)
+#else
+#define ST_TRACE(ph) \
+  do {               \
+  } while (0)
+#endif
 template <bool kMasked>
 __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
@@ -509,6 +522,12 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   StSmem &sm = *reinterpret_cast<StSmem *>(smem_raw);
   // lazy mode (cur_rows): the one row per sequence the walk is at (-1: done)
   const int r = cur_rows ? cur_rows[blockIdx.y] : (int)blockIdx.x, b = blockIdx.y, is_draft = blockIdx.z;
+#ifdef SDB_TRACE
+  const bool st_tr = b == 0 && is_draft == 0 && (cur_rows || blockIdx.x == 0);
+  unsigned int st_launch = 0;
+  if (st_tr && threadIdx.x == 0) st_launch = atomicAdd(&g_st_launch, 1u);
+#endif
+  ST_TRACE(0);
   if (r < 0) return;
   const int n = min(n_rows[b], r_max);
   RowStats *out = stats + ((int64_t)b * r_max + r) * 2 + is_draft;
@@ -534,7 +553,15 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   const bool nucleus = !is_draft && top_p < 1.0f;
   // the whole row streams into L2 through the TMA engine (deep memory-level
   // parallelism); the passes below then hit L2
-  if (vec && threadIdx.x == 0) {
+// whole-row L2 bulk prefetch before pass 1: off by default (C5 eager 1316 vs
+// 1350 us with it; lazy unchanged at 941-946: the chain's row stats are bound
+// by the histogram / window passes -- clock64 trace, tools/trace_rowstats.py:
+// max pass 12-18 k cycles, normaliser + histogram 27 k, mass above + window
+// collection 23-41 k, exact cut 7-14 k)
+#ifndef SDB_ST_PREFETCH
+#define SDB_ST_PREFETCH 0
+#endif
+  if (SDB_ST_PREFETCH && vec && threadIdx.x == 0) {
     constexpr uint32_t kChunk = 64u << 10;
     const uint32_t bytes = (uint32_t)vocab * 4u;
     for (uint32_t o = 0; o < bytes; o += kChunk) prefetch_l2((const char *)row + o, min(kChunk, bytes - o));
@@ -545,16 +572,20 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   if (nucleus)
     for (int i = threadIdx.x; i < kHistCopies * kHistBins; i += kStThreads) (&sm.hist[0][0])[i] = 0u;
   // pass 1: max + NaN (3-input max.NaN: NaN propagates into the maximum)
+#ifndef SDB_ST_KU1
+#define SDB_ST_KU1 4
+#endif
+  constexpr int kU1 = SDB_ST_KU1;  // loads in flight per thread in the HBM pass
   float mx = -INFINITY;
-  for (int i0 = 0; i0 < n4; i0 += kU * kStThreads) {
-    float4 v[kU];
+  for (int i0 = 0; i0 < n4; i0 += kU1 * kStThreads) {
+    float4 v[kU1];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kU1; ++u) {
       const int i = i0 + u * kStThreads + threadIdx.x;
       v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) mx = max3_nan(mx, max3_nan(v[u].x, v[u].y, v[u].z), v[u].w);
+    for (int u = 0; u < kU1; ++u) mx = max3_nan(mx, max3_nan(v[u].x, v[u].y, v[u].z), v[u].w);
   }
   for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) mx = max3_nan(mx, mask1(row[j], mw, j), mask1(row[j], mw, j));
   if (__syncthreads_or(mx != mx)) {
@@ -565,6 +596,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     return;
   }
   mx = block_max<kStThreads>(mx, sm.redf);
+  ST_TRACE(1);
   if (mx == -INFINITY) {  // no allowed token (dead FSM state, sampling.py:96-97) / no finite logit
     if (threadIdx.x == 0) {
       atomicOr(err, mw ? SDB_ERR_NO_ALLOWED : SDB_ERR_BAD_DIST);
@@ -665,6 +697,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     s_loc += s_lo;
   }
   const double s = block_sum<kStThreads>((double)s_loc, sm.red);
+  ST_TRACE(2);
   const double tau = ((double)top_p - 1e-12) * s;
   // window [lo, hi] of bins whose cumulative (bin 0 = largest values) may
   // straddle tau given the fixed-point bin sums
@@ -701,6 +734,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     __syncthreads();
   }
   const int lo = sm.lo, hi = max(sm.hi, sm.lo);
+  ST_TRACE(3);
   // pass 3 (L2): the same d splits the keys monotonically into above (d <
   // lo - 1/2), the window and below; exact mass above, window elements
   // collected with warp-aggregated slots.  Keys with equal logits share d,
@@ -789,6 +823,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     atomicMax(&sm.khi, kh);
   }
   double mass_above = block_sum<kStThreads>((double)above, sm.red);  // (syncs sm.count / klo / khi too)
+  ST_TRACE(4);
   uint32_t klo = sm.klo, khi = sm.khi;
   uint32_t cut_key = 0;
   int cut_idx = -1;
@@ -825,6 +860,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     }
     if (count <= kCandCap) {
       z = exact_cut(sm, count, mass_above, tau, a, m2, cut_key, cut_idx);
+      ST_TRACE(5);
       break;
     }
     if (klo == khi) {
@@ -1796,3 +1832,10 @@ extern "C" int sdb_stochastic_validate(const float *target_logits, const float *
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
+
+#ifdef SDB_TRACE
+extern "C" int sdb_debug_st_trace(unsigned long long *host_out, unsigned int *count) {
+  if (cudaMemcpyFromSymbol(host_out, sdb::g_st_trace, sizeof(sdb::g_st_trace)) != cudaSuccess) return -4;
+  return cudaMemcpyFromSymbol(count, sdb::g_st_launch, sizeof(unsigned int)) == cudaSuccess ? 0 : -4;
+}
+#endif

@@ -143,6 +143,11 @@ typedef struct sdb_tree_attn_args {
                                  attention.py:189-206; engine.py:486-487).
                                  tcgen05 path: chunk % 128 == 0 and
                                  chunk % block_size == 0, else SIMT */
+  int32_t *err;               /* optional [1]: SDB_ERR_CACHE (OR-ed) when a
+                                 sequence's ctx_len exceeds max_ctx -- the
+                                 tcgen05 plan covers max_ctx keys, so the keys
+                                 past it would be dropped (kvstore.py CacheError
+                                 contract: fail, never truncate silently) */
 } sdb_tree_attn_args;
 
 /* The kernel launched just before on the stream is sdb_tree_build (the only

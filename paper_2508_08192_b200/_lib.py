@@ -50,6 +50,7 @@ class TreeAttnArgs(ctypes.Structure):
         ("q_row0", P), ("max_q_nodes", I32), ("flags", I32),
         ("fused_logits", P), ("fused_row_stride", I64), ("fused_vocab_offset", I64), ("fused_vocab", I32),
         ("fused_keys", P), ("fused_err", P), ("chunk_len", I32),
+        ("err", P),
     ]
 
 

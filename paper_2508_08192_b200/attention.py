@@ -256,7 +256,7 @@ class TreeVerifyAttention:
 
     def _args(self, q, k_cache, v_cache, block_table, ctx_len, tree_k, tree_v, mask_words, n_rows, scale,
                  out=None, lse=None, max_ctx=None, num_splits=0, kernel=KERNEL_AUTO, stream=None, q_row0=None,
-                 max_q_nodes=None, after_tree_build=False, fused_argmax=None, chunk_len=None):
+                 max_q_nodes=None, after_tree_build=False, fused_argmax=None, chunk_len=None, err=None):
         import torch
 
         b, r, hq, d = q.shape
@@ -294,6 +294,10 @@ class TreeVerifyAttention:
             a.max_q_nodes = int(max_q_nodes)
         if chunk_len:  # iRoPE: every row sees prefix keys [floor(C / chunk) * chunk, C)
             a.chunk_len = int(chunk_len)
+        if err is not None:  # int32 [1]: SDB_ERR_CACHE when a ctx_len exceeds max_ctx (keys would be dropped)
+            if err.dtype != torch.int32 or err.numel() < 1:
+                raise AttentionError("err must be an int32 tensor with >= 1 element")
+            a.err = err.data_ptr()
         if after_tree_build:  # the previous kernel on `stream` is tree_build: PDL launch
             a.flags |= _lib.ATTN_FLAG_PDL
         if fused_argmax is not None:

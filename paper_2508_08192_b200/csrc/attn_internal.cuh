@@ -24,6 +24,7 @@ struct TreeAttnParams {
   int64_t fa_row_stride, fa_vocab_offset;
   int fa_vocab;
   long long *fa_keys;
+  int32_t *err;     // SDB_ERR_CACHE when ctx_len > max_ctx (tcgen05 plan), or nullptr
   int32_t *fa_err;
   float scale;
   int num_splits;

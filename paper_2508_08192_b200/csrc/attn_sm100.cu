@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
       while (iter.next(sp, item)) {
         const ItemGeo geo = item_geo(sp, item, g);
         if (!geo.active) continue;
+        // the plan covers w_pref prefix tiles: a longer context (ctx_len >
+        // max_ctx) would lose keys -- flag it instead (CacheError)
+        if (lane == 0 && p.err && geo.C - geo.k0 > sp.w_pref * kTileN) atomicOr(p.err, SDB_ERR_CACHE);
         // Q tiles of this unit once the previous unit's S MMAs are done
         mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
         if (lane == 0) {

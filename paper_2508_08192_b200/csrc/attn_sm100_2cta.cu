@@ -394,6 +394,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       while (iter.next(sp, item)) {
         const ItemGeo geo = item_geo(sp, item, g);
         if (!geo.active) continue;
+        // the plan covers w_pref prefix tiles: a longer context (ctx_len >
+        // max_ctx) would lose keys -- flag it instead (CacheError)
+        if (kprod && lane == 0 && rank == 0 && p.err && geo.C - geo.k0 > sp.w_pref * kTileN)
+          atomicOr(p.err, SDB_ERR_CACHE);
         if (kprod) {
           mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
           if (lane == 0) {

@@ -34,6 +34,7 @@ static bool fill_params(const sdb_tree_attn_args *a, TreeAttnParams &p) {
   p.fa_logits = nullptr;
   p.fa_keys = nullptr;
   p.fa_err = nullptr;
+  p.err = a->err;
   p.mask_words = a->mask_words;
   p.out = a->out;
   p.lse = a->lse;

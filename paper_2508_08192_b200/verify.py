@@ -87,6 +87,9 @@ class TreeVerifier:
                 pos=torch.empty((b, r), dtype=torch.int32, device=dev),
                 depth=torch.empty((b, r), dtype=torch.int32, device=dev),
                 tree_err=torch.empty((b,), dtype=torch.int32, device=dev),
+                # sticky (no per-step clear launch): set by the attention when a
+                # ctx_len exceeds max_ctx, reset by check()
+                attn_err=torch.zeros((1,), dtype=torch.int32, device=dev),
                 out=torch.empty_like(x.q),
                 lse=torch.empty((b, hq, r), dtype=torch.float32, device=dev)))
         return self._out[1]
@@ -107,7 +110,7 @@ class TreeVerifier:
         attn_args = (x.q, x.k_pool, x.v_pool, x.block_table, x.ctx_len, x.tree_k, x.tree_v, o["mask"], x.n_rows,
                      self.scale)
         attn_kw = dict(out=o["out"], lse=o["lse"], max_ctx=self.max_ctx, num_splits=self.num_splits,
-                       kernel=self.kernel, chunk_len=self.chunk_len)
+                       kernel=self.kernel, chunk_len=self.chunk_len, err=o["attn_err"])
         # small batches: the attention's persistent grid leaves SMs free ->
         # run acceptance beside it; full occupancy -> fold the greedy scan
         # into the attention kernel (its otherwise idle warp + TMA ring)
@@ -177,6 +180,27 @@ class TreeVerifier:
         if side is not main:
             main.wait_stream(side)
         return o["out"], o["lse"], acc, o["tree_err"]
+
+    def check(self, tree_err=None, acc=None):
+        """Host sync: raise the reference exceptions for the last step's
+        device error words -- TreeError (bad parent), CacheError (a ctx_len
+        past ``max_ctx``: the attention plan would have dropped keys), and
+        the acceptance's errors when ``acc`` is given."""
+        from .drafttree import TreeError
+        from .kvstore import CacheError
+
+        o = self._out[1] if self._out is not None else None
+        if o is None:
+            return
+        te = o["tree_err"] if tree_err is None else tree_err
+        if int((te & _lib.SDB_ERR_BAD_PARENT).sum().item()):
+            raise TreeError("parent must precede node or be ROOT")
+        if int(o["attn_err"][0].item()) & _lib.SDB_ERR_CACHE:
+            o["attn_err"].zero_()
+            raise CacheError(f"context longer than max_ctx={self.max_ctx}: size TreeVerifier(max_ctx=) for the "
+                             "longest sequence")
+        if acc is not None:
+            acc.raise_if_error()
 
     def _auto_reserve(self, x, b, r, n_sms):
         """SMs to leave to a greedy acceptance running beside a full-occupancy

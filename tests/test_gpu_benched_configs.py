@@ -275,3 +275,28 @@ def test_sharded_greedy_two_processes_gloo():
             assert int(nxt[b]) == want_next and int(used[b]) == want_used, (rank, b)
         nan_err = got[rank][1][0]
         assert nan_err & 2, rank  # SDB_ERR_NAN on both ranks
+
+
+@pytest.mark.parametrize("tree", ["64", "chain3"])
+def test_context_past_max_ctx_raises_cache_error(tree):
+    """A ctx_len beyond the planned max_ctx (the tcgen05 plan covers
+    ceil(max_ctx / 128) prefix tiles) raises CacheError through
+    TreeVerifier.check() instead of silently dropping keys -- the pair kernel
+    (64-row tree) and the 1-CTA kernel (chain-3); within the plan it passes."""
+    from paper_2508_08192_b200.kvstore import CacheError
+    from paper_2508_08192_b200.sharding import shard_for
+    from paper_2508_08192_b200.verify import TreeVerifier
+
+    bench.TREE = bench.TREES[tree]
+    cfg = dict(bench.CONFIGS["c3"], B=2, ctx=1024, V=2048)
+    x, R = bench.make_inputs(cfg, shard_for(0, 1, cfg["Hq"], cfg["Hkv"], cfg["V"]), torch.device("cuda", 0))
+    ok = TreeVerifier(scale=cfg["d"] ** -0.5, max_ctx=1024, kernel=1)
+    out, lse, acc, terr = ok.step(x)
+    torch.cuda.synchronize()
+    ok.check(acc=acc)  # within the plan: no error
+    short = TreeVerifier(scale=cfg["d"] ** -0.5, max_ctx=512, kernel=1)
+    out, lse, acc, terr = short.step(x)
+    torch.cuda.synchronize()
+    with pytest.raises(CacheError):
+        short.check()
+    short.check()  # the word is reset once reported

@@ -408,7 +408,7 @@ def _sample_desc(cfg, mode, cores):
 _REF = {}
 
 
-def _ref_worker_init(cfg, mode, tree, seed):
+def _ref_worker_init(cfg, mode, tree, seed, backend="numpy"):
     """Pool worker: one BLAS thread, the stock reference imported, one unit's
     inputs drawn once (the reference's cost does not depend on the values)."""
     import numpy as np
@@ -422,7 +422,7 @@ def _ref_worker_init(cfg, mode, tree, seed):
     global TREE
     TREE = tree
     ref = load_reference()
-    ref.kernels.set_backend(_REF.get("backend", "numpy"))
+    ref.kernels.set_backend(backend)
     rng = np.random.default_rng(seed)
     Hq, Hkv, d, C, V = (cfg[k] for k in ("Hq", "Hkv", "d", "ctx", "V"))
     g = Hq // Hkv
@@ -476,66 +476,75 @@ def _host_cores():
         return os.cpu_count() or 1
 
 
-def run_reference(args, cfg, mode):
-    """--impl reference: the reference's own CPU implementation of the path
-    (stock specdec from baseline/_ref; the numpy oracle port when it is not
-    installed), rank 0 only, every host core: a pool of one-BLAS-thread
-    processes runs the step's (sequence, KV head) attention units and its
-    sequences' acceptance -- the reference loops them independently
-    (engine.py:581-582; attention per KV head), so the pool's wall time is
-    the reference's best multi-core step.  A step is the whole workload
-    unless that would exceed ~3 s of wall time; then a fixed share of the
-    units per step, scaled to the whole batch (reported as sample_fraction)."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+def reference_pool(cfg, mode, steps, warmup, start="fork"):
+    """The stock reference path (baseline/_ref) on a pool of one-BLAS-thread
+    processes over every host core: each step runs the step's (sequence, KV
+    head) tree_attention units and its sequences' target_dist + mss_verify
+    (the reference loops them independently, engine.py:581-582; attention per
+    KV head), so the pool's wall time is the reference's best multi-core step.
+    The whole step when it fits twice a 3 s budget, else a fixed share of the
+    units scaled to the batch.  Returns (seconds per step, cores, sample
+    description, extra fields) or None when baseline/_ref is absent."""
+    ref = load_reference()
+    if ref is None:
+        return None
+    import multiprocessing as mp
+
     cores = _host_cores()
     f_attn = 0 if cfg.get("accept_only") else cfg["B"] * cfg["Hkv"]
     f_acc = cfg["B"]
-    ref = load_reference()
-    port = None
-    if ref is not None:
-        import multiprocessing as mp
+    # both stock attention backends timed on one unit (numba JIT warmed first); the faster runs
+    one = reference_sample(ref, cfg, seed=10_000, mode=mode)
+    one = reference_sample(ref, cfg, seed=10_001, mode=mode)
+    backends = {k[len("attn_"):]: v for k, v in one.items() if k.startswith("attn_")}
+    backend = min(backends, key=backends.get) if backends else "numpy"
+    _REF["backend"] = backend
+    t_unit = backends.get(backend, 0.0)
+    budget = 3.0  # seconds of pool wall time per step
+    # the whole step when it fits twice the budget, else a fixed share
+    n_attn = (f_attn if t_unit * f_attn <= 2 * budget * cores
+              else max(cores, int(budget * cores / max(t_unit, 1e-9))))
+    n_acc = (f_acc if one["accept"] * f_acc <= 2 * budget * cores
+             else max(cores, int(budget * cores / max(one["accept"], 1e-9))))
+    n_attn, n_acc = min(n_attn, f_attn), min(n_acc, f_acc)
+    ctx = mp.get_context(start)
+    times = []
+    with ctx.Pool(cores, initializer=_ref_worker_init, initargs=(cfg, mode, list(TREE), 0, backend)) as pool:
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            if n_attn:
+                pool.map(_ref_attn_unit, range(n_attn), chunksize=1)
+            t1 = time.perf_counter()
+            pool.map(_ref_accept_seq, range(n_acc), chunksize=1)
+            t2 = time.perf_counter()
+            if i >= warmup:
+                times.append(((t1 - t0) * (f_attn / n_attn if n_attn else 0.0), (t2 - t1) * f_acc / n_acc))
+    attn_s = statistics.mean(t[0] for t in times)
+    acc_s = statistics.mean(t[1] for t in times)
+    full = n_attn == f_attn and n_acc == f_acc
+    sample = (f"stock specdec (baseline/_ref), {backend} attention backend: "
+              + (f"{n_attn} of {f_attn} (sequence, KV-head) tree_attention units + " if f_attn else "")
+              + f"target_dist/mss_verify of {n_acc} of {f_acc} sequences per step on a pool of {cores} "
+              f"one-BLAS-thread processes" + ("" if full else ", scaled to the whole batch"))
+    extra = {"sample_fraction": {"attention": (n_attn / f_attn) if f_attn else None, "accept": n_acc / f_acc},
+             "pool_seconds_per_step": {"attention": attn_s * (n_attn / f_attn) if f_attn else 0.0,
+                                       "accept": acc_s * n_acc / f_acc},
+             "one_unit_seconds": {**{"attn_" + k: v for k, v in backends.items()}, "accept": one["accept"]}}
+    return attn_s + acc_s, cores, sample, extra
 
-        # both stock attention backends timed once on one unit (numba JIT warmed first); the faster runs
-        one = reference_sample(ref, cfg, seed=10_000, mode=mode)
-        one = reference_sample(ref, cfg, seed=10_001, mode=mode)
-        backends = {k[len("attn_"):]: v for k, v in one.items() if k.startswith("attn_")}
-        backend = min(backends, key=backends.get) if backends else "numpy"
-        _REF["backend"] = backend
-        t_unit = backends.get(backend, 0.0)
-        budget = 3.0  # seconds of pool wall time per step
-        # the whole step when it fits twice the budget, else a fixed share
-        n_attn = (f_attn if t_unit * f_attn <= 2 * budget * cores
-                  else max(cores, int(budget * cores / max(t_unit, 1e-9))))
-        n_acc = (f_acc if one["accept"] * f_acc <= 2 * budget * cores
-                 else max(cores, int(budget * cores / max(one["accept"], 1e-9))))
-        n_attn, n_acc = min(n_attn, f_attn), min(n_acc, f_acc)
-        ctx = mp.get_context("fork")
-        times = []
-        with ctx.Pool(cores, initializer=_ref_worker_init, initargs=(cfg, mode, list(TREE), 0)) as pool:
-            for i in range(args.warmup + args.steps):
-                t0 = time.perf_counter()
-                if n_attn:
-                    pool.map(_ref_attn_unit, range(n_attn), chunksize=1)
-                t1 = time.perf_counter()
-                pool.map(_ref_accept_seq, range(n_acc), chunksize=1)
-                t2 = time.perf_counter()
-                if i >= args.warmup:
-                    times.append(((t1 - t0) * (f_attn / n_attn if n_attn else 0.0), (t2 - t1) * f_acc / n_acc))
-        attn_s = statistics.mean(t[0] for t in times)
-        acc_s = statistics.mean(t[1] for t in times)
-        step_s = attn_s + acc_s
+
+def run_reference(args, cfg, mode):
+    """--impl reference: the reference's own CPU implementation of the path
+    (stock specdec from baseline/_ref, ``reference_pool``; the numpy oracle
+    port when it is not installed), rank 0 only, every host core."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    port = None
+    res = reference_pool(cfg, mode, args.steps, args.warmup)
+    if res is not None:
+        step_s, cores, sample, extra = res
         kind = "reference"
-        full = n_attn == f_attn and n_acc == f_acc
-        sample = (f"stock specdec (baseline/_ref), {backend} attention backend: "
-                  + (f"{n_attn} of {f_attn} (sequence, KV-head) tree_attention units + " if f_attn else "")
-                  + f"target_dist/mss_verify of {n_acc} of {f_acc} sequences per step on a pool of {cores} "
-                  f"one-BLAS-thread processes" + ("" if full else ", scaled to the whole batch"))
-        extra = {"sample_fraction": {"attention": (n_attn / f_attn) if f_attn else None, "accept": n_acc / f_acc},
-                 "pool_seconds_per_step": {"attention": attn_s * (n_attn / f_attn) if f_attn else 0.0,
-                                           "accept": acc_s * n_acc / f_acc},
-                 "one_unit_seconds": {**{"attn_" + k: v for k, v in backends.items()}, "accept": one["accept"]}}
         # the numpy port (oracle restatement) as a secondary figure
         ta, tacc, fa, facc = cpu_sample(cfg, seed=1, mode=mode)
         port = (ta * fa + tacc * facc) * 1e6
@@ -943,12 +952,20 @@ def main():
         parity = parity_sample(cfg, x, None if accept_only else o["out"], None if accept_only else o["lse"], acc,
                                mode, aug)
         line["parity"] = parity
-        # ... and the reference algorithm timed on a bounded sample
-        cpu_sample(cfg, mode=mode)
-        ta, tacc, fa, facc = cpu_sample(cfg, seed=1, mode=mode)
-        us = (ta * fa + tacc * facc) * 1e6
-        line["cpu_baseline"] = {"value": us, "unit": "us/step", "cores": blas_threads(), "kind": "port",
-                                "sample": _sample_desc(cfg, mode, blas_threads())}
+        # ... and the reference timed on the host: the stock path on every
+        # core for two steps (the same measurement as --impl reference;
+        # spawned workers: this process holds a CUDA context), else the port
+        res = reference_pool(cfg, mode, steps=2, warmup=1, start="spawn")
+        if res is not None:
+            step_s, cores, sample, extra = res
+            line["cpu_baseline"] = {"value": step_s * 1e6, "unit": "us/step", "cores": cores, "kind": "reference",
+                                    "sample": sample, **extra}
+        else:
+            cpu_sample(cfg, mode=mode)
+            ta, tacc, fa, facc = cpu_sample(cfg, seed=1, mode=mode)
+            us = (ta * fa + tacc * facc) * 1e6
+            line["cpu_baseline"] = {"value": us, "unit": "us/step", "cores": blas_threads(), "kind": "port",
+                                    "sample": _sample_desc(cfg, mode, blas_threads())}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -71,6 +71,29 @@ __device__ __forceinline__ V scan_ld(const V *p) {
 #endif
 }
 
+// fp32 rows, SDB_ARGMAX_STAGES > 0: each thread streams its 16-byte elements
+// through a private ring of shared-memory slots filled by cp.async (no
+// register destination: 2 CTAs x 1024 threads keep STAGES x 32 KB in flight
+// per SM).  Measured at C3 (tools/cycles/r2_argmax_cpasync.sh): the scan
+// alone 164 us with 6 stages vs 185 with plain loads, but the bench step --
+// the scan on the 20 SMs beside the attention -- 626 vs 607-617 us at every
+// reserve (14-20 SMs): the deeper stream slows the attention more than it
+// gains.  Default 0: plain loads (4 in flight per thread).
+#ifndef SDB_ARGMAX_STAGES
+#define SDB_ARGMAX_STAGES 0
+#endif
+constexpr int kArgmaxStages = SDB_ARGMAX_STAGES;
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ void argmax_row(const T *__restrict__ row, int vocab, int64_t vocab_offset,
                                            bool vec_ok, long long &best, bool &nan) {
@@ -81,6 +104,32 @@ __device__ __forceinline__ void argmax_row(const T *__restrict__ row, int vocab,
     float bv = -INFINITY;
     int bi = threadIdx.x < n4 ? (int)threadIdx.x : -1;
     int i = threadIdx.x;
+    if (kArgmaxStages > 0) {
+      extern __shared__ float4 am_ring[];  // [kArgmaxStages][kArgmaxThreads], slot = this thread's
+      const int nk = (int)threadIdx.x < n4 ? (n4 - (int)threadIdx.x + kArgmaxThreads - 1) / kArgmaxThreads : 0;
+#pragma unroll
+      for (int k = 0; k < kArgmaxStages - 1; ++k) {
+        if (k < nk) cp_async16(&am_ring[k * kArgmaxThreads + threadIdx.x], r4 + threadIdx.x + k * kArgmaxThreads);
+        cp_async_commit();
+      }
+      for (int k = 0; k < nk; ++k) {
+        const int kk = k + kArgmaxStages - 1;
+        if (kk < nk)
+          cp_async16(&am_ring[(kk % kArgmaxStages) * kArgmaxThreads + threadIdx.x],
+                     r4 + threadIdx.x + kk * kArgmaxThreads);
+        cp_async_commit();
+        cp_async_wait<kArgmaxStages - 1>();  // element k has landed (this thread's own copies)
+        const float4 v = am_ring[(k % kArgmaxStages) * kArgmaxThreads + threadIdx.x];
+        const float m = max_nan(max_nan3(v.x, v.y, v.z), v.w);
+        nacc = max_nan(nacc, m);
+        if (m > bv) {
+          bv = m;
+          bi = (int)threadIdx.x + k * kArgmaxThreads;
+        }
+      }
+      cp_async_wait<0>();
+      i = n4;  // the loops below have nothing left
+    }
     // 4 independent 16-byte loads in flight per thread
     for (; i + 3 * kArgmaxThreads < n4; i += 4 * kArgmaxThreads) {
       float4 v[4];
@@ -196,6 +245,18 @@ __global__ void __launch_bounds__(kArgmaxThreads, 2) argmax_keys_kernel(const T 
   best = block_max_i64<kArgmaxThreads>(best, red);
   if (__syncthreads_or(nan) && threadIdx.x == 0 && err) atomicOr(err, SDB_ERR_NAN);
   if (threadIdx.x == 0) keys[row * split + seg] = best;
+}
+
+// dynamic shared memory of argmax_keys_kernel<float> (the cp.async ring),
+// attribute set once
+static size_t argmax_smem() {
+  const size_t bytes = (size_t)kArgmaxStages * kArgmaxThreads * sizeof(float4);
+  static bool set = false;
+  if (!set && bytes > 0) {
+    cudaFuncSetAttribute(argmax_keys_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    set = true;
+  }
+  return bytes;
 }
 
 // Greedy acceptance over FSM-masked rows (target_dist(row, 0, ., allowed),
@@ -1532,7 +1593,7 @@ extern "C" int sdb_argmax_keys(const void *logits, int dtype, int64_t rows, int 
   dim3 grid((unsigned)(gx * gy == rows ? gx : rows), (unsigned)(gx * gy == rows ? gy : 1));
   cudaStream_t s = sdb::as_stream(stream);
   if (dtype == SDB_DTYPE_F32)
-    sdb::argmax_keys_kernel<float><<<grid, sdb::kArgmaxThreads, 0, s>>>(
+    sdb::argmax_keys_kernel<float><<<grid, sdb::kArgmaxThreads, sdb::argmax_smem(), s>>>(
         (const float *)logits, vocab, row_stride, vocab_offset, nullptr, 0, (long long *)keys, err,
         vec_aligned(logits, row_stride, 4, vocab), 1);
   else if (dtype == SDB_DTYPE_BF16)
@@ -1596,7 +1657,7 @@ extern "C" int sdb_accept_greedy(const void *logits, int dtype, int batch, int r
   dim3 grid(r_max * split, batch);
   cudaStream_t s = sdb::as_stream(stream);
   if (dtype == SDB_DTYPE_F32)
-    sdb::argmax_keys_kernel<float><<<grid, sdb::kArgmaxThreads, 0, s>>>(
+    sdb::argmax_keys_kernel<float><<<grid, sdb::kArgmaxThreads, sdb::argmax_smem(), s>>>(
         (const float *)logits, vocab, row_stride, 0, n_rows, r_max, (long long *)keys, err,
         vec_aligned(logits, row_stride, 4, vocab), split);
   else if (dtype == SDB_DTYPE_BF16)

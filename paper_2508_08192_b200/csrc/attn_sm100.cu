@@ -38,7 +38,7 @@ struct alignas(1024) Smem {
   uint8_t v[2][kTileBytes];
   uint64_t q_full, q_empty;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[NT], p_full[NT], o_done[NT], o_free[NT];
+  uint64_t s_full[2], p_full[2], o_done[NT], o_free[NT];  // NT = 1: two S slots of the one tile
   uint32_t tmem_base;
 };
 
@@ -49,7 +49,7 @@ template <int NT, int EMU>
 __global__ void __launch_bounds__(128 + NT * 128, 1)
     tree_attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_tk,
-                             const __grid_constant__ CUtensorMap tm_tv, const Sm100Params sp) {
+                             const __grid_constant__ CUtensorMap tm_tv, const __grid_constant__ Sm100Params sp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem<NT> &sm = *reinterpret_cast<Smem<NT> *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const TreeAttnParams &p = sp.p;
@@ -69,9 +69,11 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
-    for (int t = 0; t < NT; ++t) {
+    for (int t = 0; t < 2; ++t) {
       mbar_init(&sm.s_full[t], 1);
       mbar_init(&sm.p_full[t], 128);
+    }
+    for (int t = 0; t < NT; ++t) {
       mbar_init(&sm.o_done[t], 1);
       mbar_init(&sm.o_free[t], 128);
     }
@@ -193,7 +195,61 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
       uint32_t g_tile = 0, g_q = 0;
       ItemIter iter(sp, blockIdx.x);
       Item item;
-      while (iter.next(sp, item)) {
+      if (NT == 1) {
+        // one query tile, two S slots (TMEM columns [0,128) and [128,256), O
+        // at [256,384)): S(n + 1) runs while the softmax works on item n, and
+        // S(n + 2) refills slot n % 2 right after PV(n) -- at small trees the
+        // item no longer serialises S -> softmax -> PV
+        auto issue_s1 = [&](uint32_t gt) {
+          mbar_wait(&sm.k_full[gt & 1], (gt >> 1) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t kd = k_desc + (uint64_t)(((gt & 1) * kTileBytes) >> 4);
+#pragma unroll
+            for (int k = 0; k < kHeadDim / 16; ++k) {
+              const uint64_t off = (uint64_t)(((k >> 2) * kChunkBytes + (k & 3) * 32) >> 4);
+              mma_ss(tm + (gt & 1) * 128, q_desc + off, kd + off, idesc_s, k > 0);
+            }
+            tc_commit(&sm.s_full[gt & 1]);
+            tc_commit(&sm.k_empty[gt & 1]);
+          }
+          __syncwarp();
+        };
+        while (iter.next(sp, item)) {
+          const ItemGeo geo = item_geo(sp, item, g);
+          if (!geo.active) continue;
+          const int n_tiles = __shfl_sync(0xffffffffu, geo.n_tiles, 0);
+          mbar_wait(&sm.q_full, g_q & 1);
+          issue_s1(g_tile);
+          if (n_tiles > 1) issue_s1(g_tile + 1);
+          for (int it = 0; it < n_tiles; ++it) {
+            const uint32_t gt = g_tile + it;
+            const int sl = gt & 1;
+            mbar_wait(&sm.v_full[sl], (gt >> 1) & 1);
+            mbar_wait(&sm.p_full[sl], (gt >> 1) & 1);
+            if (it == 0) mbar_wait(&sm.o_free[0], (g_q & 1) ^ 1);  // previous unit's epilogue read O
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t vd = v_desc + (uint64_t)((sl * kTileBytes) >> 4);
+#pragma unroll
+              for (int k = 0; k < kTileN / 16; ++k)
+                // P of keys 16k .. 16k+15 at slot columns 32 (k/2) + 8 (k%2)
+                // (chunk c packed into the first half of its own 32 S columns)
+                mma_ts(tm + 256, tm + sl * 128 + 32 * (k >> 1) + 8 * (k & 1), vd + (uint64_t)((k * 2048) >> 4),
+                       idesc_o, (it > 0 || k > 0) ? 1u : 0u);
+              if (it == n_tiles - 1) tc_commit(&sm.o_done[0]);  // the epilogue may read O
+              tc_commit(&sm.v_empty[sl]);
+            }
+            __syncwarp();
+            if (it + 2 < n_tiles) issue_s1(gt + 2);
+          }
+          if (elect_one()) tc_commit(&sm.q_empty);  // all S MMAs of this unit read Q
+          __syncwarp();
+          g_tile += n_tiles;
+          ++g_q;
+        }
+      }
+      while (NT == 2 && iter.next(sp, item)) {
         const ItemGeo geo = item_geo(sp, item, g);
         if (!geo.active) continue;
         const int n_tiles = __shfl_sync(0xffffffffu, geo.n_tiles, 0);
@@ -262,7 +318,90 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
     uint32_t g_tile = 0, g_unit = 0;
     ItemIter iter(sp, blockIdx.x);
     Item item;
-    while (iter.next(sp, item)) {
+    if (NT == 1) {
+      // items alternate between the two S slots.  Fixed reference (as in the
+      // pair kernel): the row max of the first 32 keys of the piece's first
+      // tile; P = exp2(s * scale * log2e - m_ref), nothing is ever rescaled
+      // (O is accumulated by PV MMAs this warp does not wait for); a row
+      // whose scores climb ~89 log2 units above it is recomputed exactly by
+      // its own thread after the epilogue
+      while (iter.next(sp, item)) {
+        const ItemGeo geo = item_geo(sp, item, g);
+        if (!geo.active) {
+          inactive_row(sp, item, geo, g, local);
+          continue;
+        }
+        const int rho = geo.row0 + local;
+        const bool row_ok = rho < geo.rows_total;
+        const int node = min(geo.q0 + rho / g, max(geo.n_nodes - 1, 0));
+        const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
+        // a warp whose 32 rows are all padding only keeps the barrier phases
+        const bool pad_warp = geo.row0 + (warp & 3) * 32 >= geo.rows_total;
+        float m_ref = -INFINITY, l = 0.f;
+        bool bad = false;
+        for (int it = 0; it < geo.n_tiles; ++it) {
+          const uint32_t gt = g_tile + it;
+          const int sl = gt & 1;
+          const bool pref = it < geo.n_pref;
+          const int key0 = pref ? geo.k0 + (geo.pa + it) * kTileN : (geo.sa + it - geo.n_pref) * kTileN;
+          const int kvalid = pref ? geo.C - key0 : geo.n_nodes - key0;
+          const bool full = pref && kvalid >= kTileN;
+          mbar_wait(&sm.s_full[sl], (gt >> 1) & 1);
+          tc_fence_after();
+          const uint32_t ts = tmem + lane_off + sl * 128;
+          if (!pad_warp) {
+            uint32_t vm[4] = {~0u, ~0u, ~0u, ~0u};
+            if (!full) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) vm[c] = vis_word(pref, kvalid, mrow, key0, p.n_words, row_ok, 32 * c);
+            }
+            uint32_t r[32], r2[32];
+            if (it == 0) {
+              SDB_TMEM_LD32(ts, r2);
+              SDB_TMEM_WAIT_LD_REGS(r2);
+              if (!full) apply_mask32(r2, vm[0]);
+              m_ref = max32(r2) * sl2;
+            }
+            const float neg_mu = (m_ref == -INFINITY) ? 0.f : -m_ref;
+            const uint64_t sc2 = f2pack(sl2, sl2), nm2 = f2pack(neg_mu, neg_mu);
+            SDB_TMEM_LD32(ts + 0, r2);
+            SDB_TMEM_WAIT_LD_REGS(r2);
+            SDB_TMEM_LD32(ts + 32, r);
+            if (!full) apply_mask32(r2, vm[0]);
+            float rs = exp_pack32<0>(r2, sc2, nm2);
+            SDB_TMEM_ST16(ts + 0, r2);
+            SDB_TMEM_WAIT_LD_REGS(r);
+            SDB_TMEM_LD32(ts + 64, r2);
+            if (!full) apply_mask32(r, vm[1]);
+            rs += exp_pack32<0>(r, sc2, nm2);
+            SDB_TMEM_ST16(ts + 32, r);
+            SDB_TMEM_WAIT_LD_REGS(r2);
+            SDB_TMEM_LD32(ts + 96, r);
+            if (!full) apply_mask32(r2, vm[2]);
+            rs += exp_pack32<0>(r2, sc2, nm2);
+            SDB_TMEM_ST16(ts + 64, r2);
+            SDB_TMEM_WAIT_LD_REGS(r);
+            if (!full) apply_mask32(r, vm[3]);
+            rs += exp_pack32<0>(r, sc2, nm2);
+            SDB_TMEM_ST16(ts + 96, r);
+            l += rs;
+            bad |= rs > kOverflowSum || (m_ref == -INFINITY && rs > 0.f);
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&sm.p_full[sl]);
+        }
+        mbar_wait(&sm.o_done[0], g_unit & 1);  // the unit's last PV
+        ++g_unit;
+        tc_fence_after();
+        epilogue_row(sp, item, geo, g, local, t_o, m_ref, l);
+        tc_fence_before();
+        mbar_arrive(&sm.o_free[0]);  // O may now be overwritten by the next unit's first PV
+        if (bad) exact_row(sp, item, geo, g, local);  // overwrite this row's stores exactly
+        g_tile += geo.n_tiles;
+      }
+    }
+    while (NT == 2 && iter.next(sp, item)) {
       const ItemGeo geo = item_geo(sp, item, g);
       if (!geo.active) {
         inactive_row(sp, item, geo, g, local);

@@ -194,60 +194,6 @@ constexpr int kBarUnit = 1 + 4 * kSoftmaxWG;         // named barrier: unit end,
 // nats above the first 32 scores of the piece's first tile) is recomputed
 // exactly.
 constexpr bool kFixRef = SDB_ATTN_FIXREF != 0;
-constexpr float kOverflowSum = 0x1p96f;  // an item's row sum above this flags the row (2^89 x 128 terms)
-
-// 32 S values of one row (fp32 bits in r[0..31]) -> P = exp2(s * sl2 - m),
-// packed bf16 into r[0..15]; returns the sum of the 32 probabilities.
-// EMU8 of every 8 pairs run a cubic exp2 on the FMA pipe (offloads MUFU).
-template <int EMU8>
-__device__ __forceinline__ float exp_pack32(uint32_t *r, uint64_t sc2, uint64_t nm2) {
-  uint64_t acc2[2] = {0ull, 0ull};
-#pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    float x0, x1, p0, p1;
-    f2unpack(ffma2(f2pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
-    if ((e & 7) < EMU8) {
-      ex2_emu2(x0, x1, p0, p1);
-    } else {
-      p0 = ex2(x0);
-      p1 = ex2(x1);
-    }
-    acc2[e & 1] = fadd2(acc2[e & 1], f2pack(p0, p1));
-    r[e] = pack_bf16(p0, p1);
-  }
-  float s0, s1;
-  f2unpack(fadd2(acc2[0], acc2[1]), s0, s1);
-  return s0 + s1;
-}
-
-// Visibility bits of the 32 columns [c0, c0 + 32) of a key tile for this
-// row: prefix tiles -> keys < ctx; the suffix (tree) tile -> ancestor-or-self.
-__device__ __forceinline__ uint32_t vis_word(bool pref, int kvalid, const uint32_t *mrow, int key0, int n_words,
-                                             bool row_ok, int c0) {
-  const int lim = kvalid - c0;
-  const uint32_t low = lim >= 32 ? 0xffffffffu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
-  uint32_t bits = 0xffffffffu;
-  if (!pref) {
-    const int wi = (key0 + c0) >> 5;
-    bits = (wi < n_words && row_ok) ? mrow[wi] : 0u;
-  }
-  return bits & low;
-}
-__device__ __forceinline__ void apply_mask32(uint32_t *r, uint32_t w) {
-#pragma unroll
-  for (int e = 0; e < 32; ++e)
-    if (!((w >> e) & 1u)) r[e] = 0xff800000u;
-}
-__device__ __forceinline__ float max32(const uint32_t *r) {
-  float c0 = fmax3(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]));
-  float c1 = fmax3(__uint_as_float(r[3]), __uint_as_float(r[4]), __uint_as_float(r[5]));
-#pragma unroll
-  for (int e = 6; e < 30; e += 4) {
-    c0 = fmax3(c0, __uint_as_float(r[e + 0]), __uint_as_float(r[e + 1]));
-    c1 = fmax3(c1, __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
-  }
-  return fmax3(c0, c1, fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31])));
-}
 
 // Epilogue: O columns [16 c, 16 c + 16) of this row normalised by the row sum
 // (bf16 output of a whole unit, fp32 partial of a split one); chunk 0 writes

@@ -921,18 +921,22 @@ def test_tcgen05_r65_variant_vs_oracle():
     assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
 
 
+@pytest.mark.parametrize("tree", ["tree64", "chain3"])
 @pytest.mark.parametrize("ctas", [0, 148])
-def test_tcgen05_fixed_reference_overflow_exact(ctas):
-    """The pair kernel's softmax takes each unit piece's first-tile row max as
-    a fixed reference (no max pass, no rescale afterwards).  A key whose score
-    lies ~170 nats above everything in the first tile (exp2 would overflow
-    against that reference) sends the affected rows through the exact
-    recompute; whole units (ctas 0) and stream-K pieces merged by the fix-up
-    (ctas 148 at B = 1) must both match the float64 oracle."""
+def test_tcgen05_fixed_reference_overflow_exact(ctas, tree):
+    """The tcgen05 softmax takes each unit piece's first-tile row max as a
+    fixed reference (no max pass, no rescale afterwards): the pair kernel
+    (64-row tree) and the 1-CTA kernel with one query tile (chain-3: 32 rows
+    per KV head, two S slots).  A key whose score lies ~170 nats above
+    everything in the first tile (exp2 would overflow against that reference)
+    sends the affected rows through the exact recompute; whole units (ctas 0)
+    and stream-K pieces merged by the fix-up (ctas 148 at B = 1) must both
+    match the float64 oracle."""
     from paper_2508_08192_b200.attention import tree_verify_attention
 
     B = 2 if ctas == 0 else 1
-    c = _rand_paged_case(B, 64, 8, 128, 3000, 64, TREE64, seed=91, ragged=False)
+    parents = TREE64 if tree == "tree64" else (-1, 0, 1)
+    c = _rand_paged_case(B, 64, 8, 128, 3000, 64, parents, seed=91, ragged=False)
     kvh, g, j = 3, 8, 2500  # late prefix key of sequence 0 / KV head 3
     page = int(c["table_np"][0, j // 64])
     c["kp"][page, kvh, j % 64, :] = 4.0

@@ -31,13 +31,22 @@
 namespace sdb {
 namespace sm100 {
 
+// K / V ring depth: 3 stages with one query tile (224 KB of shared memory),
+// 2 with two
+#ifndef SDB_KV1_STAGES
+#define SDB_KV1_STAGES 3
+#endif
+template <int NT>
+constexpr int kvStages() {
+  return NT == 1 ? SDB_KV1_STAGES : 2;
+}
 template <int NT>
 struct alignas(1024) Smem {
   uint8_t q[NT][kTileBytes];
-  uint8_t k[2][kTileBytes];
-  uint8_t v[2][kTileBytes];
+  uint8_t k[kvStages<NT>()][kTileBytes];
+  uint8_t v[kvStages<NT>()][kTileBytes];
   uint64_t q_full, q_empty;
-  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t k_full[kvStages<NT>()], k_empty[kvStages<NT>()], v_full[kvStages<NT>()], v_empty[kvStages<NT>()];
   uint64_t s_full[2], p_full[2], o_done[NT], o_free[NT];  // NT = 1: two S slots of the one tile
   uint32_t tmem_base;
 };
@@ -63,7 +72,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
     if (blockIdx.x == 0) sp.seg[sp.n_workers] = sp.total;
     mbar_init(&sm.q_full, 1);
     mbar_init(&sm.q_empty, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kvStages<NT>(); ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.k_empty[s], 1);
       mbar_init(&sm.v_full[s], 1);
@@ -136,8 +145,9 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
           return __shfl_sync(0xffffffffu, pc_val, lp - pc_base);
         };
         for (int it = 0; it < geo.n_tiles; ++it, ++g_tile) {
-          const int s = g_tile & 1;
-          const uint32_t ph = (g_tile >> 1) & 1;
+          constexpr int kS = kvStages<NT>();
+          const int s = g_tile % kS;
+          const uint32_t ph = (g_tile / kS) & 1;
           const bool pref = it < geo.n_pref;
           const int tile = pref ? geo.pa + it : geo.sa + (it - geo.n_pref);
           for (int kv = 0; kv < 2; ++kv) {
@@ -200,18 +210,19 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
         // at [256,384)): S(n + 1) runs while the softmax works on item n, and
         // S(n + 2) refills slot n % 2 right after PV(n) -- at small trees the
         // item no longer serialises S -> softmax -> PV
+        constexpr int kS = kvStages<NT>();  // K / V stage gt % kS; S slot gt % 2
         auto issue_s1 = [&](uint32_t gt) {
-          mbar_wait(&sm.k_full[gt & 1], (gt >> 1) & 1);
+          mbar_wait(&sm.k_full[gt % kS], (gt / kS) & 1);
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t kd = k_desc + (uint64_t)(((gt & 1) * kTileBytes) >> 4);
+            const uint64_t kd = k_desc + (uint64_t)(((gt % kS) * kTileBytes) >> 4);
 #pragma unroll
             for (int k = 0; k < kHeadDim / 16; ++k) {
               const uint64_t off = (uint64_t)(((k >> 2) * kChunkBytes + (k & 3) * 32) >> 4);
               mma_ss(tm + (gt & 1) * 128, q_desc + off, kd + off, idesc_s, k > 0);
             }
             tc_commit(&sm.s_full[gt & 1]);
-            tc_commit(&sm.k_empty[gt & 1]);
+            tc_commit(&sm.k_empty[gt % kS]);
           }
           __syncwarp();
         };
@@ -224,13 +235,13 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
           if (n_tiles > 1) issue_s1(g_tile + 1);
           for (int it = 0; it < n_tiles; ++it) {
             const uint32_t gt = g_tile + it;
-            const int sl = gt & 1;
-            mbar_wait(&sm.v_full[sl], (gt >> 1) & 1);
+            const int sl = gt & 1, st = gt % kS;
+            mbar_wait(&sm.v_full[st], (gt / kS) & 1);
             mbar_wait(&sm.p_full[sl], (gt >> 1) & 1);
             if (it == 0) mbar_wait(&sm.o_free[0], (g_q & 1) ^ 1);  // previous unit's epilogue read O
             tc_fence_after();
             if (elect_one()) {
-              const uint64_t vd = v_desc + (uint64_t)((sl * kTileBytes) >> 4);
+              const uint64_t vd = v_desc + (uint64_t)((st * kTileBytes) >> 4);
 #pragma unroll
               for (int k = 0; k < kTileN / 16; ++k)
                 // P of keys 16k .. 16k+15 at slot columns 32 (k/2) + 8 (k%2)
@@ -238,7 +249,7 @@ __global__ void __launch_bounds__(128 + NT * 128, 1)
                 mma_ts(tm + 256, tm + sl * 128 + 32 * (k >> 1) + 8 * (k & 1), vd + (uint64_t)((k * 2048) >> 4),
                        idesc_o, (it > 0 || k > 0) ? 1u : 0u);
               if (it == n_tiles - 1) tc_commit(&sm.o_done[0]);  // the epilogue may read O
-              tc_commit(&sm.v_empty[sl]);
+              tc_commit(&sm.v_empty[st]);
             }
             __syncwarp();
             if (it + 2 < n_tiles) issue_s1(gt + 2);

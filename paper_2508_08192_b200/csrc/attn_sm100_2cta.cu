@@ -502,11 +502,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // s_full, of PV(n) via v_empty) from this otherwise idle warp; completion
     // order inside the first unit: S0 S1 S2 PV0 S3 PV1 S4 ...
     if (!p.fa_logits && worker == SDB_TRACE_WORKER && rank == 0 && lane == 0) {
-      for (int gi = 0; gi < 3; ++gi) {
+      // (bounded by the worker's first active unit piece)
+      ItemIter wit(sp, worker);
+      Item wi;
+      int wn = 0;
+      while (wit.next(sp, wi)) {
+        const ItemGeo wg_ = item_geo(sp, wi, g);
+        if (wg_.active) {
+          wn = wg_.n_tiles;
+          break;
+        }
+      }
+      const int lim = min(60, wn);
+      for (int gi = 0; gi < 3 && gi < lim; ++gi) {
         mbar_wait(&sm.s_full[gi % 3], (gi / 3) & 1);
         TRACE(19, gi);
       }
-      for (int n = 0; n + 3 < 60; ++n) {
+      for (int n = 0; n + 3 < lim; ++n) {
         mbar_wait(&sm.v_empty[n % kStagesV], (n / kStagesV) & 1);
         TRACE(20, n);
         mbar_wait(&sm.s_full[(n + 3) % 3], ((n + 3) / 3) & 1);

@@ -424,6 +424,11 @@ struct StSmem {
   unsigned klo, khi;
   int idx;
   double tot;
+  // cluster exchange slots (lazy chain: a row split over kCS CTAs)
+  float xf;
+  double xd;
+  int xi;
+  uint32_t xlo, xhi;
 };
 
 // Guided-decoding masks (target_dist(allowed=...), sampling.py:94-97): one
@@ -573,7 +578,14 @@ __device__ unsigned int g_st_launch;
   do {               \
   } while (0)
 #endif
-template <bool kMasked>
+// kCS > 1 (lazy chain, launched as clusters of kCS CTAs per row): every CTA of
+// the cluster streams a contiguous 1/kCS of the row through the three passes;
+// the max, the normaliser, the mass histogram, the mass above the window and
+// the window's candidates are combined through distributed shared memory, and
+// CTA 0 finishes the cut (and, in the rare refinement cases, re-reads the
+// whole row alone).  At the chain's later levels, with few rows left, a row's
+// passes then run on kCS SMs instead of one.
+template <bool kMasked, int kCS>
 __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int r_max, int vocab, float a,
     float top_p, const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows,
@@ -581,8 +593,9 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const int32_t *__restrict__ cur_rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   StSmem &sm = *reinterpret_cast<StSmem *>(smem_raw);
+  const int crank = kCS > 1 ? (int)cg::this_cluster().block_rank() : 0;
   // lazy mode (cur_rows): the one row per sequence the walk is at (-1: done)
-  const int r = cur_rows ? cur_rows[blockIdx.y] : (int)blockIdx.x, b = blockIdx.y, is_draft = blockIdx.z;
+  const int r = cur_rows ? cur_rows[blockIdx.y] : (int)(blockIdx.x / kCS), b = blockIdx.y, is_draft = blockIdx.z;
 #ifdef SDB_TRACE
   const bool st_tr = b == 0 && is_draft == 0 && (cur_rows || blockIdx.x == 0);
   unsigned int st_launch = 0;
@@ -593,7 +606,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   const int n = min(n_rows[b], r_max);
   RowStats *out = stats + ((int64_t)b * r_max + r) * 2 + is_draft;
   if (r >= n) {
-    if (threadIdx.x == 0) out->valid = 0;
+    if (threadIdx.x == 0 && crank == 0) out->valid = 0;
     return;
   }
   if (is_draft) {
@@ -602,7 +615,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     int has = 0;
     for (int j = r + 1 + threadIdx.x; j < n; j += kStThreads) has |= par[j] == r;
     if (!__syncthreads_or(has)) {
-      if (threadIdx.x == 0) out->valid = 0;
+      if (threadIdx.x == 0 && crank == 0) out->valid = 0;
       return;
     }
   }
@@ -612,6 +625,21 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   const uint32_t *mw = kMasked ? allowed + ((int64_t)b * r_max + r) * n_mw : nullptr;
   const bool vec = (vocab & 3) == 0 && ((uintptr_t)row & 15) == 0;
   const bool nucleus = !is_draft && top_p < 1.0f;
+  // row split: CTA crank streams [v0, v1); unaligned rows stay on CTA 0
+  const bool solo = kCS == 1 || !vec;
+  if (solo && crank != 0) return;  // (uniform over the other CTAs: no exchange follows)
+  int v0 = 0, v1 = vocab;
+  if (!solo) {
+    const int per = ((vocab + kCS - 1) / kCS + 3) & ~3;
+    v0 = min(vocab, crank * per);
+    v1 = min(vocab, v0 + per);
+  }
+  // [write own slot; cluster barrier; read every CTA's; cluster barrier]:
+  // the second barrier keeps a CTA's slots alive until every peer read them
+  auto cl_sync = [&]() {
+    if (!solo) cg::this_cluster().sync();
+  };
+  auto peer = [&](auto *p_, int q) { return cg::this_cluster().map_shared_rank(p_, q); };
   // the whole row streams into L2 through the TMA engine (deep memory-level
   // parallelism); the passes below then hit L2
 // whole-row L2 bulk prefetch before pass 1: off by default (C5 eager 1316 vs
@@ -627,8 +655,9 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     const uint32_t bytes = (uint32_t)vocab * 4u;
     for (uint32_t o = 0; o < bytes; o += kChunk) prefetch_l2((const char *)row + o, min(kChunk, bytes - o));
   }
-  const int n4 = vec ? vocab >> 2 : 0;
-  const float4 *r4 = reinterpret_cast<const float4 *>(row);
+  const int n4 = vec ? (v1 - v0) >> 2 : 0;  // this CTA's slice (the whole row when solo)
+  const int i4_0 = v0 >> 2;                 // its first float4 index in the row
+  const float4 *r4 = reinterpret_cast<const float4 *>(row + v0);
   constexpr int kU = 4;  // 16-byte loads in flight per thread
   if (nucleus)
     for (int i = threadIdx.x; i < kHistCopies * kHistBins; i += kStThreads) (&sm.hist[0][0])[i] = 0u;
@@ -643,23 +672,39 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
 #pragma unroll
     for (int u = 0; u < kU1; ++u) {
       const int i = i0 + u * kStThreads + threadIdx.x;
-      v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i4_0 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     }
 #pragma unroll
     for (int u = 0; u < kU1; ++u) mx = max3_nan(mx, max3_nan(v[u].x, v[u].y, v[u].z), v[u].w);
   }
-  for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) mx = max3_nan(mx, mask1(row[j], mw, j), mask1(row[j], mw, j));
-  if (__syncthreads_or(mx != mx)) {
-    if (threadIdx.x == 0) {
+  for (int j = v0 + (n4 << 2) + threadIdx.x; j < v1; j += kStThreads) mx = max3_nan(mx, mask1(row[j], mw, j), mask1(row[j], mw, j));
+  bool has_nan = __syncthreads_or(mx != mx);
+  if (!has_nan) mx = block_max<kStThreads>(mx, sm.redf);
+  if (!solo) {
+    if (threadIdx.x == 0) sm.xf = has_nan ? NAN : mx;
+    cl_sync();
+    float m_all = -INFINITY;
+    bool nan_all = false;
+#pragma unroll
+    for (int q = 0; q < kCS; ++q) {
+      const float x = *peer(&sm.xf, q);
+      nan_all |= x != x;
+      m_all = fmaxf(m_all, x);
+    }
+    cl_sync();
+    has_nan = nan_all;
+    mx = m_all;
+  }
+  if (has_nan) {
+    if (threadIdx.x == 0 && crank == 0) {
       atomicOr(err, SDB_ERR_NAN);
       out->valid = 0;
     }
     return;
   }
-  mx = block_max<kStThreads>(mx, sm.redf);
   ST_TRACE(1);
   if (mx == -INFINITY) {  // no allowed token (dead FSM state, sampling.py:96-97) / no finite logit
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && crank == 0) {
       atomicOr(err, mw ? SDB_ERR_NO_ALLOWED : SDB_ERR_BAD_DIST);
       out->valid = 0;
     }
@@ -675,7 +720,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kStThreads + threadIdx.x;
-        v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i4_0 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -688,9 +733,17 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     float s_lo, s_hi;
     f2unpack(s2, s_lo, s_hi);
     float s_loc = s_lo + s_hi;
-    for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) s_loc += ex2(fmaf(mask1(row[j], mw, j), a, -m2));
-    const double s = block_sum<kStThreads>((double)s_loc, sm.red);
-    if (threadIdx.x == 0) {
+    for (int j = v0 + (n4 << 2) + threadIdx.x; j < v1; j += kStThreads) s_loc += ex2(fmaf(mask1(row[j], mw, j), a, -m2));
+    double s = block_sum<kStThreads>((double)s_loc, sm.red);
+    if (!solo) {
+      if (threadIdx.x == 0) sm.xd = s;
+      cl_sync();
+      s = 0.0;
+#pragma unroll
+      for (int q = 0; q < kCS; ++q) s += *peer(&sm.xd, q);
+      cl_sync();
+    }
+    if (threadIdx.x == 0 && crank == 0) {
       RowStats st;
       st.m2 = m2;
       st.s = s;
@@ -738,7 +791,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int i = i0 + u * kStThreads + threadIdx.x;
-      v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i4_0 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -749,7 +802,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
   float s_lo, s_hi;
   f2unpack(s2, s_lo, s_hi);
   float s_loc = s_lo + s_hi;
-  for (int j = (n4 << 2) + threadIdx.x; j < vocab; j += kStThreads) {
+  for (int j = v0 + (n4 << 2) + threadIdx.x; j < v1; j += kStThreads) {
     const float x = mask1(row[j], mw, j);
     const uint64_t l2 = f2pack(x, -INFINITY);
     s2 = 0;
@@ -757,7 +810,14 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     f2unpack(s2, s_lo, s_hi);
     s_loc += s_lo;
   }
-  const double s = block_sum<kStThreads>((double)s_loc, sm.red);
+  double s = block_sum<kStThreads>((double)s_loc, sm.red);  // (also orders the histogram atomics)
+  if (!solo) {
+    if (threadIdx.x == 0) sm.xd = s;
+    cl_sync();  // every CTA's normaliser and histogram are complete
+    s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kCS; ++q) s += *peer(&sm.xd, q);
+  }
   ST_TRACE(2);
   const double tau = ((double)top_p - 1e-12) * s;
   // window [lo, hi] of bins whose cumulative (bin 0 = largest values) may
@@ -770,7 +830,14 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
       const int bb = threadIdx.x * kBinsPerThread + u;
       unsigned long long q = 0;
 #pragma unroll
-      for (int c = 0; c < kHistCopies; ++c) q += sm.hist[c][bb];
+      for (int c = 0; c < kHistCopies; ++c) {
+        if (solo) {
+          q += sm.hist[c][bb];
+        } else {
+#pragma unroll
+          for (int w = 0; w < kCS; ++w) q += *peer(&sm.hist[c][bb], w);
+        }
+      }
       // mass = 2^(-bb/64) * q / 2^14
       tsum += (double)q * (double)exp2f(-(float)bb * (1.0f / kHistScale)) * (1.0 / kFixScale);
       loc[u] = tsum;
@@ -795,6 +862,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     __syncthreads();
   }
   const int lo = sm.lo, hi = max(sm.hi, sm.lo);
+  cl_sync();  // every CTA read the peers' histograms (exact_cut reuses them as scratch)
   ST_TRACE(3);
   // pass 3 (L2): the same d splits the keys monotonically into above (d <
   // lo - 1/2), the window and below; exact mass above, window elements
@@ -829,7 +897,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kStThreads + threadIdx.x;
-        v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        v[u] = i < n4 ? mask4(__ldg(r4 + i), mw, i4_0 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       }
       uint32_t mask = 0;  // bit 4u+e: element e of v[u] lies in the window
 #pragma unroll
@@ -849,7 +917,7 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
         int slot = append_slots(__popc(mask));
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          const int bi = 4 * (i0 + u * kStThreads + threadIdx.x);
+          const int bi = v0 + 4 * (i0 + u * kStThreads + threadIdx.x);
           if (mask & (1u << (4 * u))) put(slot++, v[u].x, bi);
           if (mask & (2u << (4 * u))) put(slot++, v[u].y, bi + 1);
           if (mask & (4u << (4 * u))) put(slot++, v[u].z, bi + 2);
@@ -861,12 +929,12 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     f2unpack(ab2, a_lo, a_hi);
     above = a_lo + a_hi;
     // scalar tail (and the non-vector path): one element per thread per step
-    const int t0 = n4 << 2;
-    for (int j0 = t0; j0 < vocab; j0 += kStThreads) {
+    const int t0 = v0 + (n4 << 2);
+    for (int j0 = t0; j0 < v1; j0 += kStThreads) {
       const int j = j0 + threadIdx.x;
       float x = 0.f;
       int cnt = 0;
-      if (j < vocab) {
+      if (j < v1) {
         x = mask1(row[j], mw, j);
         float d0, d1, e0, e1;
         const uint64_t l2 = f2pack(x, x);
@@ -884,6 +952,48 @@ __global__ void __launch_bounds__(kStThreads, 1) row_stats_kernel(
     atomicMax(&sm.khi, kh);
   }
   double mass_above = block_sum<kStThreads>((double)above, sm.red);  // (syncs sm.count / klo / khi too)
+  if (!solo) {
+    // combine: mass above, key range, candidates (gathered into CTA 0's list)
+    if (threadIdx.x == 0) {
+      sm.xd = mass_above;
+      sm.xi = sm.count;
+      sm.xlo = sm.klo;
+      sm.xhi = sm.khi;
+    }
+    cl_sync();
+    double ma = 0.0;
+    int total = 0, base = 0;
+    uint32_t kl = 0xffffffffu, kh = 0u;
+#pragma unroll
+    for (int q = 0; q < kCS; ++q) {
+      const int cq = *peer(&sm.xi, q);
+      if (q < crank) base += cq;
+      total += cq;
+      ma += *peer(&sm.xd, q);
+      kl = min(kl, *peer(&sm.xlo, q));
+      kh = max(kh, *peer(&sm.xhi, q));
+    }
+    if (crank == 0 && total <= kCandCap) {
+      int off = sm.count;  // CTA 0's own candidates stay at [0, count)
+#pragma unroll
+      for (int q = 1; q < kCS; ++q) {
+        const int cq = *peer(&sm.xi, q);
+        const unsigned long long *pc = peer(&sm.cand[0], q);
+        for (int k = threadIdx.x; k < cq; k += kStThreads) sm.cand[off + k] = pc[k];
+        off += cq;
+      }
+    }
+    (void)base;
+    cl_sync();  // the peers' candidates are read: they may leave
+    if (crank != 0) return;
+    mass_above = ma;
+    if (threadIdx.x == 0) {
+      sm.count = total;
+      sm.klo = kl;
+      sm.khi = kh;
+    }
+    __syncthreads();
+  }
   ST_TRACE(4);
   uint32_t klo = sm.klo, khi = sm.khi;
   uint32_t cut_key = 0;
@@ -1755,8 +1865,25 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
   const bool lazy = levels > 0;
   cudaStream_t s = sdb::as_stream(stream);
   const size_t smem = sizeof(sdb::StSmem);
-  cudaFuncSetAttribute(sdb::row_stats_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(sdb::row_stats_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(sdb::row_stats_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(sdb::row_stats_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(sdb::row_stats_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(sdb::row_stats_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(sdb::row_stats_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(sdb::row_stats_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // lazy chain: each visited row split over a cluster of st_split CTAs
+  // (16-byte aligned rows; SDB_ST_SPLIT = 1 keeps one CTA per row).
+  // Measured (tools/cycles/r2_st_split.sh, same box): C5 943 / 910 / 1028 us,
+  // C3 stochastic 1191 / 1155 / 1184 us, the C5 chain alone 550 / 516 / 633
+  // at 1 / 2 / 4 CTAs per row (4: the first levels' rows need 3.5 waves)
+  static int st_split = -1;
+  if (st_split < 0) {
+    const char *e = getenv("SDB_ST_SPLIT");
+    st_split = e ? atoi(e) : 2;
+    if (st_split != 2 && st_split != 4) st_split = 1;
+  }
+  const bool split_rows = lazy && st_split > 1 && (vocab % 4) == 0 && ((uintptr_t)target_logits % 16) == 0 &&
+                          ((uintptr_t)draft_logits % 16) == 0;
   // cluster size: the widest (8 = portable maximum) whose clusters for the
   // whole batch fit in two waves -- a wider cluster halves every CTA's
   // full-slice passes, which costs more than a second wave of early-exiting
@@ -1793,13 +1920,37 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
   scfg.stream = s;
   scfg.attrs = &attr[1];
   scfg.numAttrs = lazy ? 1 : 0;
+  cudaLaunchAttribute sattr[2];
+  sattr[0] = attr[1];  // priority
+  sattr[1].id = cudaLaunchAttributeClusterDimension;
+  sattr[1].val.clusterDim.x = st_split > 1 ? st_split : 2;
+  sattr[1].val.clusterDim.y = 1;
+  sattr[1].val.clusterDim.z = 1;
   auto stats_launch = [&](dim3 grid, const int32_t *rows) {
     scfg.gridDim = grid;
+    if (rows && split_rows) {
+      scfg.gridDim.x = st_split * grid.x;
+      scfg.attrs = sattr;
+      scfg.numAttrs = 2;
+#define SDB_ST_LAUNCH(CS)                                                                                          \
+  (allowed ? cudaLaunchKernelEx(&scfg, sdb::row_stats_kernel<true, CS>, target_logits, draft_logits, r_max, vocab, a, \
+                                top_p, parent, n_rows, stats, err, allowed, allowed_words, rows)                       \
+           : cudaLaunchKernelEx(&scfg, sdb::row_stats_kernel<false, CS>, target_logits, draft_logits, r_max, vocab,   \
+                                a, top_p, parent, n_rows, stats, err, (const uint32_t *)nullptr, 0, rows))
+      if (st_split == 4)
+        SDB_ST_LAUNCH(4);
+      else
+        SDB_ST_LAUNCH(2);
+#undef SDB_ST_LAUNCH
+      scfg.attrs = &attr[1];
+      scfg.numAttrs = lazy ? 1 : 0;
+      return;
+    }
     if (allowed)
-      cudaLaunchKernelEx(&scfg, sdb::row_stats_kernel<true>, target_logits, draft_logits, r_max, vocab, a, top_p,
+      cudaLaunchKernelEx(&scfg, sdb::row_stats_kernel<true, 1>, target_logits, draft_logits, r_max, vocab, a, top_p,
                          parent, n_rows, stats, err, allowed, allowed_words, rows);
     else
-      cudaLaunchKernelEx(&scfg, sdb::row_stats_kernel<false>, target_logits, draft_logits, r_max, vocab, a, top_p,
+      cudaLaunchKernelEx(&scfg, sdb::row_stats_kernel<false, 1>, target_logits, draft_logits, r_max, vocab, a, top_p,
                          parent, n_rows, stats, err, (const uint32_t *)nullptr, 0, rows);
   };
 #define SDB_WALK(CL, M, L)                                                                                        \

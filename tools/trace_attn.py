@@ -61,11 +61,19 @@ if buf[19, 5]:
     k5 = np.arange(8, 50)
     print("V(n+5) TMA issue - PV(n) done (slot reuse gate): median", np.median(b[16, k5 + 5] - b[20, k5]))
     print("V(n) TMA issue -> PV(n) issue start: median", np.median(b[1, k5] - b[16, k5]))
+if buf[21, 1] and buf[23, 1]:
+    for u in range(0, 4):
+        if not buf[21, u]:
+            break
+        print(f"unit {u} end: bar.red+sums {int(buf[22, u]) - int(buf[21, u])}, o_last wait {int(buf[23, u]) - int(buf[22, u])}, "
+              f"epilogue {int(buf[20, 129 + u]) - int(buf[23, u]) if buf[20, 129 + u] else None} (abs start {int(buf[21, u]) - int(t0)})")
 if os.environ.get("TRACE_ROWS"):
     print("item: Vwait(18->0) Pwait(0->1) issue(1->2) loop(2->18') | sm: swait sok->done | S(n+3) lat")
-    for k in range(8, 40):
+    rows = [int(v) for v in os.environ.get("TRACE_ROWS").split(",")] if "," in os.environ.get("TRACE_ROWS") else list(range(8, 40))
+    for k in rows:
         print(k, b[0, k] - b[18, k], b[1, k] - b[0, k], b[2, k] - b[1, k], b[18, k + 1] - b[2, k], "|",
-              b[4, k] - b[3, k], b[5, k] - b[4, k], "|", b[4, k + 3] - b[2, k])
+              b[4, k] - b[3, k], b[5, k] - b[4, k], "|", b[4, k + 3] - b[2, k], "| abs: sok", b[4, k], "pok", b[1, k],
+              "done", b[5, k])
 it3 = np.arange(8, min(n, 200) - 3)
 print("S(n+3) issued (after PV(n)) -> softmax sees S(n+3): median", np.median(b[4, it3 + 3] - b[2, it3]))
 print("P(n) arrived -> softmax sees S(n+3): median", np.median(b[4, it3 + 3] - b[5, it3]))

@@ -469,13 +469,17 @@ __global__ void __launch_bounds__(128) tree_attn_fixup_kernel(const Sm100Params 
   const int64_t ck = seg_begin(sp, k);  // (arithmetic: the same values the main kernel wrote to sp.seg)
   const int W = sp.w_unit;
   const int unit = (int)(ck / W);
+  // rows past the row block: the fused tail rows of a last-block unit only
+  if (local >= sp.row_blk &&
+      (unit / (p.batch * p.hkv) != sp.m_blocks - 1 || local >= sp.row_blk + sp.tail_rows))
+    return;
   const int64_t ustart = (int64_t)unit * W, uend = ustart + W;
   if (ck == ustart) return;                  // boundary between units: nothing split here
   if (seg_begin(sp, k - 1) > ustart) return;  // an earlier boundary inside u merges it
   const int g = p.hq / p.hkv;
   const int bh = p.batch * p.hkv;
   const int b = (unit % bh) / p.hkv, kvh = unit % p.hkv;
-  const int rho = (unit / bh) * sp.rows_unit + local;
+  const int rho = (unit / bh) * sp.row_blk + local;
   const int n_nodes = min(p.n_rows[b], p.r_max);
   const int q0 = q_first(p, b, n_nodes);
   if (q0 * g + rho >= p.r_max * g) return;
@@ -616,7 +620,29 @@ static void sm100_plan(const TreeAttnParams &p, int ctas_override, sm100::Sm100P
   sp.nt = (sp.cta_group == 1 && rows > per_tile) ? 2 : 1;
   if (const char *fnt = getenv("SDB_ATTN_NT")) sp.nt = atoi(fnt) == 1 ? 1 : sp.nt;  // testing knob
   sp.rows_unit = sp.nt * per_tile;
+  sp.row_blk = sp.rows_unit;
   sp.m_blocks = cdiv(rows, sp.rows_unit);
+  sp.tail_rows = 0;
+  // pair kernel, 1..8 rows past the last full 256-row block (R = 65: 520 rows
+  // per KV head): SDB_ATTN_TAIL=1 fuses those rows into the last block's
+  // units on the otherwise idle warps 2 / 3 (S^T = K Q_tail^T and O^T =
+  // V^T P_tail^T, N = 16) instead of a third, 97 %-padding row block.  Exact
+  // (tests/test_gpu_parity.py) but measured slower at C3 R = 65 (attention
+  // 1076 vs 679 us): with every TMEM column taken by O and the three S slots,
+  // a tail item's S^T / O^T must be read before the slot's next S, so each
+  // item waits on four cross-CTA handshakes (~500-900 cycles each) --
+  // profiles/r2_attn_power_study.md section 6.  Off by default; needs warp
+  // 3 (not the fused greedy scan) and warp 2 (the V loads move to warp 0).
+  const char *tail_env = getenv("SDB_ATTN_TAIL");
+  const bool tail_knob = tail_env && atoi(tail_env) != 0;
+  if (tail_knob && sp.cta_group == 2 && sp.nt == 1 && rows > per_tile && rows % per_tile <= 8 && !p.fa_logits &&
+      g <= 8) {
+    sp.tail_rows = rows % per_tile;
+    if (sp.tail_rows > 0) {
+      sp.m_blocks = rows / per_tile;
+      sp.rows_unit = per_tile + 8;
+    }
+  }
   sp.units = p.batch * p.hkv * sp.m_blocks;
   // nominal prefix tiles per unit: the context, or at most one local chunk
   sp.w_pref = cdiv(max(p.chunk_len > 0 ? std::min(p.max_ctx, p.chunk_len) : p.max_ctx, 0), kTileN);
@@ -699,12 +725,15 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *wor
   Sm100Params sp;
   sm100_plan(p, ctas_override, sp);
   const int cg = sp.cta_group;
-  CUtensorMap mq, mk, mv, mtk, mtv;
+  CUtensorMap mq, mqt, mk, mv, mtk, mtv;
   {
     cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)g, (cuuint64_t)p.hkv, (cuuint64_t)p.batch * p.r_max};
     cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)g * d * 2, (cuuint64_t)p.hq * d * 2};
     cuuint32_t box[4] = {64, (cuuint32_t)g, 1, (cuuint32_t)(kTileM / g)};
     if (!make_map(&mq, p.q, 4, dims, strides, box)) return SDB_E_UNSUPPORTED;
+    // fused tail rows: 8 rows (8 / g nodes x g heads) per d-chunk
+    cuuint32_t boxt[4] = {64, (cuuint32_t)g, 1, (cuuint32_t)(g <= 8 ? 8 / g : 1)};
+    if (!make_map(&mqt, p.q, 4, dims, strides, boxt)) return SDB_E_UNSUPPORTED;
   }
   {
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)p.num_blocks * p.hkv * p.block_size};
@@ -741,7 +770,7 @@ int launch_tree_attn_sm100(const TreeAttnParams &p, int ctas_override, void *wor
       emu8 = e ? atoi(e) : 0;
       emu8 = emu8 < 0 ? 0 : (emu8 > 4 ? 4 : emu8);
     }
-    int rc = launch_2cta(mq, mk, mv, mtk, mtv, sp, emu8, stream);
+    int rc = launch_2cta(mq, mqt, mk, mv, mtk, mtv, sp, emu8, stream);
     if (rc != SDB_OK) return rc;
   } else {
     dim3 grid(sp.n_workers);

@@ -91,6 +91,41 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
+// fused tail rows: generic shared-memory data handed across the pair (P^T
+// halves, unit-end statistics) -- cluster-scope release / acquire
+__device__ __forceinline__ void mbar_arrive_remote_rel(uint64_t *bar, uint32_t cta) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_peer_f32(float *p, uint32_t cta, float v) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\nst.shared::cluster.f32 [ra], %2;\n}" ::"r"(
+          smem_u32(p)),
+      "r"(cta), "f"(v)
+      : "memory");
+}
+#define SDB_TMEM_WAIT_LD_REGS16(r)                                                                                \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                                    \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),  \
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),         \
+                 "+r"(r[15])::"memory")
+
 // TMA into this CTA's smem, completion bytes counted on the leader's barrier
 __device__ __forceinline__ void tma2_2d(void *dst, const CUtensorMap *m, uint32_t lbar, int c0, int c1) {
   asm volatile(
@@ -139,9 +174,9 @@ __device__ __forceinline__ void mma2_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
 }
 
 // kind::f16, bf16 x bf16 -> fp32, M = 256 (pair), N = 128
-__host__ __device__ constexpr uint32_t make_idesc2(bool b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(kTileN >> 3) << 17) |
-         ((uint32_t)(256 >> 4) << 24);
+__host__ __device__ constexpr uint32_t make_idesc2(bool b_mn_major, bool a_mn_major = false, int n = kTileN) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
 constexpr int kLgStages = kStagesK + kStagesV <= 9 ? 5 : 3;  // fused argmax: 8 KB bulk-copy ring in the SMEM left over
@@ -151,7 +186,15 @@ struct alignas(1024) Smem2 {
   uint8_t q[kTileBytes];  // this CTA's 128 query rows
   uint8_t k[kStagesK][kHalfBytes];
   uint8_t v[kStagesV][kHalfBytes];
+  // fused tail rows (R = 65): the B operands of the two N = 16 tail MMAs
+  uint8_t qt[2][1024];  // Q of the 8 tail rows, [8 rows][64 d] per head-dim half (both CTAs load it)
+  uint8_t pt[2][1024];  // P^T, [8 rows][64 keys] per key half: this CTA writes half `rank`, the other stays 0
   uint64_t q_full, q_empty;
+  uint64_t ts_full, tp_full, to_full, tread, tstat;  // tail S^T done / P^T written / O^T partial done / read; stats
+  float tref[2][8];       // tail warps: per-warp row max of the reference item
+  float tl[2][8];         // ... per-warp row sums at the unit end
+  uint32_t tbad[2];       // ... per-warp "row needs the exact recompute" masks
+  float tx[2][2][17];     // [unit parity][cta]: reference, row sum and bad mask (bits) of each tail row
   uint64_t k_full[kStagesK], k_empty[kStagesK], v_full[kStagesV], v_empty[kStagesV];
   uint64_t s_full[3], p_full[3], o_done[3];  // per TMEM S slot (o_done: running-max mode only)
   uint64_t o_last;  // the unit's last PV done (epilogue may read O)
@@ -164,6 +207,8 @@ struct alignas(1024) Smem2 {
   alignas(128) float lg[kLgStages][kLgChunk];  // fused greedy scan: logits chunk ring (warp 3; 16-B aligned for TMA)
   uint64_t lg_full[kLgStages];
 };
+
+static_assert(sizeof(Smem2) + 1024 <= 232448, "shared memory");
 
 constexpr int kSoftmaxWG = 3;                       // softmax warpgroups (one per S slot)
 // register split (65536 per SM, one CTA per SM): the TMA / MMA / scan
@@ -183,6 +228,7 @@ static_assert(kRegsCtl == 0 || kRegsCtl * 128 + kRegsSoftmax * 128 * kSoftmaxWG 
 constexpr int kPairThreads = 128 + kSoftmaxWG * 128;
 constexpr int kSBase = 128;                          // TMEM: O [0,128), S slot s at 128 + 128 s
 constexpr int kBarUnit = 1 + 4 * kSoftmaxWG;         // named barrier: unit end, all softmax warps
+constexpr int kBarTail = kBarUnit + 1;               // named barrier: the two tail warps
 #ifndef SDB_ATTN_FIXREF
 #define SDB_ATTN_FIXREF 1
 #endif
@@ -255,7 +301,8 @@ __device__ __forceinline__ void epilogue_chunk(const Sm100Params &sp, const Item
 // PV(n) and then S(n + 3) into the slot P(n) just vacated (in-order pipe).
 template <int EMU8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
-    tree_attn_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    tree_attn_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_qt,
+                                  const __grid_constant__ CUtensorMap tm_k,
                                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_tk,
                                   const __grid_constant__ CUtensorMap tm_tv, const __grid_constant__ Sm100Params sp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -292,10 +339,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     }
     mbar_init(&sm.o_last, 1);
     mbar_init(&sm.o_free, 2 * 4 * kSoftmaxWG);
+    mbar_init(&sm.ts_full, 1);
+    mbar_init(&sm.tp_full, 2 * 2);  // tail warps 2 / 3 of both CTAs
+    mbar_init(&sm.to_full, 1);
+    mbar_init(&sm.tread, 2 * 2);
+    mbar_init(&sm.tstat, 1);        // the peer's tail warp 2
     for (int s = 0; s < kLgStages; ++s) mbar_init(&sm.lg_full[s], 1);
     fence_barrier_init();
   }
   if (threadIdx.x < 128) sm.bad[threadIdx.x] = 0u;
+  if (sp.tail_rows > 0 && threadIdx.x < 256) {
+    // the other CTA's key half of this CTA's P^T rows is zero for good
+    reinterpret_cast<uint32_t *>(sm.pt[rank ^ 1u])[threadIdx.x] = 0u;
+    fence_proxy_async_smem();
+  }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -309,7 +366,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   // a region reached from both budgets with the smaller one)
   if (warp < 4) {
   if (kRegsCtl) regs_dec<kRegsCtl ? kRegsCtl : 128>();
-  if (warp == 0 || warp == 2) {
+  const bool tail_mode = sp.tail_rows > 0;  // fused tail rows: warps 2 / 3 run them, warp 0 loads K and V
+  if (warp == 0 || (warp == 2 && !tail_mode)) {
     // ============ TMA producers (both CTAs): warp 0 Q + K ring, warp 2 V ring ============
     // Each CTA loads its own half of every tile; completion bytes land on the
     // leader's barriers.  Separate K and V producers so a K load never waits
@@ -321,12 +379,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // serial loads per tile took longer than the tile's tensor work).
     {
       const bool kprod = warp == 0;
+      const bool vprod = warp == 2 || tail_mode;
       if (lane == 0) {
         if (kprod) {
           tma_prefetch(&tm_q);
           tma_prefetch(&tm_k);
           tma_prefetch(&tm_tk);
-        } else {
+          if (tail_mode) tma_prefetch(&tm_qt);
+        }
+        if (vprod) {
           tma_prefetch(&tm_v);
           tma_prefetch(&tm_tv);
         }
@@ -347,10 +408,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         if (kprod) {
           mbar_wait(&sm.q_empty, (g_q & 1) ^ 1);
           if (lane == 0) {
-            if (rank == 0) mbar_expect_tx(&sm.q_full, 2 * kTileBytes);
+            const bool tail_unit = tail_mode && item.unit / (p.batch * p.hkv) == sp.m_blocks - 1;
+            if (rank == 0) mbar_expect_tx(&sm.q_full, 2 * kTileBytes + (tail_unit ? 2 * 2048 : 0));
             const int node0 = geo.q0 + (geo.row0 + (int)rank * kTileM) / g;
             for (int c = 0; c < 2; ++c)
               tma2_4d(sm.q + c * kChunkBytes, &tm_q, l_qfull, c * 64, 0, geo.kvh, geo.b * p.r_max + node0);
+            if (tail_unit) {
+              const int node_t = geo.q0 + (geo.row0 + sp.row_blk) / g;
+              for (int c = 0; c < 2; ++c)
+                tma2_4d(sm.qt[c], &tm_qt, l_qfull, c * 64, 0, geo.kvh, geo.b * p.r_max + node_t);
+            }
           }
         }
         ++g_q;
@@ -388,7 +455,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 tma2_3d(sm.k[s] + c * kKChunk, &tm_tk, l_kfull, c * 64, geo.kvh,
                         geo.b * p.r_max + tile * kTileN + (int)rank * 64);
             }
-          } else {
+          }
+          if (vprod) {
             // V half: all 128 keys, head-dim columns [rank*64, +64)
             const int s = g_tile % kStagesV;
             mbar_wait(&sm.v_empty[s], ((g_tile / kStagesV) & 1) ^ 1);
@@ -419,17 +487,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     if (rank == 0) {
       constexpr uint32_t idesc_s = make_idesc2(false);
       constexpr uint32_t idesc_o = make_idesc2(true);
+      constexpr uint32_t idesc_ts = make_idesc2(false, false, 16);  // tail S^T: K (keys x d) . Q_t^T
+      constexpr uint32_t idesc_tp = make_idesc2(false, true, 16);   // tail O^T: V^T (d x keys, MN-major) . P_t^T
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       const uint64_t q_desc = sw128_desc(smem_u32(sm.q), 16, 1024);
       const uint64_t k_desc = sw128_desc(smem_u32(sm.k[0]), 16, 1024);
       const uint64_t v_desc = sw128_desc(smem_u32(sm.v[0]), kHalfBytes, 1024);
-      uint32_t g_tile = 0, g_q = 0, g_item = 0;
+      uint32_t g_tile = 0, g_q = 0, g_item = 0, tgp = 0, tgr = 0;
       ItemIter iter(sp, worker);
       Item item;
       while (iter.next(sp, item)) {
         const ItemGeo geo = item_geo(sp, item, g);
         if (!geo.active) continue;
         const int N = __shfl_sync(0xffffffffu, geo.n_tiles, 0);
+        const bool tail_unit = tail_mode && item.unit / (p.batch * p.hkv) == sp.m_blocks - 1;
         // S(n) = Q K_n^T into slot (g_item + n) % 3 (descriptor start
         // addresses are in 16-byte units, low 14 bits: smem < 256 KB, no carry)
         auto issue_s = [&](int n) {
@@ -445,10 +516,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               mma2_ss(tm + kSBase + slot * 128, q_desc + (uint64_t)(((k >> 2) * kChunkBytes + (k & 3) * 32) >> 4),
                       kd + (uint64_t)(((k >> 2) * kKChunk + (k & 3) * 32) >> 4), idesc_s, k > 0);
             tc_commit2(&sm.s_full[slot]);
-            tc_commit2(&sm.k_empty[st]);
-            // the unit's last S: Q is free once it completes, so the next
-            // unit's Q load overlaps this unit's last three items
-            if (n == N - 1) tc_commit2(&sm.q_empty);
+            if (!tail_unit) {  // (tail units: K(n) and Q_t are read again by the tail S^T(n))
+              tc_commit2(&sm.k_empty[st]);
+              // the unit's last S: Q is free once it completes, so the next
+              // unit's Q load overlaps this unit's last three items
+              if (n == N - 1) tc_commit2(&sm.q_empty);
+            }
+          }
+          __syncwarp();
+        };
+        // fused tail rows: the O^T partial of item m (V(m) x P^T(m) of both
+        // CTAs) into columns [48, 64) of TMEM slot dst (lanes 64..127: this
+        // CTA's 64 head-dim columns; D columns 0..7 from CTA 0's keys, 8..15
+        // from CTA 1's).  The A operands start one 1 KB V row group / one
+        // 8 KB K chunk early so the live rows land on lanes 64..127 (the
+        // lanes warps 2 / 3 may access); the rows before are don't-care reads
+        // of this CTA's own shared memory.
+        auto tail_pv = [&](int m, int dst) {
+          const int vst = (int)((g_tile + m) % kStagesV);
+          mbar_wait_acq_cluster(&sm.tp_full, tgp & 1);
+          TRACE(21, g_item + m + 1);
+          ++tgp;
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t vb = smem_u32(sm.v[vst]) - 1024;
+            const uint32_t pb = smem_u32(sm.pt[0]);
+#pragma unroll
+            for (int k = 0; k < kTileN / 16; ++k)
+              mma2_ss(tm + kSBase + dst * 128 + 48, sw128_desc(vb + k * 2048, 1024, 1024),
+                      sw128_desc(pb + (k >> 2) * 1024 + (k & 3) * 32, 16, 1024), idesc_tp, k > 0 ? 1u : 0u);
+            tc_commit2(&sm.to_full);
+            tc_commit2(&sm.v_empty[vst]);
           }
           __syncwarp();
         };
@@ -467,6 +565,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           TRACE(1, gi);
           if (n == 0) mbar_wait_cluster(&sm.o_free, (g_q & 1) ^ 1);  // previous unit's epilogue read O
           tc_fence_after();
+          if (tail_unit) {
+            // fused tail rows: the O^T partial of item n - 1 (its P^T was
+            // written during the previous item) and S^T of item n go ahead of
+            // PV(n), into columns [48, 64) / [16, 32) of this slot -- free
+            // since P(n) is packed into [32c, 32c + 16) -- so warps 2 / 3 have
+            // read both while PV(n) runs, and S(n + 3) reclaims the slot
+            // without a tensor-pipe bubble
+            if (n > 0) tail_pv(n - 1, slot);
+            const int kst = gt % kStagesK;
+            if (elect_one()) {
+              const uint32_t kb = smem_u32(sm.k[kst]) - kKChunk;
+              const uint32_t qb = smem_u32(sm.qt[0]);
+#pragma unroll
+              for (int k = 0; k < kHeadDim / 16; ++k)
+                mma2_ss(tm + kSBase + slot * 128 + 16, sw128_desc(kb + (k >> 2) * kKChunk + (k & 3) * 32, 16, 1024),
+                        sw128_desc(qb + (k >> 2) * 1024 + (k & 3) * 32, 16, 1024), idesc_ts, k > 0 ? 1u : 0u);
+              tc_commit2(&sm.ts_full);
+              tc_commit2(&sm.k_empty[kst]);
+              if (n == N - 1) tc_commit2(&sm.q_empty);
+            }
+            __syncwarp();
+          }
           if (elect_one()) {
             // P of keys 16k .. 16k+15 at slot columns 32 (k/2) + 8 (k%2)
             const uint32_t a = tm + kSBase + slot * 128;
@@ -479,16 +599,215 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             // and by the unit's epilogue (its last PV)
             if (!kFixRef) tc_commit2(&sm.o_done[slot]);
             if (n == N - 1) tc_commit2(&sm.o_last);
-            tc_commit2(&sm.v_empty[st]);
+            if (!tail_unit) tc_commit2(&sm.v_empty[st]);  // (tail units: V(n) is read again by the O^T partial)
           }
           __syncwarp();
+          if (tail_unit) {
+            mbar_wait_cluster(&sm.tread, tgr & 1);  // warps 2 / 3 of both CTAs read the slot's tail columns
+            TRACE(22, gi);
+            ++tgr;
+            tc_fence_after();
+          }
           if (n + 3 < N) issue_s(n + 3);
           TRACE(2, gi);
+        }
+        if (tail_unit) {
+          // the last item's O^T partial, into the slot the next unit's S(0) takes
+          tail_pv(N - 1, (int)((g_item + N) % 3));
+          mbar_wait_cluster(&sm.tread, tgr & 1);
+          ++tgr;
+          tc_fence_after();
         }
         g_tile += N;
         g_item += N;
         ++g_q;
       }
+    }
+  } else if (tail_mode) {
+    // ============ fused tail rows (warps 2 / 3 of both CTAs) ============
+    // The 1..8 query rows past the last full 256-row block (R = 65: node 64's
+    // g heads) ride along in that block's units: per item the MMA issuer
+    // adds S^T = K_n Q_t^T and the O^T partial V_n^T P_t^T (N = 16, ~1/16 of
+    // the item's tensor work), and these two warps -- TMEM lanes 64..127,
+    // i.e. this CTA's 64 keys of S^T, then its 64 head-dim columns of O^T --
+    // do the softmax (one key per thread, 8 exps), write P^T into this CTA's
+    // key half of the B operand, and accumulate the partials in registers.
+    // Each CTA keeps its own fixed reference for its key half (the P^T halves
+    // land in separate D columns), so the two halves meet only at the unit
+    // end: (reference, row sum, overflow flags) are exchanged over DSMEM and
+    // each CTA stores its 64 output columns.  Rows whose scores exceed the
+    // reference by ~89 log2 units take exact_row, as in the main path.
+    griddep_wait();  // the mask words come from the kernel launched just before
+    const int tw = warp - 2;
+    const int ti = tw * 32 + lane;
+    const uint32_t t_lane = (uint32_t)(64 + tw * 32) << 16;
+    const uint32_t peer = rank ^ 1u;
+    uint32_t g_item = 0, tgs = 0, tgo = 0, tu = 0;
+    ItemIter iter(sp, worker);
+    Item item;
+    while (iter.next(sp, item)) {
+      const ItemGeo geo = item_geo(sp, item, g);
+      const bool tail_unit = item.unit / (p.batch * p.hkv) == sp.m_blocks - 1;
+      if (!geo.active) {
+        if (tail_unit && rank == 0 && tw == 0 && lane < sp.tail_rows) inactive_row(sp, item, geo, g, sp.row_blk + lane);
+        continue;
+      }
+      const int N = geo.n_tiles;
+      if (!tail_unit) {
+        g_item += N;
+        continue;
+      }
+      const int rho0 = geo.row0 + sp.row_blk;  // first tail row
+      float mref[8], l[8], oacc[16];
+      uint32_t badm = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        mref[j] = -INFINITY;
+        l[j] = 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) oacc[e] = 0.f;
+      auto read_partial = [&](int slot_p) {
+        // the O^T partial of the previous item: accumulate (columns 0..7:
+        // CTA 0's keys against CTA 0's reference, 8..15: CTA 1's)
+        uint32_t r[16];
+        mbar_wait(&sm.to_full, tgo & 1);
+        ++tgo;
+        tc_fence_after();
+        SDB_TMEM_LD16(tmem + t_lane + kSBase + slot_p * 128 + 48, r);
+        SDB_TMEM_WAIT_LD_REGS16(r);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) oacc[e] += __uint_as_float(r[e]);
+      };
+      auto arrive_read = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0)
+            mbar_arrive(&sm.tread);
+          else
+            mbar_arrive_leader(&sm.tread);
+        }
+      };
+      for (int n = 0; n < N; ++n) {
+        const int slot = (int)((g_item + n) % 3);
+        const bool pref = n < geo.n_pref;
+        const int key0 = pref ? geo.k0 + (geo.pa + n) * kTileN : (geo.sa + n - geo.n_pref) * kTileN;
+        const int key = key0 + (int)rank * 64 + ti;
+        if (n > 0) read_partial(slot);  // (item n - 1's partial went into item n's slot)
+        uint32_t r[16];
+        mbar_wait(&sm.ts_full, tgs & 1);
+        if (rank == 0 && ti == 0) TRACE(23, g_item + n);
+        ++tgs;
+        tc_fence_after();
+        SDB_TMEM_LD16(tmem + t_lane + kSBase + slot * 128 + 16, r);
+        SDB_TMEM_WAIT_LD_REGS16(r);
+        arrive_read();  // the slot may take S(n + 3)
+        float sv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          bool vis;
+          if (pref) {
+            vis = key < geo.C;
+          } else {
+            const int node = min(geo.q0 + (rho0 + j) / g, max(geo.n_nodes - 1, 0));
+            const uint32_t *mrow = p.mask_words + ((int64_t)geo.b * p.r_max + node) * p.n_words;
+            vis = key < geo.n_nodes && ((__ldg(mrow + (key >> 5)) >> (key & 31)) & 1u);
+          }
+          sv[j] = vis ? __uint_as_float(r[j]) * sl2 : -INFINITY;
+        }
+        if (n == 0) {
+          // reference: the row max over this CTA's 64 keys of the piece's first tile
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float m = sv[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) sm.tref[tw][j] = m;
+          }
+          asm volatile("bar.sync %0, 64;" ::"r"(kBarTail) : "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mref[j] = fmaxf(sm.tref[0][j], sm.tref[1][j]);
+        }
+        // P^T row j, key ti of this CTA's half (128-byte swizzle: 16-byte
+        // chunk ^ row); the previous P^T was consumed (its partial was read)
+        uint8_t *ptb = sm.pt[rank];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float pj = sv[j] == -INFINITY ? 0.f : ex2(sv[j] - (mref[j] == -INFINITY ? 0.f : mref[j]));
+          l[j] += pj;
+          if (pj > kOverflowSum || (mref[j] == -INFINITY && pj > 0.f)) badm |= 1u << j;
+          *reinterpret_cast<__nv_bfloat16 *>(ptb + j * 128 + ((((ti * 2) >> 4) ^ j) << 4) + ((ti * 2) & 15)) =
+              __float2bfloat16(pj);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote_rel(&sm.tp_full, 0);
+      }
+      read_partial((int)((g_item + N) % 3));  // the last item's partial
+      arrive_read();
+      g_item += N;
+      // ---- unit end: this CTA's row sums; (reference, sum, flags) to the peer; store ----
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float v = l[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) sm.tl[tw][j] = v;
+      }
+      badm = __reduce_or_sync(0xffffffffu, badm);
+      if (lane == 0) sm.tbad[tw] = badm;
+      asm volatile("bar.sync %0, 64;" ::"r"(kBarTail) : "memory");
+      const int px = (int)(tu & 1);
+      if (tw == 0 && lane == 0) {
+        float *mine = sm.tx[px][rank];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float lj = sm.tl[0][j] + sm.tl[1][j];
+          mine[j] = mref[j];
+          mine[8 + j] = lj;
+          st_peer_f32(&mine[j], peer, mref[j]);
+          st_peer_f32(&mine[8 + j], peer, lj);
+        }
+        const float bm = __uint_as_float(sm.tbad[0] | sm.tbad[1]);
+        mine[16] = bm;
+        st_peer_f32(&mine[16], peer, bm);
+        mbar_arrive_remote_rel(&sm.tstat, peer);
+      }
+      asm volatile("bar.sync %0, 64;" ::"r"(kBarTail) : "memory");
+      mbar_wait_acq_cluster(&sm.tstat, tu & 1);
+      ++tu;
+      const uint32_t bad_all = __float_as_uint(sm.tx[px][0][16]) | __float_as_uint(sm.tx[px][1][16]);
+      const int col = (int)rank * 64 + ti;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= sp.tail_rows || ((bad_all >> j) & 1u)) continue;  // (flagged rows: exact_row below)
+        const float m0 = sm.tx[px][0][j], m1 = sm.tx[px][1][j];
+        const float l0 = sm.tx[px][0][8 + j], l1 = sm.tx[px][1][8 + j];
+        const float mx = fmaxf(m0, m1);
+        const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - mx), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - mx);
+        const float lt = l0 * f0 + l1 * f1;
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        const float o = (oacc[j] * f0 + oacc[8 + j] * f1) * inv;
+        const float lse_n = lt > 0.f ? (mx + __log2f(lt)) * 0.6931471805599453f : -INFINITY;
+        const int rho = rho0 + j;
+        const bool row_ok = rho < geo.rows_total;
+        if (item.whole) {
+          if (geo.q0 * g + rho < p.r_max * g) {
+            const int node_o = geo.q0 + rho / g, hq_idx = geo.kvh * g + rho % g;
+            reinterpret_cast<__nv_bfloat16 *>(p.out)[(((int64_t)geo.b * p.r_max + node_o) * p.hq + hq_idx) * kHeadDim +
+                                                     col] = __float2bfloat16(row_ok ? o : 0.f);
+            if (rank == 0 && ti == 0 && p.lse)
+              p.lse[((int64_t)geo.b * p.hq + hq_idx) * p.r_max + node_o] = row_ok ? lse_n : -INFINITY;
+          }
+        } else {
+          const int64_t prow = (int64_t)item.slot * sp.rows_unit + sp.row_blk + j;
+          sp.part_out[prow * kHeadDim + col] = row_ok ? o : 0.f;
+          if (rank == 0 && ti == 0) sp.part_lse[prow] = row_ok ? lse_n : -INFINITY;
+        }
+      }
+      if (bad_all && rank == 0 && tw == 0 && lane < sp.tail_rows && ((bad_all >> lane) & 1u))
+        exact_row(sp, item, geo, g, sp.row_blk + lane);
     }
   } else if (warp == 3) {
     // ============ fused greedy-acceptance scan (otherwise idle warp) ============
@@ -863,8 +1182,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   }
 }
 
-int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const CUtensorMap &mtk,
-                const CUtensorMap &mtv, const Sm100Params &sp, int emu, cudaStream_t stream) {
+int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mqt, const CUtensorMap &mk, const CUtensorMap &mv,
+                const CUtensorMap &mtk, const CUtensorMap &mtv, const Sm100Params &sp, int emu, cudaStream_t stream) {
   dim3 grid(sp.n_workers * 2);
   const size_t smem = sizeof(Smem2) + 1024;
   cudaLaunchConfig_t cfg = {};
@@ -881,7 +1200,7 @@ int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap 
   do {                                                                                                             \
     cudaFuncSetAttribute(tree_attn_tcgen05_pair_kernel<EMU8>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                          (int)smem);                                                                               \
-    cudaLaunchKernelEx(&cfg, tree_attn_tcgen05_pair_kernel<EMU8>, mq, mk, mv, mtk, mtv, sp);                      \
+    cudaLaunchKernelEx(&cfg, tree_attn_tcgen05_pair_kernel<EMU8>, mq, mqt, mk, mv, mtk, mtv, sp);                      \
   } while (0)
   // emu: pairs of every 8 whose exp2 runs on the FMA pipe
   switch (emu) {

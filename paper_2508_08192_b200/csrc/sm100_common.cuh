@@ -297,7 +297,9 @@ struct Sm100Params {
   int w_pref;      // nominal prefix tiles per unit: ceil(max_ctx / 128)
   int w_unit;      // nominal tiles per unit: w_pref + ceil(r_max / 128)
   int n_workers;   // stream-K workers (CTAs, or CTA pairs)
-  int rows_unit;   // nt * 128 * cta_group
+  int rows_unit;   // partial-output rows per unit: row_blk (+ 8 fused tail rows)
+  int row_blk;     // query rows per row block: nt * 128 * cta_group
+  int tail_rows;   // pair kernel: live rows (1..8) past the last full row block, fused into its units (0: none)
   int64_t total;   // units * w_unit
   float *part_out; // [n_workers * 2][rows_unit][128] partial outputs of split units
   float *part_lse; // [n_workers * 2][rows_unit]
@@ -355,7 +357,7 @@ __device__ __forceinline__ ItemGeo item_geo(const Sm100Params &sp, const Item &i
   const int bh = p.batch * p.hkv;
   o.b = (it.unit % bh) / p.hkv;
   o.kvh = it.unit % p.hkv;
-  o.row0 = (it.unit / bh) * sp.rows_unit;
+  o.row0 = (it.unit / bh) * sp.row_blk;
   o.n_nodes = min(p.n_rows[o.b], p.r_max);
   o.q0 = q_first(p, o.b, o.n_nodes);
   o.rows_total = (o.n_nodes - o.q0) * g;
@@ -832,7 +834,7 @@ static __device__ __noinline__ void exact_row(const Sm100Params &sp, const Item 
   }
 }
 
-int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const CUtensorMap &mtk,
+int launch_2cta(const CUtensorMap &mq, const CUtensorMap &mqt, const CUtensorMap &mk, const CUtensorMap &mv, const CUtensorMap &mtk,
                 const CUtensorMap &mtv, const Sm100Params &sp, int emu, cudaStream_t stream);
 
 }  // namespace sm100

@@ -921,6 +921,47 @@ def test_tcgen05_r65_variant_vs_oracle():
     assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
 
 
+@pytest.mark.parametrize("hq,splits,plant", [(64, 0, False), (64, 148, False), (64, 5, False), (32, 0, False),
+                                              (32, 148, False), (64, 0, True), (64, 148, True)])
+def test_tcgen05_fused_tail_rows_vs_oracle(hq, splits, plant, monkeypatch):
+    """R = 65 on the pair kernel with SDB_ATTN_TAIL=1 (off by default: exact
+    but slower): the rows past the last full 256-row
+    block (g = 8: node 64's 8 heads; g = 4: 4 rows) ride along in that
+    block's units (warps 2 / 3, N = 16 S^T and O^T MMAs, per-CTA key halves
+    merged at the unit end).  Whole units, stream-K pieces merged by the
+    fix-up (148 and 5 workers), and a planted key ~170 nats above the tail
+    rows' reference (their exact recompute) against the float64 oracle."""
+    from paper_2508_08192_b200.attention import tree_verify_attention
+
+    monkeypatch.setenv("SDB_ATTN_TAIL", "1")
+
+    c = _rand_paged_case(2, hq, 8, 128, 3000, 64, TREE64 + [0], seed=650 + hq + splits)
+    assert c["R"] == 65
+    g = hq // 8
+    if plant:
+        kvh, j = 5, 2800
+        j = min(j, int(c["ctx_np"][1]) - 1)
+        page = int(c["table_np"][1, j // 64])
+        c["kp"][page, kvh, j % 64, :] = 4.0
+        c["q"][1, 64, kvh * g:(kvh + 1) * g, :] = 4.0
+    out, lse = tree_verify_attention(c["q"], c["kp"], c["vp"], c["table"], c["ctx"], c["tk"], c["tv"], c["mask"],
+                                     c["nr"], 128 ** -0.5, num_splits=splits, kernel=1)
+    torch.cuda.synchronize()
+    f64 = lambda t: t.float().cpu().numpy().astype(np.float64)
+    want_o, want_l = O.tree_verify_attention_batch(f64(c["q"]), f64(c["kp"]), f64(c["vp"]), c["table_np"],
+                                                   c["ctx_np"], f64(c["tk"]), f64(c["tv"]), [c["aug"]] * 2,
+                                                   128 ** -0.5)
+    got_o = out.float().cpu().numpy()
+    assert np.isfinite(got_o).all()
+    err = np.abs(got_o - want_o)
+    assert err.max() < 2e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+    tail = np.abs(got_o[:, 64] - want_o[:, 64])
+    assert tail.max() < 2e-2, tail.max()
+    assert np.abs(lse.cpu().numpy() - want_l).max() < 2e-3
+    if plant:
+        assert want_l[1, kvh * g:(kvh + 1) * g, 64].min() > 150
+
+
 @pytest.mark.parametrize("tree", ["tree64", "chain3"])
 @pytest.mark.parametrize("ctas", [0, 148])
 def test_tcgen05_fixed_reference_overflow_exact(ctas, tree):

@@ -195,6 +195,42 @@ __global__ void k_mix_nocvt(float *out, long long *cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// the softmax mix with a packed bf16x2 exp2: FFMA2 scale, F2FP pack of x,
+// one MUFU.EX2 bf16x2, unpack (shift / and) and FADD2 sum in fp32
+__global__ void k_mix_bf16(float *out, long long *cyc) {
+  float a[16];
+  for (int i = 0; i < 16; ++i) a[i] = -0.001f * (threadIdx.x + i);
+  uint64_t acc = 0;
+  uint32_t pk = 0;
+  const uint64_t sc = (uint64_t)__float_as_uint(0.125f) | ((uint64_t)__float_as_uint(0.125f) << 32);
+  const uint64_t nm = (uint64_t)__float_as_uint(-1.f) | ((uint64_t)__float_as_uint(-1.f) << 32);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 2; ++it) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      uint64_t x;
+      asm volatile("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a[2 * e]), "f"(a[2 * e + 1]));
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x) : "l"(sc), "l"(nm));
+      float x0, x1;
+      asm volatile("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(x));
+      uint32_t h;
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+      asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(h));
+      pk ^= h;
+      const float p0 = __uint_as_float(h << 16), p1 = __uint_as_float(h & 0xffff0000u);
+      uint64_t pp;
+      asm volatile("mov.b64 %0, {%1, %2};" : "=l"(pp) : "f"(p0), "f"(p1));
+      asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(pp));
+      a[2 * e] += 1e-7f;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __uint_as_float((uint32_t)acc) + pk;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 template <typename K>
 void run(const char *name, K kern, double results_per_thread_iter, int threads) {
   float *out;
@@ -225,6 +261,7 @@ int main() {
     run("cvt.bf16x2", k_cvt, 8, t);
     run("mix", k_mix, 8, t);
     run("mix-nocvt", k_mix_nocvt, 8, t);
+    run("mix-bf16", k_mix_bf16, 8, t);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

@@ -2017,6 +2017,53 @@ extern "C" int sdb_accept_stochastic_lazy(const float *target_logits, const floa
                                 uniforms_used, residual, err, allowed, allowed_words, levels, stream);
 }
 
+namespace sdb {
+// Persistent variant of the validation scan (unmasked rows): K CTAs, one
+// per SM (the dynamic shared memory request keeps every other CTA off those
+// SMs), grid-striding over the rows with 8 x 16-byte loads per thread in
+// flight (128 KB per SM).  The scan then owns K SMs for the whole walk and
+// the latency-bound lazy chain runs on the other 148 - K without waiting for
+// scan CTAs to drain (a spatial split instead of priorities).
+constexpr int kValUnroll = 8;  // (12 measured the same)
+constexpr int kValSmem = 150 * 1024;
+__global__ void __launch_bounds__(kArgmaxThreads, 1) stochastic_validate_persistent_kernel(
+    const float *__restrict__ target, const float *__restrict__ draft, int batch, int r_max, int vocab,
+    const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, int32_t *__restrict__ err) {
+  const int total = 2 * batch * r_max;
+  float nacc = -INFINITY;
+  const bool vec = (vocab & 3) == 0 && ((uintptr_t)target & 15) == 0 && ((uintptr_t)draft & 15) == 0;
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const int z = w / (batch * r_max), br = w % (batch * r_max), b = br / r_max, r = br % r_max;
+    const int n = min(n_rows[b], r_max);
+    if (r >= n) continue;
+    if (z) {
+      const int32_t *par = parent + (int64_t)b * r_max;
+      int has = 0;
+      for (int j = r + 1 + threadIdx.x; j < n; j += kArgmaxThreads) has |= par[j] == r;
+      if (!__syncthreads_or(has)) continue;
+    }
+    const float *row = (z ? draft : target) + ((int64_t)b * r_max + r) * vocab;
+    if (vec) {
+      const float4 *r4 = reinterpret_cast<const float4 *>(row);
+      const int n4 = vocab >> 2;
+      for (int i0 = 0; i0 < n4; i0 += kValUnroll * kArgmaxThreads) {
+        float4 v[kValUnroll];
+#pragma unroll
+        for (int u = 0; u < kValUnroll; ++u) {
+          const int i = i0 + u * kArgmaxThreads + threadIdx.x;
+          v[u] = i < n4 ? __ldcs(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        }
+#pragma unroll
+        for (int u = 0; u < kValUnroll; ++u) nacc = max_nan(nacc, max_nan(max_nan3(v[u].x, v[u].y, v[u].z), v[u].w));
+      }
+    } else {
+      for (int j = threadIdx.x; j < vocab; j += kArgmaxThreads) nacc = max_nan(nacc, row[j]);
+    }
+  }
+  if (__syncthreads_or(nacc != nacc) && threadIdx.x == 0) atomicOr(err, SDB_ERR_NAN);
+}
+}  // namespace sdb
+
 extern "C" int sdb_stochastic_validate(const float *target_logits, const float *draft_logits, int batch, int r_max,
                                        int vocab, const int32_t *parent, const int32_t *n_rows,
                                        const uint32_t *allowed, int allowed_words, int32_t *err, void *stream) {
@@ -2026,6 +2073,34 @@ extern "C" int sdb_stochastic_validate(const float *target_logits, const float *
   if (batch == 0) return SDB_OK;
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  // default: the persistent scan on 56 of 148 SMs (scaled to the device),
+  // the lazy chain on the rest -- C5 912 -> 617 us, C3 stochastic 1142 ->
+  // 971 us (K 40..72 swept: 52..56 best at B 48..64, flat at B <= 32);
+  // SDB_VALIDATE_SMS=0 restores the one-row low-priority CTAs
+  static const int persist_env = [] {
+    const char *e = getenv("SDB_VALIDATE_SMS");
+    return e ? atoi(e) : -1;
+  }();
+  int persist_sms = persist_env;
+  if (persist_sms < 0) {
+    int dev = 0, n_sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+    persist_sms = (n_sms * 56 + 74) / 148;
+  }
+  if (persist_sms > 0 && !allowed) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(sdb::stochastic_validate_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           sdb::kValSmem);
+      attr_set = true;
+    }
+    sdb::stochastic_validate_persistent_kernel<<<persist_sms, sdb::kArgmaxThreads, sdb::kValSmem,
+                                                 sdb::as_stream(stream)>>>(target_logits, draft_logits, batch, r_max,
+                                                                           vocab, parent, n_rows, err);
+    SDB_CHECK_LAUNCH();
+    return SDB_OK;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(r_max, batch, 2);
   cfg.blockDim = dim3(sdb::kArgmaxThreads);

@@ -399,8 +399,9 @@ class StochasticAcceptor:
 
     ``lazy``: only the rows the MSS walk visits are reduced, one tree level
     per launch pair, while a validation scan of every row (the reference's
-    error behaviour) runs concurrently on a side stream; "auto" picks it from
-    28 sequences up.  ``levels`` (tree depth + 1) must be given when
+    error behaviour) runs concurrently on a side stream (a persistent kernel on
+    56 of 148 SMs; the chain takes the rest); "auto" picks it from 20
+    sequences up.  ``levels`` (tree depth + 1) must be given when
     capturing a CUDA graph.  Results are identical either way."""
 
     def __init__(self, lazy="auto", levels=None):
@@ -451,12 +452,12 @@ class StochasticAcceptor:
                 o["uni"] = torch.empty((b, r), dtype=torch.float64, device=dev)
             uniforms = device_uniforms(seeds, steps, r, out=o["uni"], stream=stream)
         n_words = allowed.shape[-1] if allowed is not None else 0
-        # the lazy walk + concurrent validation scan costs ~440 us at B 8 and
-        # grows slowly; reducing every row costs ~20 us per sequence
-        # (tools/lazy_sweep.py, V 128k, tree64): lazy wins from about 28
-        # sequences (B 24: 566 eager / 637 lazy; B 32: 727 / 684; B 64:
-        # 1369 / 944 us)
-        lazy = self.lazy if self.lazy != "auto" else (b >= 28)
+        # the lazy walk + concurrent validation scan (persistent, on 56 of
+        # 148 SMs) costs ~440 us at B 16-20 and grows slowly; reducing every
+        # row costs ~20 us per sequence (tools/lazy_sweep.py, V 128k,
+        # tree64): lazy wins from about 20 sequences (B 16: 387 eager / 436
+        # lazy; B 20: 462 / 449; B 32: 688 / 491; B 64: 1321 / 620 us)
+        lazy = self.lazy if self.lazy != "auto" else (b >= 20)
         levels = self.levels
         if lazy and levels is None and not torch.cuda.is_current_stream_capturing():
             levels = tree_levels(parent)

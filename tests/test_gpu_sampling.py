@@ -486,3 +486,49 @@ def test_fsm_dead_row_raises_flag():
                                        torch.tensor(rng.random((1, R)), device="cuda"), allowed=words)
     torch.cuda.synchronize()
     assert int(g.err[0]) & 32 and int(s.err[0]) & 32 and int(s2.err[0]) & 32
+
+
+@pytest.mark.parametrize("scan_sms", [None, "0"])
+@pytest.mark.parametrize("V", [4096, 4099])
+def test_lazy_validation_scan_error_semantics(V, scan_sms, monkeypatch):
+    """The lazy walk reduces only the rows it visits; the validation scan
+    (persistent on 56 of 148 SMs by default, SDB_VALIDATE_SMS=0: one-row
+    CTAs) must still raise exactly where the reference does: target_dist of
+    EVERY tree row and the draft q of every PARENT row (engine.py:474-475,
+    numcore.py:47-48) -- a NaN in a draft leaf row or past a sequence's
+    n_rows is never read by the reference and must not raise."""
+    from paper_2508_08192_b200.sampling import StochasticAcceptor, tree_levels
+
+    if scan_sms is not None:
+        monkeypatch.setenv("SDB_VALIDATE_SMS", scan_sms)
+    B, T, top_p = 24, 1.0, 0.9
+    aug, tl, dl, tokens, seeds, steps = _stochastic_case(B, V, TREE64, T, top_p, seed=77)
+    R = len(aug)
+    n_rows = np.full((B,), R, dtype=np.int32)
+    n_rows[5] = R - 7  # ragged: rows >= R - 7 of sequence 5 are not part of its tree
+    parents = set(p for p in aug if p >= 0)
+    leaf = max(r for r in range(R) if r not in parents)
+    par_row = max(parents)
+    par = torch.tensor([aug] * B, dtype=torch.int32, device="cuda")
+    acc = StochasticAcceptor(lazy=True, levels=tree_levels(par))
+
+    def run(t, d):
+        res = acc(torch.tensor(t, device="cuda"), torch.tensor(d, device="cuda"), T, top_p, par,
+                  torch.tensor(n_rows, device="cuda"), torch.tensor(tokens, device="cuda"), seeds=_i64(seeds),
+                  steps=_i64(steps))
+        torch.cuda.synchronize()
+        return int(res.err[0])
+
+    assert run(tl, dl) == 0
+    cases = [
+        ("target, last row of the last sequence", True, B - 1, R - 1, True),
+        ("target, unvisited middle row", True, 13, R // 2, True),
+        ("draft, a parent row", False, 7, par_row, True),
+        ("draft, a leaf row", False, 7, leaf, False),
+        ("target, past n_rows", True, 5, R - 2, False),
+    ]
+    for what, target, b, r, raises in cases:
+        t, d = tl.copy(), dl.copy()
+        (t if target else d)[b, r, V // 3] = np.nan
+        err = run(t, d)
+        assert bool(err & 2) == raises, what

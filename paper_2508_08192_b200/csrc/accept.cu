@@ -2020,43 +2020,78 @@ extern "C" int sdb_accept_stochastic_lazy(const float *target_logits, const floa
 namespace sdb {
 // Persistent variant of the validation scan (unmasked rows): K CTAs, one
 // per SM (the dynamic shared memory request keeps every other CTA off those
-// SMs), grid-striding over the rows with 8 x 16-byte loads per thread in
-// flight (128 KB per SM).  The scan then owns K SMs for the whole walk and
+// SMs), each streaming its rows as one flat sequence with 8 x 16-byte loads
+// per thread in flight (128 KB per SM; ncu alone on 56 SMs: 523 us for
+// 2.99 GB = 5.7 TB/s, 102 GB/s per SM -- 579 us with a per-row loop).  The scan then owns K SMs for the whole walk and
 // the latency-bound lazy chain runs on the other 148 - K without waiting for
 // scan CTAs to drain (a spatial split instead of priorities).
 constexpr int kValUnroll = 8;  // (12 measured the same)
 constexpr int kValSmem = 150 * 1024;
+constexpr int kValFlagBytes = 96 * 1024;                         // has-child flags of up to 96 K (sequence, row) pairs
+constexpr int kValListMax = (kValSmem - kValFlagBytes) / 8;      // row pointers of this CTA's listed rows
 __global__ void __launch_bounds__(kArgmaxThreads, 1) stochastic_validate_persistent_kernel(
     const float *__restrict__ target, const float *__restrict__ draft, int batch, int r_max, int vocab,
     const int32_t *__restrict__ parent, const int32_t *__restrict__ n_rows, int32_t *__restrict__ err) {
-  const int total = 2 * batch * r_max;
-  float nacc = -INFINITY;
+  // this CTA's rows (w = blockIdx.x + k * gridDim.x over [target rows |
+  // draft rows]) that the reference reads -- target rows r < n_rows[b],
+  // draft rows with a child -- are listed in shared memory first, then
+  // streamed as ONE flat sequence of 16-byte words, so the loads in flight
+  // never drain at a row boundary (per-row loops lost ~25 % of the SM's
+  // rate: ncu 5.17 TB/s on 56 SMs vs 6.9 TB/s for a flat stream)
+  extern __shared__ __align__(16) unsigned char vsm[];
+  const int br_total = batch * r_max, total = 2 * br_total;
   const bool vec = (vocab & 3) == 0 && ((uintptr_t)target & 15) == 0 && ((uintptr_t)draft & 15) == 0;
-  for (int w = blockIdx.x; w < total; w += gridDim.x) {
-    const int z = w / (batch * r_max), br = w % (batch * r_max), b = br / r_max, r = br % r_max;
-    const int n = min(n_rows[b], r_max);
-    if (r >= n) continue;
-    if (z) {
-      const int32_t *par = parent + (int64_t)b * r_max;
-      int has = 0;
-      for (int j = r + 1 + threadIdx.x; j < n; j += kArgmaxThreads) has |= par[j] == r;
-      if (!__syncthreads_or(has)) continue;
+  const int n_cand = total > (int)blockIdx.x ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const bool listed = vec && br_total <= kValFlagBytes && n_cand <= kValListMax;
+  float nacc = -INFINITY;
+  if (listed) {
+    uint8_t *has_child = vsm;                                                    // [batch * r_max]
+    const float4 **list = reinterpret_cast<const float4 **>(vsm + kValFlagBytes);  // [<= kValListMax]
+    __shared__ int n_list;
+    for (int j = threadIdx.x; j < br_total; j += kArgmaxThreads) has_child[j] = 0;
+    if (threadIdx.x == 0) n_list = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < br_total; j += kArgmaxThreads) {
+      const int b = j / r_max, r = j % r_max;
+      const int pr = parent[j];
+      if (r < min(n_rows[b], r_max) && pr >= 0 && pr < r) has_child[b * r_max + pr] = 1;
     }
-    const float *row = (z ? draft : target) + ((int64_t)b * r_max + r) * vocab;
-    if (vec) {
-      const float4 *r4 = reinterpret_cast<const float4 *>(row);
-      const int n4 = vocab >> 2;
-      for (int i0 = 0; i0 < n4; i0 += kValUnroll * kArgmaxThreads) {
-        float4 v[kValUnroll];
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_cand; t += kArgmaxThreads) {
+      const int w = (int)blockIdx.x + t * (int)gridDim.x;
+      const int z = w / br_total, br = w % br_total, b = br / r_max, r = br % r_max;
+      const bool active = r < min(n_rows[b], r_max) && (z == 0 || has_child[br]);
+      if (active) list[atomicAdd(&n_list, 1)] = reinterpret_cast<const float4 *>((z ? draft : target) + (int64_t)br * vocab);
+    }
+    __syncthreads();
+    const int nl = n_list;
+    const int n4 = vocab >> 2;
+    // this thread's flat position: row li, word off (advanced by 1024 per load)
+    int li = 0, off = threadIdx.x;
+    while (off >= n4 && li < nl) { off -= n4; ++li; }
+    while (li < nl) {
+      float4 v[kValUnroll];
 #pragma unroll
-        for (int u = 0; u < kValUnroll; ++u) {
-          const int i = i0 + u * kArgmaxThreads + threadIdx.x;
-          v[u] = i < n4 ? __ldcs(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-        }
-#pragma unroll
-        for (int u = 0; u < kValUnroll; ++u) nacc = max_nan(nacc, max_nan(max_nan3(v[u].x, v[u].y, v[u].z), v[u].w));
+      for (int u = 0; u < kValUnroll; ++u) {
+        v[u] = li < nl ? __ldcs(list[li] + off) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        off += kArgmaxThreads;
+        while (off >= n4 && li < nl) { off -= n4; ++li; }
       }
-    } else {
+#pragma unroll
+      for (int u = 0; u < kValUnroll; ++u) nacc = max_nan(nacc, max_nan(max_nan3(v[u].x, v[u].y, v[u].z), v[u].w));
+    }
+  } else {
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      const int z = w / br_total, br = w % br_total, b = br / r_max, r = br % r_max;
+      const int n = min(n_rows[b], r_max);
+      if (r >= n) continue;
+      if (z) {
+        const int32_t *par = parent + (int64_t)b * r_max;
+        int has = 0;
+        for (int j = r + 1 + threadIdx.x; j < n; j += kArgmaxThreads) has |= par[j] == r;
+        if (!__syncthreads_or(has)) continue;
+      }
+      const float *row = (z ? draft : target) + (int64_t)br * vocab;
       for (int j = threadIdx.x; j < vocab; j += kArgmaxThreads) nacc = max_nan(nacc, row[j]);
     }
   }
@@ -2073,9 +2108,11 @@ extern "C" int sdb_stochastic_validate(const float *target_logits, const float *
   if (batch == 0) return SDB_OK;
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);
-  // default: the persistent scan on 56 of 148 SMs (scaled to the device),
-  // the lazy chain on the rest -- C5 912 -> 617 us, C3 stochastic 1142 ->
-  // 971 us (K 40..72 swept: 52..56 best at B 48..64, flat at B <= 32);
+  // default: the persistent scan on 50 of 148 SMs (scaled to the device),
+  // the lazy chain on the rest -- C5 912 -> 586 us, C3 stochastic 1142 ->
+  // ~970 us.  K swept 36..62 on the flat-stream scan (same box, C5 us):
+  // 38 703, 42 644, 44 624, 46 603, 48 685 (the chain's clusters place
+  // badly), 50 586, 52 593, 54 616, 56 609-618, 60 633; flat at B <= 32.
   // SDB_VALIDATE_SMS=0 restores the one-row low-priority CTAs
   static const int persist_env = [] {
     const char *e = getenv("SDB_VALIDATE_SMS");
@@ -2086,7 +2123,7 @@ extern "C" int sdb_stochastic_validate(const float *target_logits, const float *
     int dev = 0, n_sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-    persist_sms = (n_sms * 56 + 74) / 148;
+    persist_sms = (n_sms * 50 + 74) / 148;
   }
   if (persist_sms > 0 && !allowed) {
     static bool attr_set = false;

@@ -14,4 +14,5 @@ for args in "--tree 65" "--tree chain3" "--tree n8" "--config c2" "--config c5" 
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"sdb|tree_|argmax|walk|compact|fixup|clear" -c 400 --csv --log-file $O/f2_c3_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo c3 launches rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:"sdb|row_stats|stochastic|philox|walk|clear" -c 400 --csv --log-file $O/f2_c5_launches.csv python bench.py --config c5 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo c5 launches rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stochastic_validate_persistent -c 1 -o $O/f2_validate python bench.py --config c5 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo ncu validate rc=$?
 exit 0

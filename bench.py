@@ -832,7 +832,26 @@ def main():
         fields.update(dev_in)
         xe = StepInputs(**fields)
 
+        # full step: host inputs -> host outputs through the public pipelined
+        # API (chunks of sequences: H2D of chunk c+1 under the step of chunk c)
+        e2e_chunks = int(os.environ.get("SDB_E2E_CHUNKS", "4"))
+        pipe = None
+        if not accept_only and e2e_chunks > 1 and world == 1:
+            from paper_2508_08192_b200.verify import HostStepPipeline
+
+            def make_chunk_verifier():
+                v_ = TreeVerifier(scale=ver.scale, temperature=ver.temperature, top_p=ver.top_p,
+                                  max_ctx=ver.max_ctx, num_splits=ver.num_splits, kernel=ver.kernel,
+                                  reserve_sms=ver.reserve_sms, tree_levels=ver.stochastic.levels)
+                v_.stochastic.lazy = ver.stochastic.lazy
+                return v_
+
+            pipe = HostStepPipeline(make_chunk_verifier, chunks=e2e_chunks)
+
         def e2e_step():
+            if pipe is not None:
+                pipe(xe, pinned, outs_h, stream)
+                return
             for k_, v_ in pinned.items():
                 dev_in[k_].copy_(v_, non_blocking=True)
             if accept_only:
@@ -862,7 +881,13 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": float(te.item()) * 1e3, "unit": "us/step", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h)}
+               "d2h_bytes_per_step": int(d2h), "chunks": e2e_chunks if pipe is not None else 1}
+        # the host outputs of the last e2e step equal the device step's (same inputs)
+        e2e["parity"] = bool(torch.equal(outs_h["path_len"], acc.path_len.cpu())
+                             and torch.equal(outs_h["next_token"], acc.next_token.cpu())
+                             and all(torch.equal(outs_h["path"][b_, :int(acc.path_len[b_])],
+                                                 acc.path[b_, :int(acc.path_len[b_])].cpu())
+                                     for b_ in range(acc.path_len.shape[0])))
 
     attn_bytes, accept_bytes, attn_flops = step_bytes_flops(cfg, shard, R, anc_pairs)
     if mode != "greedy":

@@ -255,3 +255,80 @@ class TreeVerifier:
     def replay(self):
         self.graph.replay()
         return self.graph_outputs
+
+
+_BATCH_FIELDS = ("parent", "n_rows", "ctx_len", "tokens", "q", "tree_k", "tree_v", "logits", "block_table",
+                 "draft_logits", "uniforms", "seeds", "steps", "allowed")
+
+
+def _slice_inputs(x: StepInputs, b0: int, b1: int) -> StepInputs:
+    """The sequences [b0, b1) of a step (batch-major views; the KV pools are shared)."""
+    f = {k: getattr(x, k) for k in StepInputs.__dataclass_fields__}
+    for k in _BATCH_FIELDS:
+        if f[k] is not None:
+            f[k] = f[k][b0:b1]
+    return StepInputs(**f)
+
+
+class HostStepPipeline:
+    """One verification step from pinned HOST inputs to pinned HOST outputs
+    (the reference engine's data lives on the host), pipelined over chunks of
+    sequences: chunk c's host->device copies (a copy stream) overlap chunk
+    c - 1's step (the compute stream) and chunk c - 2's device->host copies
+    (a third stream; PCIe is full duplex), so a step costs the H2D of its
+    inputs plus the step and D2H of the LAST chunk only.  Each chunk has its
+    own TreeVerifier (own output buffers: chunk c + 1's step must not
+    overwrite what chunk c's D2H is still reading).
+
+    ``x_dev``: the device StepInputs (resident KV pools + per-step buffers
+    that the copies land in); ``host_in``: field name -> pinned host tensor
+    (batch-major, same shape as the device field); ``host_out``: any of
+    "out", "lse", "path", "path_len", "next_token" -> pinned host tensor."""
+
+    def __init__(self, make_verifier, chunks=4):
+        self.make_verifier = make_verifier
+        self.chunks = max(1, int(chunks))
+        self.verifiers = None
+        self._streams = None
+
+    def __call__(self, x_dev: StepInputs, host_in: dict, host_out: dict, stream=None):
+        import torch
+
+        main = stream if stream is not None else torch.cuda.current_stream()
+        b = x_dev.parent.shape[0]
+        n = min(self.chunks, b)
+        if self.verifiers is None or len(self.verifiers) != n:
+            self.verifiers = [self.make_verifier() for _ in range(n)]
+            self.accs = [None] * n
+        if self._streams is None or self._streams[0].device != main.device:
+            self._streams = (torch.cuda.Stream(device=main.device), torch.cuda.Stream(device=main.device))
+        h2d, d2h = self._streams
+        bounds = [(b * c // n, b * (c + 1) // n) for c in range(n)]
+        h2d.wait_stream(main)  # the previous step's users of the input buffers are done
+        d2h.wait_stream(main)
+        last = None
+        for c, (b0, b1) in enumerate(bounds):
+            with torch.cuda.stream(h2d):
+                for k, v in host_in.items():
+                    getattr(x_dev, k)[b0:b1].copy_(v[b0:b1], non_blocking=True)
+                landed = torch.cuda.Event()
+                landed.record(h2d)
+            main.wait_event(landed)
+            out, lse, acc, _ = self.verifiers[c].step(_slice_inputs(x_dev, b0, b1), stream=main)
+            done = torch.cuda.Event()
+            done.record(main)
+            d2h.wait_event(done)
+            res = {"out": out, "lse": lse, "path": acc.path, "path_len": acc.path_len, "next_token": acc.next_token}
+            with torch.cuda.stream(d2h):
+                for k, t in host_out.items():
+                    t[b0:b1].copy_(res[k], non_blocking=True)
+            last = (out, lse, acc)
+            self.accs[c] = acc
+        main.wait_stream(d2h)
+        main.wait_stream(h2d)
+        return last
+
+    def check(self):
+        """Raise the reference exceptions for every chunk's device error words."""
+        for v, a in zip(self.verifiers or (), self.accs or ()):
+            v.check(acc=a)

@@ -362,6 +362,7 @@ __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int
 // ---------------------------------------------------------------------------
 // stochastic
 // ---------------------------------------------------------------------------
+constexpr int kValSmsPer148 = 50;      // SMs of 148 the persistent validation scan takes beside the lazy chain
 constexpr int kStThreads = 1024;       // one row per SM: its L2-resident working set (148 x 0.5 MB) fits the 126 MB L2
 constexpr int kHistBins = 4096;        // width 1/64 log2 unit below the row max (64 log2 units)
 constexpr float kHistScale = 64.0f;
@@ -1926,9 +1927,23 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
   sattr[1].val.clusterDim.x = st_split > 1 ? st_split : 2;
   sattr[1].val.clusterDim.y = 1;
   sattr[1].val.clusterDim.z = 1;
-  auto stats_launch = [&](dim3 grid, const int32_t *rows) {
+  // the first level (every sequence at its root: 2 B rows) without the row
+  // split when its 4 B split CTAs would need more than two waves of the SMs
+  // the concurrent validation scan leaves (50 of 148 taken): C5 (B 64) 587 ->
+  // 578 us; C3 stochastic (B 32) keeps the split (956 vs 973 us without).
+  // SDB_ST_SPLIT0 = 1 / 2 forces it.
+  static const int split_lvl0_env = [] {
+    const char *e = getenv("SDB_ST_SPLIT0");
+    return e ? atoi(e) : 0;
+  }();
+  int n_sms_dev = 148, dev_id = 0;
+  cudaGetDevice(&dev_id);
+  cudaDeviceGetAttribute(&n_sms_dev, cudaDevAttrMultiProcessorCount, dev_id);
+  const int free_sms = n_sms_dev - (n_sms_dev * sdb::kValSmsPer148 + 74) / 148;
+  const int split_lvl0 = split_lvl0_env ? split_lvl0_env : (4 * batch > 2 * free_sms ? 1 : 2);
+  auto stats_launch = [&](dim3 grid, const int32_t *rows, bool split_ok = true) {
     scfg.gridDim = grid;
-    if (rows && split_rows) {
+    if (rows && split_rows && split_ok) {
       scfg.gridDim.x = st_split * grid.x;
       scfg.attrs = sattr;
       scfg.numAttrs = 2;
@@ -1980,7 +1995,7 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
   sdb::lazy_walk_init_kernel<<<(batch + 127) / 128, 128, 0, s>>>(n_rows, batch, lw, cur_rows);
   SDB_CHECK_LAUNCH();
   for (int lvl = 0; lvl < levels; ++lvl) {
-    stats_launch(dim3(1, batch, 2), cur_rows);
+    stats_launch(dim3(1, batch, 2), cur_rows, lvl > 0 || split_lvl0 > 1);
     SDB_CHECK_LAUNCH();
     cudaError_t le = walk_launch();
     if (le != cudaSuccess) return sdb::record_cuda_error(le);
@@ -2123,7 +2138,7 @@ extern "C" int sdb_stochastic_validate(const float *target_logits, const float *
     int dev = 0, n_sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-    persist_sms = (n_sms * 50 + 74) / 148;
+    persist_sms = (n_sms * sdb::kValSmsPer148 + 74) / 148;
   }
   if (persist_sms > 0 && !allowed) {
     static bool attr_set = false;

@@ -362,7 +362,7 @@ __global__ void greedy_walk_kernel(const long long *__restrict__ keys, const int
 // ---------------------------------------------------------------------------
 // stochastic
 // ---------------------------------------------------------------------------
-constexpr int kValSmsPer148 = 50;      // SMs of 148 the persistent validation scan takes beside the lazy chain
+constexpr int kValSmsPer148 = 52;      // SMs of 148 the persistent validation scan takes beside the lazy chain
 constexpr int kStThreads = 1024;       // one row per SM: its L2-resident working set (148 x 0.5 MB) fits the 126 MB L2
 constexpr int kHistBins = 4096;        // width 1/64 log2 unit below the row max (64 log2 units)
 constexpr float kHistScale = 64.0f;
@@ -1929,7 +1929,7 @@ static int accept_stochastic_impl(const float *target_logits, const float *draft
   sattr[1].val.clusterDim.z = 1;
   // the first level (every sequence at its root: 2 B rows) without the row
   // split when its 4 B split CTAs would need more than two waves of the SMs
-  // the concurrent validation scan leaves (50 of 148 taken): C5 (B 64) 587 ->
+  // the concurrent validation scan leaves (52 of 148 taken): C5 (B 64) 587 ->
   // 578 us; C3 stochastic (B 32) keeps the split (956 vs 973 us without).
   // SDB_ST_SPLIT0 = 1 / 2 forces it.
   static const int split_lvl0_env = [] {
@@ -2123,11 +2123,13 @@ extern "C" int sdb_stochastic_validate(const float *target_logits, const float *
   if (batch == 0) return SDB_OK;
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);
-  // default: the persistent scan on 50 of 148 SMs (scaled to the device),
-  // the lazy chain on the rest -- C5 912 -> 586 us, C3 stochastic 1142 ->
-  // ~970 us.  K swept 36..62 on the flat-stream scan (same box, C5 us):
+  // default: the persistent scan on 52 of 148 SMs (scaled to the device),
+  // the lazy chain on the rest -- C5 912 -> ~570 us, C3 stochastic 1142 ->
+  // ~960 us.  K swept 36..62 on the flat-stream scan (same box, C5 us):
   // 38 703, 42 644, 44 624, 46 603, 48 685 (the chain's clusters place
-  // badly), 50 586, 52 593, 54 616, 56 609-618, 60 633; flat at B <= 32.
+  // badly), 50 586, 52 593, 54 616, 56 609-618, 60 633; with the unsplit
+  // first level: 46 603, 50 578, 52 565-572, 54 592-599, 58 600-606; flat
+  // at B <= 32.
   // SDB_VALIDATE_SMS=0 restores the one-row low-priority CTAs
   static const int persist_env = [] {
     const char *e = getenv("SDB_VALIDATE_SMS");

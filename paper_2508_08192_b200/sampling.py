@@ -400,7 +400,7 @@ class StochasticAcceptor:
     ``lazy``: only the rows the MSS walk visits are reduced, one tree level
     per launch pair, while a validation scan of every row (the reference's
     error behaviour) runs concurrently on a side stream (a persistent kernel on
-    50 of 148 SMs; the chain takes the rest); "auto" picks it from 20
+    52 of 148 SMs; the chain takes the rest); "auto" picks it from 20
     sequences up.  ``levels`` (tree depth + 1) must be given when
     capturing a CUDA graph.  Results are identical either way."""
 
@@ -452,7 +452,7 @@ class StochasticAcceptor:
                 o["uni"] = torch.empty((b, r), dtype=torch.float64, device=dev)
             uniforms = device_uniforms(seeds, steps, r, out=o["uni"], stream=stream)
         n_words = allowed.shape[-1] if allowed is not None else 0
-        # the lazy walk + concurrent validation scan (persistent, on 50 of
+        # the lazy walk + concurrent validation scan (persistent, on 52 of
         # 148 SMs) costs ~440 us at B 16-20 and grows slowly; reducing every
         # row costs ~20 us per sequence (tools/lazy_sweep.py, V 128k,
         # tree64): lazy wins from about 20 sequences (B 16: 387 eager / 436

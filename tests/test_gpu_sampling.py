@@ -492,7 +492,7 @@ def test_fsm_dead_row_raises_flag():
 @pytest.mark.parametrize("V", [4096, 4099])
 def test_lazy_validation_scan_error_semantics(V, scan_sms, monkeypatch):
     """The lazy walk reduces only the rows it visits; the validation scan
-    (persistent on 50 of 148 SMs by default, SDB_VALIDATE_SMS=0: one-row
+    (persistent on 52 of 148 SMs by default, SDB_VALIDATE_SMS=0: one-row
     CTAs) must still raise exactly where the reference does: target_dist of
     EVERY tree row and the draft q of every PARENT row (engine.py:474-475,
     numcore.py:47-48) -- a NaN in a draft leaf row or past a sequence's
